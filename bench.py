@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path (BASELINE.json metric: "BP3 diffusion GDOF/s per GPU
+vs p; CG [DOFs x iters]/s at 1/2/4/8 B200").
+
+One *step* = one CG iteration of the BP3 diffusion operator (SURVEY.md §8(a)
+rows a4-a10: fused apply + dot + fused updates), p = 5, Gauss Q = p+2,
+curvilinear unit cube, homogeneous Dirichlet, manufactured RHS; 62^3 elements
+= 30,080,231 dofs per GPU (configs[2] size; weak scaling stacks one 62^3 slab
+per GPU in z, exchanged over NCCL).  ``value`` = global DOFs x iterations / s
+over all GPUs (G[DOF*it]/s), device-timed with CUDA events, max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--p 5] [--sweep]
+    python bench.py --impl reference ...   # the CPU oracle (rank 0 only)
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BP3 diffusion GDOF/s per GPU vs p; CG [DOFs x iters]/s at 1/2/4/8 B200"
+UNIT = "GDOF*it/s"
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def alg_bytes(nx, ny, nz, p, Q, nc):
+    """8 N_L (read x) + 8 N_L (write y) + 8 n_c E Q^3 (qdata)."""
+    N = (p * nx + 1) * (p * ny + 1) * (p * nz + 1)
+    E = nx * ny * nz
+    return 16 * N + 8 * nc * E * Q ** 3, N, E
+
+
+def brick_direct_points(nx, ny, nz, p, B):
+    """Lattice points NOT on an interior brick face (written by the brick kernel
+    itself; the rest go through the fix-up kernel)."""
+    def axis(n, b):
+        N = p * n + 1
+        nb = -(-n // b)
+        return N - (nb - 1)
+    return axis(nx, B[0]) * axis(ny, B[1]) * axis(nz, B[2])
+
+
+SHAPES = {2: (8, 4, 4), 3: (4, 4, 2), 4: (4, 2, 2), 5: (2, 2, 2), 6: (2, 2, 2), 7: (2, 2, 1),
+          8: (2, 2, 1), 9: (2, 1, 1)}  # fused_impl.cuh Shape<P1>
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock/throttle sampling (NVML) during the timed region."""
+
+    def __init__(self, device: int, period=0.02):
+        self.device, self.period = device, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            names = {
+                "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+                "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+                "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+                "display_clock_setting": 0x100}
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for k, v in names.items():
+                            if r & v and k != "gpu_idle":
+                                self.reasons.add(k)
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception:
+            self._t = None
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def cpu_info():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ----------------------------------------------------------------------------- reference arm
+def oracle_cg_sample(p, n, iters, warmup=0):
+    """The CPU oracle (brute-force EA operator + textbook CG) on a bounded sample
+    of the BP3 workload.  Returns (dofs*iters/s, setup_s, cg_s, dofs, threads)."""
+    import oracle as O
+    om = O.Mesh(n, n, n, p, alpha=0.1)
+    t0 = time.perf_counter()
+    Ae = O.element_matrices(om, O.DIFFUSION, O.GAUSS)
+    b = O.rhs(om, O.DIFFUSION, O.GAUSS, bc=1)
+    t1 = time.perf_counter()
+    if warmup:
+        O.cg(b, m=om, Ae=Ae, bc=1, max_iter=warmup, fixed_iters=True)
+    t2 = time.perf_counter()
+    O.cg(b, m=om, Ae=Ae, bc=1, max_iter=iters, fixed_iters=True)
+    t3 = time.perf_counter()
+    return om.n_dofs * iters / (t3 - t2), t1 - t0, t3 - t2, om.n_dofs, O.num_threads()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    p, n = args.p, args.ref_n
+    val, setup_s, cg_s, dofs, threads = oracle_cg_sample(p, n, args.steps, args.warmup)
+    v = val / 1e9
+    sample = (f"BP3 p={p} on {n}^3 elements ({dofs} dofs), brute-force EA setup {setup_s:.1f} s "
+              f"(untimed), {args.steps} timed fixed CG iterations ({cg_s:.2f} s); CPU {cpu_info()}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * cg_s / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"bp3_p{p}_oracle_sample_{n}^3",
+                                        "p": p, "elements": n ** 3, "dofs": dofs},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2402_15940_b200 as hf
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = hf.Comm.from_torch_distributed()
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    p = args.p
+    n = args.n or int(round(311.0 / p))
+    nx = ny = n
+    nz = n * world
+    Q = p + 2
+    mesh = hf.Mesh(nx, ny, nz, p, alpha=0.1, comm=comm)
+    op = hf.Operator(mesh, kind=hf.DIFFUSION, rule=hf.GAUSS, bc=hf.BC_DIRICHLET)
+    b = op.rhs()
+    x = torch.zeros(mesh.n_local, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up: W CG iterations
+    op.cg(b, x, max_iter=max(args.warmup, 1), fixed_iters=True)
+
+    # ---- timed: exactly K CG iterations (one hofem_cg call in fixed-iteration mode;
+    # its initial residual apply is inside the timed region and not counted)
+    x.zero_()
+    barrier()
+    hf.launch_count_reset()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        st, stats, _ = op.cg(b, x, max_iter=args.steps, fixed_iters=True)
+        e1.record(stream)
+        barrier()
+    launches = hf.launch_count()
+    t_cg = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    assert stats.iterations == args.steps
+    n_global = mesh.n_global
+    value = n_global * args.steps / t_cg / 1e9
+
+    # ---- apply-only: GDOF/s per GPU + live per-kernel durations (profiling hooks)
+    xa = mesh.random(1)
+    ya = torch.empty_like(xa)
+    for _ in range(3):
+        op.apply(xa, ya)
+    napply = args.apply_reps
+    barrier()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for _ in range(napply):
+        op.apply(xa, ya)
+    a1.record(stream)
+    barrier()
+    t_apply = max_over_ranks(a0.elapsed_time(a1) / 1e3 / napply)
+    hf.profile_enable(True)
+    for _ in range(napply):
+        op.apply(xa, ya)
+    prof = hf.profile_read()
+    hf.profile_enable(False)
+    t_brick = prof.brick_ms / 1e3 / max(prof.brick_launches, 1)
+    t_fix = prof.fixup_ms / 1e3 / max(prof.fixup_launches, 1)
+    nzl = n
+    bytes_apply, N_l, E_l = alg_bytes(nx, ny, nzl, p, Q, 6)
+    nd = brick_direct_points(nx, ny, nzl, p, SHAPES[p + 1])
+    bytes_brick = 8 * N_l + 8 * 6 * E_l * Q ** 3 + 8 * nd
+    peak, peak_src = load_peaks()
+    achieved = bytes_brick / t_brick / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"bp3_p{p}_n{n}")
+        except Exception:
+            traffic = None
+
+    # ---- e2e: public API with host buffers (H2D b, solve, D2H x) per solve
+    e2e = None
+    if not args.no_e2e:
+        hb = torch.empty(mesh.n_local, dtype=torch.float64, pin_memory=True)
+        hb.copy_(b.cpu())
+        hx = torch.empty(mesh.n_local, dtype=torch.float64, pin_memory=True)
+        db = torch.empty_like(b)
+        it = args.e2e_iters
+        reps = args.e2e_reps
+        barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(reps):
+            db.copy_(hb, non_blocking=True)
+            x.zero_()
+            op.cg(db, x, max_iter=it, fixed_iters=True)
+            hx.copy_(x, non_blocking=True)
+        s1.record(stream)
+        barrier()
+        t_e2e = max_over_ranks(s0.elapsed_time(s1) / 1e3)
+        e2e = {"value": n_global * it * reps / t_e2e / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 8 * mesh.n_local, "d2h_bytes_per_step": 8 * mesh.n_local,
+               "step": f"one hofem_cg solve of {it} fixed iterations incl. H2D of b and D2H of x "
+                       f"(per rank); {reps} solves timed"}
+
+    # ---- optional sweep (apply GDOF/s per GPU vs p, fused vs unfused, BP1/BP5)
+    sweep = run_sweep(args, hf, torch, stream) if args.sweep else None
+
+    # ---- CPU baseline: rank 0, N = 1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, setup_s, cg_s, dofs, threads = oracle_cg_sample(p, args.ref_n, args.ref_iters)
+        cpu = {"value": v / 1e9, "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": f"BP3 p={p} on {args.ref_n}^3 elements ({dofs} dofs): brute-force EA "
+                         f"setup {setup_s:.1f} s (excluded), {args.ref_iters} fixed CG iterations "
+                         f"in {cg_s:.2f} s; CPU {cpu_info()}"}
+
+    clocks = clk.summary()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_cg / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"bp3_p{p}_{nx}x{ny}x{n}_per_gpu", "p": p, "q": Q,
+                       "elements_per_gpu": nx * ny * n, "dofs_global": n_global,
+                       "dofs_per_gpu": N_l, "bc": "dirichlet", "mesh": "curvilinear alpha=0.1",
+                       "parallelism": f"z-slab x{world} (NCCL plane exchange + allreduce)",
+                       "l2": "inputs larger than L2 (qdata 3.9 GB/GPU, vectors 240 MB)"},
+            "apply_gdof_s_per_gpu": N_l / t_apply / 1e9,
+            "apply_ms": 1e3 * t_apply,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": f"fused_brick<DIFF,P1={p + 1},Q={Q}>",
+                         "alg_bytes_per_launch": bytes_brick, "launch_ms": 1e3 * t_brick,
+                         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
+                         "apply_frac": bytes_apply / t_apply / 1e9 / peak,
+                         "fixup_ms": 1e3 * t_fix},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        if sweep is not None:
+            line["sweep"] = sweep
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_sweep(args, hf, torch, stream):
+    """Apply throughput per GPU vs p (configs 2-4 of BASELINE.json)."""
+    peak, _ = load_peaks()
+    out = []
+    reps = 20
+    for bench, kind, rule, ps in (("bp3", hf.DIFFUSION, hf.GAUSS, range(1, 9)),
+                                  ("bp5", hf.DIFFUSION, hf.GLL, range(4, 9)),
+                                  ("bp1", hf.MASS, hf.GAUSS, range(1, 9))):
+        for p in ps:
+            n = int(round((99.0 if bench == "bp1" else 311.0) / p))
+            Q = p + 2 if rule == hf.GAUSS else p + 1
+            nc = 1 if kind == hf.MASS else 6
+            m = hf.Mesh(n, n, n, p, alpha=0.1)
+            op = hf.Operator(m, kind=kind, rule=rule)
+            x = m.random(3)
+            y = torch.empty_like(x)
+            res = {"bench": bench, "p": p, "n": n, "dofs": m.n_local}
+            for name, fn in (("fused", op.apply), ("unfused", op.apply_unfused)):
+                if name == "unfused" and bench == "bp1":
+                    continue
+                for _ in range(3):
+                    fn(x, y)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(reps):
+                    fn(x, y)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                t = e0.elapsed_time(e1) / 1e3 / reps
+                bts, N, E = alg_bytes(n, n, n, p, Q, nc)
+                res[name] = {"gdof_s": N / t / 1e9, "ms": 1e3 * t,
+                             "alg_gbs": bts / t / 1e9, "frac": bts / t / 1e9 / peak}
+            op.close()
+            m.close()
+            torch.cuda.empty_cache()
+            out.append(res)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--p", type=int, default=5)
+    ap.add_argument("--n", type=int, default=0, help="elements per axis per GPU (0: round(311/p))")
+    ap.add_argument("--apply-reps", type=int, default=50)
+    ap.add_argument("--e2e-iters", type=int, default=100)
+    ap.add_argument("--e2e-reps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-n", type=int, default=6, help="oracle sample: elements per axis")
+    ap.add_argument("--ref-iters", type=int, default=20)
+    ap.add_argument("--sweep", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,187 @@
+/*
+ * hofem.h -- C ABI of the B200-native matrix-free high-order FEM hot path of
+ * arXiv 2402.15940 ("High-performance finite elements with MFEM"):
+ * partial-assembly (PA) sum-factorization operator actions on structured
+ * curvilinear high-order hexahedral meshes -- the CEED bake-off mass (BP1) and
+ * diffusion (BP3, BP5) actions y = R^T B^T D B R x -- and the CG solve built on
+ * them, slab-partitioned over up to 8 GPUs with NCCL.
+ *
+ * Citations are PAPER.md line numbers (section in parentheses) and the
+ * DESIGN.md readings R1-R14 (= SURVEY.md §8(c)) for everything the paper leaves
+ * open.  Operator decomposition: A = P^T G^T B^T D B G P (PAPER.md:595,
+ * fig_feod, §3.5); this library calls the paper's element restriction "G" R, and
+ * its P is the z-slab interface exchange.
+ *
+ * Conventions (all entry points):
+ *  - Every vector argument is a DEVICE pointer to contiguous FP64 owned by the
+ *    caller (e.g. a torch.float64 CUDA tensor's data_ptr()).  Vectors are
+ *    rank-local L-vectors of length n_local, lexicographic with x fastest:
+ *    l = I + Nx*(J + Ny*K) (reading R3).  The two z-interface planes are
+ *    duplicated on both neighbouring ranks and kept bitwise identical (R9).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Everything is stream-ordered and asynchronous, except the calls marked
+ *    SYNC, which synchronize `stream` before returning.
+ *  - Opaque handles are owned by the library; each destroy frees exactly what
+ *    the matching create allocated.  The library never frees caller buffers.
+ *  - x and y must not alias; y is fully overwritten.
+ *  - On error the outputs are unspecified; handles stay valid except after
+ *    HOFEM_ERR_CUDA / HOFEM_ERR_NCCL.  hofem_last_error() gives a message.
+ *  - There is no CPU fallback: every step of every call runs in this library's
+ *    CUDA kernels (sm_100a).  Without a usable CUDA device, calls that touch the
+ *    device return HOFEM_ERR_CUDA.
+ */
+#ifndef HOFEM_H
+#define HOFEM_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HOFEM_OK = 0,
+  HOFEM_ERR_ARG = 1,       /* precondition violated: p<1 or p>8, n<1, NULL, x==y, bad rule/kind */
+  HOFEM_ERR_MESH = 2,      /* detJ <= 0 at some quadrature point */
+  HOFEM_ERR_CUDA = 3,      /* CUDA runtime error (message in hofem_last_error) */
+  HOFEM_ERR_NCCL = 4,      /* NCCL error */
+  HOFEM_ERR_OOM = 5,       /* device allocation failed */
+  HOFEM_ERR_BREAKDOWN = 6, /* CG: p^T A p <= 0 */
+  HOFEM_NOT_CONVERGED = 7  /* CG: max_iter reached, outputs valid */
+} hofem_status;
+
+/* Thread-local message describing the last non-OK status (never NULL). */
+const char* hofem_last_error(void);
+
+/* ---------------------------------------------------------------- comm (P) */
+/* NCCL communicator for the z-slab partition (§2.3: the
+ * parallel operator P^T A P).  hofem_comm_unique_id writes the
+ * 128-byte ncclUniqueId on rank 0; the caller broadcasts it (torch.distributed)
+ * and every rank calls hofem_comm_init with its rank and CUDA device. */
+hofem_status hofem_comm_unique_id(void* nccl_id_out /* 128 bytes, host */);
+hofem_status hofem_comm_init(const void* nccl_id /* 128 B host */, int rank, int nranks,
+                             int device, void** comm_out);
+void hofem_comm_destroy(void* comm);
+
+/* ---------------------------------------------------------------- mesh (a1) */
+/* Structured nx*ny*nz_global hex mesh of [0,extent0]x[0,extent1]x[0,extent2],
+ * isoparametric degree p (geometry order = p), nodes at GLL
+ * points mapped by the smooth deformation Phi of reading R4 with amplitude
+ * alpha (0 = affine box).  With comm != NULL, rank r gets the element layers
+ * ez in [r*nz/R, (r+1)*nz/R) (R must divide nz_global) and its L-vector covers
+ * lattice planes K in [p*z0, p*z1] (reading R9). 1 <= p <= 8. */
+typedef struct {
+  int nx, ny, nz_global, p;
+  double extent[3];
+  double alpha;
+} hofem_mesh_desc;
+
+typedef struct {
+  long long n_local;    /* L-vector length on this rank = Nx*Ny*Nz_local */
+  long long n_owned;    /* dofs this rank owns (dot products / counting, R8-R9) */
+  long long n_global;   /* global dof count (p*nx+1)(p*ny+1)(p*nz+1) */
+  long long elems_local;
+  long long plane;      /* Nx*Ny, the size of one z lattice plane */
+  int rank, nranks, z0, nz_local;
+} hofem_mesh_info;
+
+hofem_status hofem_mesh_create(const hofem_mesh_desc* desc, void* comm /* NULL => 1 rank */,
+                               void* stream, void** mesh_out);
+hofem_status hofem_mesh_info_get(const void* mesh, hofem_mesh_info* info_out);
+/* Nodal coordinates: xyz[c*n_local + l], c = 0,1,2 (device, 3*n_local FP64). */
+hofem_status hofem_mesh_coords(const void* mesh, double* xyz, void* stream);
+void hofem_mesh_destroy(void* mesh);
+
+/* ---------------------------------------------------------- operator (a2-a9) */
+typedef enum { HOFEM_MASS = 1, HOFEM_DIFFUSION = 2 } hofem_kind;
+/* Quadrature (reading R2): GAUSS Q = p+2 (BP1, BP3); GLL Q = p+1 collocated with
+ * the nodes, so B1d = I (BP5).  q_override != 0 selects another Q in [1, 16]
+ * (Q = p+1 with GAUSS, Q = p+2 with GLL also use the fused kernels). */
+typedef enum { HOFEM_GAUSS = 1, HOFEM_GLL = 2 } hofem_rule;
+typedef enum { HOFEM_BC_NONE = 0, HOFEM_BC_DIRICHLET = 1 } hofem_bc;
+
+/* SYNC.  Build the partially assembled operator: only the quadrature-point data
+ * D is stored (§2.2 "Partial Assembly"): mass W*detJ, diffusion
+ * the symmetric W adj(J) adj(J)^T / detJ (6 entries [00,01,02,11,12,22]),
+ * layout [E][n_c][Q^3] (R3).  Returns HOFEM_ERR_MESH if detJ <= 0 anywhere.
+ * bc = DIRICHLET applies the homogeneous whole-boundary convention of R6:
+ * z = x; z[ess] = 0; y = A z; y[ess] = x[ess]. */
+hofem_status hofem_op_create(void* mesh, hofem_kind kind, hofem_rule rule, int q_override,
+                             hofem_bc bc, void* stream, void** op_out);
+
+/* y = P^T R^T B^T D B R P x: the fused path.  One sm_100a kernel
+ * per element brick does gather (R), the 1D B/G contractions dimension by
+ * dimension, the pointwise D, the transposed contractions and the in-brick
+ * deterministic sum; a fix-up kernel sums brick-interface dofs in fixed order;
+ * with >1 rank the interface planes are then exchanged over NCCL (P).
+ * Bitwise deterministic run to run. */
+hofem_status hofem_op_apply(void* op, const double* x, double* y, void* stream);
+
+/* Same operator, unfused reference path: gather kernel (R through the l2e
+ * table) -> element kernel -> deterministic scatter through precomputed
+ * transposed offsets (R^T, ascending (e, i) order). */
+hofem_status hofem_op_apply_unfused(void* op, const double* x, double* y, void* stream);
+
+/* Device pointer to the stored qdata (owned by op) and its length E*n_c*Q^3. */
+hofem_status hofem_op_qdata(const void* op, const double** qdata, long long* count);
+/* Q (1D quadrature points) actually used by op. */
+hofem_status hofem_op_nq1d(const void* op, int* q_out);
+
+/* b_i = sum_e sum_q W_q detJ f(x(xi_q)) phi_i(xi_q) (reading R11): diffusion
+ * f = 3 pi^2 prod sin(pi x_j), mass f = prod sin(pi x_j); b[ess] = 0 when op has
+ * Dirichlet BCs.  Interface planes are summed across ranks. */
+hofem_status hofem_rhs_manufactured(void* op, double* b, void* stream);
+
+/* Counter-based random L-vector of reading R12, indexed by the GLOBAL dof:
+ * x_g = 2*((splitmix64(seed + (g+1)*0x9E3779B97F4A7C15) >> 11) * 2^-53) - 1. */
+hofem_status hofem_fill_random(const void* mesh, unsigned long long seed, double* x, void* stream);
+
+void hofem_op_destroy(void* op);
+
+/* -------------------------------------------------------------------- CG (a10) */
+typedef struct {
+  int iterations;        /* iterations performed */
+  int converged;         /* 1 if ||r_k|| <= rel_tol ||r_0|| (or fixed count done) */
+  double r0_norm;        /* ||r_0||_2 over owned dofs, all ranks */
+  double final_rel_res;  /* ||r_k|| / ||r_0|| */
+} hofem_cg_stats;
+
+/* SYNC.  Unpreconditioned CG (§2.1; reading R7):
+ * r0 = b - A x0, p = r0; per iteration Ap = A p (fused apply), pAp = p.Ap
+ * (owned dofs, NCCL allreduce), alpha = rr/pAp, x += alpha p, r -= alpha Ap,
+ * rr' = r.r (fused with the update), beta = rr'/rr, p = r + beta p.  alpha and
+ * beta stay on the device.  Stops when ||r|| <= rel_tol ||r0|| (tested every
+ * check_every iterations: the only device->host copy), or runs exactly max_iter
+ * iterations when fixed_iters = 1.  x: in x0, out the iterate.
+ * rr_history (host, nullable, length max_iter+1) receives r_k.r_k.
+ * Returns HOFEM_NOT_CONVERGED if max_iter was hit in tolerance mode,
+ * HOFEM_ERR_BREAKDOWN if pAp <= 0. */
+hofem_status hofem_cg(void* op, const double* b, double* x, double rel_tol, int max_iter,
+                      int fixed_iters, int check_every, double* rr_history,
+                      hofem_cg_stats* stats, void* stream);
+
+/* SYNC.  out = sum over owned dofs of a_l*b_l, allreduced over ranks; the
+ * reduction order is fixed (deterministic). */
+hofem_status hofem_dot(const void* mesh, const double* a, const double* b, double* out_host,
+                       void* stream);
+
+/* Kernel timing hooks for the bench's roofline figure.  When enabled, the
+ * library records CUDA events on the launching stream around every fused brick
+ * kernel and every brick fix-up kernel; hofem_profile_read synchronizes on
+ * those events, returns the summed device durations and clears the record. */
+typedef struct {
+  long long brick_launches;
+  double brick_ms;
+  long long fixup_launches;
+  double fixup_ms;
+} hofem_profile_stats;
+hofem_status hofem_profile_enable(int enable);
+hofem_status hofem_profile_read(hofem_profile_stats* out);
+
+/* Number of kernel launches the library issued since the last reset (for the
+ * bench's gpu_launches claim); counts every <<<>>> launch of this library. */
+long long hofem_launch_count(void);
+void hofem_launch_count_reset(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HOFEM_H */

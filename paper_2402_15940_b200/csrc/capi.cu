@@ -1,0 +1,269 @@
+// capi.cu -- the C ABI declared in include/hofem.h: argument checking, handle
+// lifetime, error reporting, and the host-side orchestration of the kernels.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+
+#include "internal.h"
+
+namespace hofem {
+
+namespace {
+thread_local char g_err[512] = "no error";
+std::atomic<long long> g_launches{0};
+}  // namespace
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+hofem_status cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return HOFEM_OK;
+  set_error("%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+  if (e == cudaErrorMemoryAllocation) return HOFEM_ERR_OOM;
+  return HOFEM_ERR_CUDA;
+}
+
+void count_launch(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+hofem_status profile_enable(int on);
+hofem_status profile_read(hofem_profile_stats* out);
+
+hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int max_iter,
+                      int fixed_iters, int check_every, double* rr_history,
+                      hofem_cg_stats* stats, cudaStream_t s);
+
+hofem_status apply_any(Op* op, const double* x, double* y, cudaStream_t s) {
+  if (fused_supported(op)) return apply_fused(op, x, y, s);
+  return apply_unfused(op, x, y, s);
+}
+
+namespace {
+
+template <class T>
+hofem_status dalloc(T** p, long long n, const char* what) {
+  if (cudaMalloc(p, sizeof(T) * (n > 0 ? n : 1)) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("%s: out of device memory (%lld elements)", what, n);
+    return HOFEM_ERR_OOM;
+  }
+  return HOFEM_OK;
+}
+
+void free_mesh(Mesh* m) {
+  if (!m) return;
+  cudaFree(m->d_xi); cudaFree(m->d_coords);
+  cudaFree(m->d_l2e); cudaFree(m->d_toff); cudaFree(m->d_tidx);
+  cudaFree(m->d_partials); cudaFree(m->d_counter); cudaFree(m->d_scalars);
+  cudaFree(m->d_recv); cudaFree(m->d_send);
+  delete m;
+}
+
+void free_op(Op* op) {
+  if (!op) return;
+  cudaFree(op->d_B); cudaFree(op->d_G); cudaFree(op->d_qdata);
+  cudaFree(op->d_ein); cudaFree(op->d_eout); cudaFree(op->d_bbuf);
+  cudaFree(op->d_r); cudaFree(op->d_p); cudaFree(op->d_Ap); cudaFree(op->d_cg);
+  delete op;
+}
+
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace
+}  // namespace hofem
+
+using namespace hofem;
+
+extern "C" {
+
+const char* hofem_last_error(void) { return g_err; }
+
+hofem_status hofem_profile_enable(int enable) { return profile_enable(enable); }
+hofem_status hofem_profile_read(hofem_profile_stats* out) {
+  if (!out) { set_error("hofem_profile_read: NULL"); return HOFEM_ERR_ARG; }
+  return profile_read(out);
+}
+
+long long hofem_launch_count(void) { return g_launches.load(); }
+void hofem_launch_count_reset(void) { g_launches.store(0); }
+
+hofem_status hofem_mesh_create(const hofem_mesh_desc* d, void* comm, void* stream,
+                               void** mesh_out) {
+  if (!d || !mesh_out) { set_error("hofem_mesh_create: NULL argument"); return HOFEM_ERR_ARG; }
+  if (d->p < 1 || d->p > kMaxP || d->nx < 1 || d->ny < 1 || d->nz_global < 1 ||
+      !(d->extent[0] > 0) || !(d->extent[1] > 0) || !(d->extent[2] > 0)) {
+    set_error("hofem_mesh_create: need 1<=p<=%d, n>=1, extents>0", kMaxP);
+    return HOFEM_ERR_ARG;
+  }
+  Comm* c = static_cast<Comm*>(comm);
+  const int R = c ? c->nranks : 1, r = c ? c->rank : 0;
+  if (d->nz_global % R != 0) {
+    set_error("hofem_mesh_create: nranks=%d must divide nz_global=%d", R, d->nz_global);
+    return HOFEM_ERR_ARG;
+  }
+  int dev = 0;
+  HOFEM_CUDA(cudaGetDevice(&dev));
+  auto* m = new Mesh();
+  m->desc = *d;
+  m->comm = c;
+  m->rank = r; m->nranks = R;
+  m->p = d->p; m->P1 = d->p + 1;
+  m->nx = d->nx; m->ny = d->ny; m->nzl = d->nz_global / R; m->z0 = r * m->nzl;
+  m->Nx = (long long)d->p * d->nx + 1;
+  m->Ny = (long long)d->p * d->ny + 1;
+  m->Nzl = (long long)d->p * m->nzl + 1;
+  m->NzG = (long long)d->p * d->nz_global + 1;
+  m->plane = m->Nx * m->Ny;
+  m->n_local = m->plane * m->Nzl;
+  m->n_owned = (r == R - 1) ? m->n_local : m->n_local - m->plane;
+  m->n_global = m->plane * m->NzG;
+  m->elems = (long long)d->nx * d->ny * m->nzl;
+  double xi[kMaxP + 1], w[kMaxP + 1];
+  gll_nodes_weights(d->p, xi, w);
+  hofem_status st = HOFEM_OK;
+#define CK(x) do { st = (x); if (st != HOFEM_OK) { free_mesh(m); return st; } } while (0)
+  CK(dalloc(&m->d_xi, m->P1, "mesh"));
+  CK(dalloc(&m->d_coords, 3 * m->n_local, "mesh coords"));
+  CK(dalloc(&m->d_partials, 2 * kNumSMs + 64, "mesh"));
+  CK(dalloc(&m->d_counter, 4, "mesh"));
+  CK(dalloc(&m->d_scalars, 16, "mesh"));
+  if (R > 1) CK(dalloc(&m->d_recv, 2 * m->plane, "mesh planes"));
+  CK(cuda_status(cudaMemcpyAsync(m->d_xi, xi, sizeof(double) * m->P1, cudaMemcpyHostToDevice,
+                                 S(stream)), "mesh upload"));
+  CK(cuda_status(cudaMemsetAsync(m->d_counter, 0, 4 * sizeof(unsigned), S(stream)), "memset"));
+  CK(mesh_build_coords(m, S(stream)));
+  CK(cuda_status(cudaStreamSynchronize(S(stream)), "mesh_create sync"));
+#undef CK
+  *mesh_out = m;
+  return HOFEM_OK;
+}
+
+hofem_status hofem_mesh_info_get(const void* mesh, hofem_mesh_info* info) {
+  const Mesh* m = static_cast<const Mesh*>(mesh);
+  if (!m || !info) { set_error("hofem_mesh_info_get: NULL"); return HOFEM_ERR_ARG; }
+  info->n_local = m->n_local; info->n_owned = m->n_owned; info->n_global = m->n_global;
+  info->elems_local = m->elems; info->plane = m->plane;
+  info->rank = m->rank; info->nranks = m->nranks; info->z0 = m->z0; info->nz_local = m->nzl;
+  return HOFEM_OK;
+}
+
+hofem_status hofem_mesh_coords(const void* mesh, double* xyz, void* stream) {
+  const Mesh* m = static_cast<const Mesh*>(mesh);
+  if (!m || !xyz) { set_error("hofem_mesh_coords: NULL"); return HOFEM_ERR_ARG; }
+  HOFEM_CUDA(cudaMemcpyAsync(xyz, m->d_coords, sizeof(double) * 3 * m->n_local,
+                             cudaMemcpyDeviceToDevice, S(stream)));
+  return HOFEM_OK;
+}
+
+void hofem_mesh_destroy(void* mesh) { free_mesh(static_cast<Mesh*>(mesh)); }
+
+hofem_status hofem_op_create(void* mesh, hofem_kind kind, hofem_rule rule, int q_override,
+                             hofem_bc bc, void* stream, void** op_out) {
+  Mesh* m = static_cast<Mesh*>(mesh);
+  if (!m || !op_out) { set_error("hofem_op_create: NULL"); return HOFEM_ERR_ARG; }
+  if ((kind != HOFEM_MASS && kind != HOFEM_DIFFUSION) || (rule != HOFEM_GAUSS && rule != HOFEM_GLL) ||
+      (bc != HOFEM_BC_NONE && bc != HOFEM_BC_DIRICHLET) || q_override < 0 || q_override > kMaxQ) {
+    set_error("hofem_op_create: bad kind/rule/bc/q_override");
+    return HOFEM_ERR_ARG;
+  }
+  const int Q = q_override ? q_override : (rule == HOFEM_GAUSS ? m->p + 2 : m->p + 1);
+  if (rule == HOFEM_GLL && Q < 2) { set_error("hofem_op_create: GLL needs Q>=2"); return HOFEM_ERR_ARG; }
+  auto* op = new Op();
+  op->mesh = m; op->kind = kind; op->rule = rule; op->Q = Q; op->bc = bc;
+  op->nc = kind == HOFEM_MASS ? 1 : 6;
+  if (build_tables(m->p, Q, rule, &op->tab)) {
+    delete op;
+    set_error("hofem_op_create: 1D tables failed");
+    return HOFEM_ERR_ARG;
+  }
+  hofem_status st = HOFEM_OK;
+#define CK(x) do { st = (x); if (st != HOFEM_OK) { free_op(op); return st; } } while (0)
+  const int P1 = m->P1;
+  op->qcount = m->elems * op->nc * (long long)Q * Q * Q;
+  CK(dalloc(&op->d_B, Q * P1, "op tables"));
+  CK(dalloc(&op->d_G, Q * P1, "op tables"));
+  CK(dalloc(&op->d_qdata, op->qcount, "qdata"));
+  CK(cuda_status(cudaMemcpyAsync(op->d_B, op->tab.B, sizeof(double) * Q * P1,
+                                 cudaMemcpyHostToDevice, S(stream)), "upload B"));
+  CK(cuda_status(cudaMemcpyAsync(op->d_G, op->tab.G, sizeof(double) * Q * P1,
+                                 cudaMemcpyHostToDevice, S(stream)), "upload G"));
+  int bad = 0;
+  CK(build_qdata(op, S(stream), &bad));
+  if (bad) {
+    free_op(op);
+    set_error("hofem_op_create: detJ <= 0 at some quadrature point (invalid mesh)");
+    return HOFEM_ERR_MESH;
+  }
+#undef CK
+  *op_out = op;
+  return HOFEM_OK;
+}
+
+hofem_status hofem_op_apply(void* op_, const double* x, double* y, void* stream) {
+  Op* op = static_cast<Op*>(op_);
+  if (!op || !x || !y || x == y) { set_error("hofem_op_apply: NULL or aliased x/y"); return HOFEM_ERR_ARG; }
+  return apply_any(op, x, y, S(stream));
+}
+
+hofem_status hofem_op_apply_unfused(void* op_, const double* x, double* y, void* stream) {
+  Op* op = static_cast<Op*>(op_);
+  if (!op || !x || !y || x == y) { set_error("hofem_op_apply_unfused: NULL or aliased x/y"); return HOFEM_ERR_ARG; }
+  return apply_unfused(op, x, y, S(stream));
+}
+
+hofem_status hofem_op_qdata(const void* op_, const double** qdata, long long* count) {
+  const Op* op = static_cast<const Op*>(op_);
+  if (!op || !qdata || !count) { set_error("hofem_op_qdata: NULL"); return HOFEM_ERR_ARG; }
+  *qdata = op->d_qdata;
+  *count = op->qcount;
+  return HOFEM_OK;
+}
+
+hofem_status hofem_op_nq1d(const void* op_, int* q) {
+  const Op* op = static_cast<const Op*>(op_);
+  if (!op || !q) { set_error("hofem_op_nq1d: NULL"); return HOFEM_ERR_ARG; }
+  *q = op->Q;
+  return HOFEM_OK;
+}
+
+hofem_status hofem_rhs_manufactured(void* op_, double* b, void* stream) {
+  Op* op = static_cast<Op*>(op_);
+  if (!op || !b) { set_error("hofem_rhs_manufactured: NULL"); return HOFEM_ERR_ARG; }
+  HOFEM_TRY(build_rhs(op, b, S(stream)));
+  return exchange_planes(op, nullptr, b, S(stream));
+}
+
+hofem_status hofem_fill_random(const void* mesh, unsigned long long seed, double* x, void* stream) {
+  const Mesh* m = static_cast<const Mesh*>(mesh);
+  if (!m || !x) { set_error("hofem_fill_random: NULL"); return HOFEM_ERR_ARG; }
+  return fill_random(m, seed, x, S(stream));
+}
+
+void hofem_op_destroy(void* op) { free_op(static_cast<Op*>(op)); }
+
+hofem_status hofem_cg(void* op_, const double* b, double* x, double rel_tol, int max_iter,
+                      int fixed_iters, int check_every, double* rr_history,
+                      hofem_cg_stats* stats, void* stream) {
+  Op* op = static_cast<Op*>(op_);
+  if (!op || !b || !x || b == x) { set_error("hofem_cg: NULL or aliased b/x"); return HOFEM_ERR_ARG; }
+  return cg_solve(op, b, x, rel_tol, max_iter, fixed_iters, check_every, rr_history, stats,
+                  S(stream));
+}
+
+hofem_status hofem_dot(const void* mesh, const double* a, const double* b, double* out_host,
+                       void* stream) {
+  Mesh* m = const_cast<Mesh*>(static_cast<const Mesh*>(mesh));
+  if (!m || !a || !b || !out_host) { set_error("hofem_dot: NULL"); return HOFEM_ERR_ARG; }
+  HOFEM_TRY(dot_device(m, a, b, m->d_scalars, S(stream)));
+  HOFEM_CUDA(cudaMemcpyAsync(out_host, m->d_scalars, sizeof(double), cudaMemcpyDeviceToHost,
+                             S(stream)));
+  HOFEM_CUDA(cudaStreamSynchronize(S(stream)));
+  return HOFEM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,115 @@
+// comm.cu -- the parallel prolongation/restriction P, P^T of the paper's triple
+// product P^T A P (§2.3), collapsed for a z-slab partition into
+// one exchange per apply: each rank sends its two boundary
+// lattice planes (contiguous in the x-fastest layout, so no pack kernel) to its
+// z-neighbours with grouped ncclSend/ncclRecv over NVLink, then adds what it
+// received.  a+b == b+a in IEEE arithmetic, so both copies of a shared plane end
+// bitwise identical (reading R9).  Dirichlet rows on the planes are re-imposed
+// after the sum.  CG dot products use ncclAllReduce of one FP64 (§8(e)).
+#include "internal.h"
+
+namespace hofem {
+
+namespace {
+
+__global__ void add_plane_kernel(long long plane, long long Nx, long long Ny, long long Kg,
+                                 long long NzG, int bcmode, const double* __restrict__ xbc,
+                                 const double* __restrict__ recv, double* __restrict__ y) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= plane) return;
+  double v = y[t] + recv[t];
+  if (bcmode) {
+    long long I = t % Nx, J = t / Nx;
+    if (I == 0 || I == Nx - 1 || J == 0 || J == Ny - 1 || Kg == 0 || Kg == NzG - 1)
+      v = bcmode == 1 ? xbc[t] : 0.0;
+  }
+  y[t] = v;
+}
+
+hofem_status nccl_status(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return HOFEM_OK;
+  set_error("%s: %s", what, ncclGetErrorString(r));
+  return HOFEM_ERR_NCCL;
+}
+
+}  // namespace
+
+hofem_status exchange_planes(Op* op, const double* x, double* y, cudaStream_t s) {
+  Mesh* m = op->mesh;
+  if (m->nranks <= 1) return HOFEM_OK;
+  const long long plane = m->plane;
+  const int r = m->rank, R = m->nranks;
+  ncclComm_t c = m->comm->nccl;
+  double* top = y + (m->Nzl - 1) * plane;
+  HOFEM_TRY(nccl_status(ncclGroupStart(), "ncclGroupStart"));
+  if (r > 0) {
+    HOFEM_TRY(nccl_status(ncclSend(y, plane, ncclDouble, r - 1, c, s), "ncclSend lo"));
+    HOFEM_TRY(nccl_status(ncclRecv(m->d_recv, plane, ncclDouble, r - 1, c, s), "ncclRecv lo"));
+  }
+  if (r < R - 1) {
+    HOFEM_TRY(nccl_status(ncclSend(top, plane, ncclDouble, r + 1, c, s), "ncclSend hi"));
+    HOFEM_TRY(nccl_status(ncclRecv(m->d_recv + plane, plane, ncclDouble, r + 1, c, s),
+                          "ncclRecv hi"));
+  }
+  HOFEM_TRY(nccl_status(ncclGroupEnd(), "ncclGroupEnd"));
+  const int bcmode = op->bc ? (x ? 1 : 2) : 0;
+  const unsigned g = (unsigned)((plane + 255) / 256);
+  const long long K0 = (long long)m->p * m->z0;
+  if (r > 0) {
+    add_plane_kernel<<<g, 256, 0, s>>>(plane, m->Nx, m->Ny, K0, m->NzG, bcmode, x, m->d_recv, y);
+    HOFEM_LAUNCHED();
+  }
+  if (r < R - 1) {
+    add_plane_kernel<<<g, 256, 0, s>>>(plane, m->Nx, m->Ny, K0 + m->Nzl - 1, m->NzG, bcmode,
+                                       x ? x + (m->Nzl - 1) * plane : nullptr,
+                                       m->d_recv + plane, top);
+    HOFEM_LAUNCHED();
+  }
+  return HOFEM_OK;
+}
+
+hofem_status allreduce_sum(Mesh* m, double* d_val, int count, cudaStream_t s) {
+  if (m->nranks <= 1) return HOFEM_OK;
+  return nccl_status(
+      ncclAllReduce(d_val, d_val, count, ncclDouble, ncclSum, m->comm->nccl, s), "ncclAllReduce");
+}
+
+}  // namespace hofem
+
+extern "C" {
+
+hofem_status hofem_comm_unique_id(void* out) {
+  if (!out) { hofem::set_error("hofem_comm_unique_id: NULL"); return HOFEM_ERR_ARG; }
+  ncclUniqueId id;
+  HOFEM_TRY(hofem::nccl_status(ncclGetUniqueId(&id), "ncclGetUniqueId"));
+  static_assert(sizeof(id) == 128, "ncclUniqueId must be 128 bytes");
+  memcpy(out, &id, sizeof(id));
+  return HOFEM_OK;
+}
+
+hofem_status hofem_comm_init(const void* nccl_id, int rank, int nranks, int device,
+                             void** comm_out) {
+  if (!nccl_id || !comm_out || nranks < 1 || rank < 0 || rank >= nranks) {
+    hofem::set_error("hofem_comm_init: bad arguments");
+    return HOFEM_ERR_ARG;
+  }
+  HOFEM_CUDA(cudaSetDevice(device));
+  auto* c = new hofem::Comm();
+  c->rank = rank; c->nranks = nranks; c->device = device;
+  ncclUniqueId id;
+  memcpy(&id, nccl_id, sizeof(id));
+  hofem_status st = hofem::nccl_status(ncclCommInitRank(&c->nccl, nranks, id, rank),
+                                       "ncclCommInitRank");
+  if (st != HOFEM_OK) { delete c; return st; }
+  *comm_out = c;
+  return HOFEM_OK;
+}
+
+void hofem_comm_destroy(void* comm) {
+  auto* c = static_cast<hofem::Comm*>(comm);
+  if (!c) return;
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+// fused_p.cu -- instantiation of the fused brick kernels for one P1 = p+1
+// (compiled once per P1 with -DHOFEM_P1=<P1>, so the builds run in parallel).
+#include <string.h>
+
+#include "fused_impl.cuh"
+
+#ifndef HOFEM_P1
+#error "compile with -DHOFEM_P1=<p+1>"
+#endif
+
+namespace hofem {
+
+namespace {
+
+template <int KIND, int P1, int Q>
+cudaError_t launch_general(const double* B, const double* G, const FusedArgs& A, int nbricks,
+                           cudaStream_t s) {
+  using S = Shape<P1>;
+  using C = Cfg<KIND, P1, Q, S::BX, S::BY, S::BZ>;
+  Tab<P1, Q> T;
+  memcpy(T.B, B, sizeof(T.B));
+  memcpy(T.G, G, sizeof(T.G));
+  auto kern = fused_brick<KIND, P1, Q, S::BX, S::BY, S::BZ, S::NT, S::MINB>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  kern<<<nbricks, S::NT, C::SMEM_BYTES, s>>>(T, A);
+  return cudaPeekAtLastError();
+}
+
+template <int P1>
+cudaError_t launch_colloc(const double* G, const FusedArgs& A, int nbricks, cudaStream_t s) {
+  using S = Shape<P1>;
+  using C = Cfg<KIND_COLLOC, P1, P1, S::BX, S::BY, S::BZ>;
+  Tab<P1, P1> T;
+  memset(T.B, 0, sizeof(T.B));
+  memcpy(T.G, G, sizeof(T.G));
+  auto kern = fused_brick_colloc<P1, S::BX, S::BY, S::BZ, S::NT, S::MINB>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  kern<<<nbricks, S::NT, C::SMEM_BYTES, s>>>(T, A);
+  return cudaPeekAtLastError();
+}
+
+}  // namespace
+
+template <>
+bool fused_launch<HOFEM_P1>(int kind, int Q, const double* B, const double* G,
+                            const FusedArgs& A, int nbricks, cudaStream_t s, cudaError_t* err) {
+  constexpr int P1 = HOFEM_P1;
+  if (kind == KIND_COLLOC) {
+    if (Q != P1) return false;
+    *err = launch_colloc<P1>(G, A, nbricks, s);
+    return true;
+  }
+  if (Q == P1 + 1) {
+    *err = kind == KIND_MASS ? launch_general<KIND_MASS, P1, P1 + 1>(B, G, A, nbricks, s)
+                             : launch_general<KIND_DIFF, P1, P1 + 1>(B, G, A, nbricks, s);
+    return true;
+  }
+  if (Q == P1) {
+    *err = kind == KIND_MASS ? launch_general<KIND_MASS, P1, P1>(B, G, A, nbricks, s)
+                             : launch_general<KIND_DIFF, P1, P1>(B, G, A, nbricks, s);
+    return true;
+  }
+  return false;
+}
+
+template <>
+FusedLaunch fused_shape<HOFEM_P1>(int kind) {
+  using S = Shape<HOFEM_P1>;
+  constexpr int p = HOFEM_P1 - 1;
+  (void)kind;
+  return FusedLaunch{S::BX, S::BY, S::BZ, (p * S::BX + 1) * (p * S::BY + 1) * (p * S::BZ + 1)};
+}
+
+}  // namespace hofem

@@ -1,0 +1,273 @@
+"""Thin Python binding of the C ABI in ``include/hofem.h`` (ctypes).
+
+Argument marshalling only: every step of the hot path runs in libhofem.so's
+CUDA kernels.  Vectors are torch.float64 CUDA tensors (device memory and
+streams come from PyTorch); their ``data_ptr()`` is passed straight through.
+There is no CPU fallback: if the library or a CUDA device is missing, every
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libhofem.so")
+
+MASS, DIFFUSION = 1, 2
+GAUSS, GLL = 1, 2
+BC_NONE, BC_DIRICHLET = 0, 1
+
+OK, ERR_ARG, ERR_MESH, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_BREAKDOWN, NOT_CONVERGED = range(8)
+_NAMES = ["OK", "ERR_ARG", "ERR_MESH", "ERR_CUDA", "ERR_NCCL", "ERR_OOM", "ERR_BREAKDOWN",
+          "NOT_CONVERGED"]
+
+
+class HofemError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_NAMES[status] if 0 <= status < 8 else status}: {msg}")
+        self.status = status
+
+
+class MeshDesc(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int), ("ny", ctypes.c_int), ("nz_global", ctypes.c_int),
+                ("p", ctypes.c_int), ("extent", ctypes.c_double * 3), ("alpha", ctypes.c_double)]
+
+
+class MeshInfo(ctypes.Structure):
+    _fields_ = [("n_local", ctypes.c_longlong), ("n_owned", ctypes.c_longlong),
+                ("n_global", ctypes.c_longlong), ("elems_local", ctypes.c_longlong),
+                ("plane", ctypes.c_longlong), ("rank", ctypes.c_int), ("nranks", ctypes.c_int),
+                ("z0", ctypes.c_int), ("nz_local", ctypes.c_int)]
+
+
+class ProfileStats(ctypes.Structure):
+    _fields_ = [("brick_launches", ctypes.c_longlong), ("brick_ms", ctypes.c_double),
+                ("fixup_launches", ctypes.c_longlong), ("fixup_ms", ctypes.c_double)]
+
+
+class CGStats(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int), ("converged", ctypes.c_int),
+                ("r0_norm", ctypes.c_double), ("final_rel_res", ctypes.c_double)]
+
+
+# name -> (restype, argtypes); the names are exactly those of include/hofem.h
+_V, _I, _LL, _D = ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong, ctypes.c_double
+_PV = ctypes.POINTER(ctypes.c_void_p)
+SIGNATURES = {
+    "hofem_last_error": (ctypes.c_char_p, []),
+    "hofem_comm_unique_id": (_I, [_V]),
+    "hofem_comm_init": (_I, [_V, _I, _I, _I, _PV]),
+    "hofem_comm_destroy": (None, [_V]),
+    "hofem_mesh_create": (_I, [ctypes.POINTER(MeshDesc), _V, _V, _PV]),
+    "hofem_mesh_info_get": (_I, [_V, ctypes.POINTER(MeshInfo)]),
+    "hofem_mesh_coords": (_I, [_V, _V, _V]),
+    "hofem_mesh_destroy": (None, [_V]),
+    "hofem_op_create": (_I, [_V, _I, _I, _I, _I, _V, _PV]),
+    "hofem_op_apply": (_I, [_V, _V, _V, _V]),
+    "hofem_op_apply_unfused": (_I, [_V, _V, _V, _V]),
+    "hofem_op_qdata": (_I, [_V, ctypes.POINTER(_V), ctypes.POINTER(_LL)]),
+    "hofem_op_nq1d": (_I, [_V, ctypes.POINTER(_I)]),
+    "hofem_rhs_manufactured": (_I, [_V, _V, _V]),
+    "hofem_fill_random": (_I, [_V, ctypes.c_ulonglong, _V, _V]),
+    "hofem_op_destroy": (None, [_V]),
+    "hofem_cg": (_I, [_V, _V, _V, _D, _I, _I, _I, _V, ctypes.POINTER(CGStats), _V]),
+    "hofem_dot": (_I, [_V, _V, _V, ctypes.POINTER(_D), _V]),
+    "hofem_profile_enable": (_I, [_I]),
+    "hofem_profile_read": (_I, [ctypes.POINTER(ProfileStats)]),
+    "hofem_launch_count": (_LL, []),
+    "hofem_launch_count_reset": (None, []),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libhofem.so (built by paper_2402_15940_b200.build).  Raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built: run python -m paper_2402_15940_b200.build "
+                               "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != OK:
+        raise HofemError(st, lib().hofem_last_error().decode())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: torch.Tensor):
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise ValueError("expected a contiguous torch.float64 CUDA tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _cudart():
+    import glob
+    import nvidia.cuda_runtime  # type: ignore
+    for d in nvidia.cuda_runtime.__path__:
+        for f in glob.glob(os.path.join(d, "lib", "libcudart.so*")):
+            return ctypes.CDLL(f)
+    return ctypes.CDLL("libcudart.so.12")
+
+
+def copy_device_to_tensor(dev_ptr: int, n: int, device=None) -> torch.Tensor:
+    """Copy n FP64 values from a library-owned device pointer into a new tensor."""
+    out = torch.empty(n, dtype=torch.float64, device=device or "cuda")
+    rt = _cudart()
+    rt.cudaMemcpyAsync.argtypes = [_V, _V, ctypes.c_size_t, _I, _V]
+    st = rt.cudaMemcpyAsync(ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(dev_ptr), n * 8, 3,
+                            _stream())
+    if st != 0:
+        raise RuntimeError(f"cudaMemcpyAsync failed: {st}")
+    return out
+
+
+class Comm:
+    """NCCL communicator for the z-slab partition (one process per GPU)."""
+
+    def __init__(self, rank: int, nranks: int, device: int, nccl_id: bytes):
+        h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(nccl_id, 128)
+        _check(lib().hofem_comm_init(buf, rank, nranks, device, ctypes.byref(h)))
+        self.handle = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(lib().hofem_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_torch_distributed(cls):
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return cls(rank, world, torch.cuda.current_device(), obj[0])
+
+    def close(self):
+        if self.handle:
+            lib().hofem_comm_destroy(self.handle)
+            self.handle = None
+
+
+class Mesh:
+    def __init__(self, nx, ny, nz, p, alpha=0.1, extent=(1.0, 1.0, 1.0), comm: Comm | None = None,
+                 stream=None):
+        d = MeshDesc(nx, ny, nz, p, (ctypes.c_double * 3)(*extent), alpha)
+        h = ctypes.c_void_p()
+        _check(lib().hofem_mesh_create(ctypes.byref(d), comm.handle if comm else None,
+                                       _stream(stream), ctypes.byref(h)))
+        self.handle = h
+        self.p = p
+        info = MeshInfo()
+        _check(lib().hofem_mesh_info_get(h, ctypes.byref(info)))
+        self.info = info
+        self.n_local = info.n_local
+        self.n_owned = info.n_owned
+        self.n_global = info.n_global
+        self.dims = (p * nx + 1, p * ny + 1, p * info.nz_local + 1)
+
+    def coords(self, stream=None) -> torch.Tensor:
+        out = torch.empty(3 * self.n_local, dtype=torch.float64, device="cuda")
+        _check(lib().hofem_mesh_coords(self.handle, _ptr(out), _stream(stream)))
+        return out.view(3, self.n_local)
+
+    def random(self, seed: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        out = torch.empty(self.n_local, dtype=torch.float64, device="cuda") if out is None else out
+        _check(lib().hofem_fill_random(self.handle, ctypes.c_ulonglong(seed), _ptr(out),
+                                       _stream(stream)))
+        return out
+
+    def dot(self, a: torch.Tensor, b: torch.Tensor, stream=None) -> float:
+        v = ctypes.c_double()
+        _check(lib().hofem_dot(self.handle, _ptr(a), _ptr(b), ctypes.byref(v), _stream(stream)))
+        return v.value
+
+    def close(self):
+        if self.handle:
+            lib().hofem_mesh_destroy(self.handle)
+            self.handle = None
+
+
+class Operator:
+    def __init__(self, mesh: Mesh, kind=DIFFUSION, rule=GAUSS, q_override=0, bc=BC_NONE,
+                 stream=None):
+        h = ctypes.c_void_p()
+        _check(lib().hofem_op_create(mesh.handle, kind, rule, q_override, bc, _stream(stream),
+                                     ctypes.byref(h)))
+        self.handle = h
+        self.mesh = mesh
+        q = ctypes.c_int()
+        _check(lib().hofem_op_nq1d(h, ctypes.byref(q)))
+        self.Q = q.value
+        self.kind, self.rule, self.bc = kind, rule, bc
+
+    def apply(self, x: torch.Tensor, y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        y = torch.empty_like(x) if y is None else y
+        _check(lib().hofem_op_apply(self.handle, _ptr(x), _ptr(y), _stream(stream)))
+        return y
+
+    def apply_unfused(self, x: torch.Tensor, y: torch.Tensor | None = None, stream=None):
+        y = torch.empty_like(x) if y is None else y
+        _check(lib().hofem_op_apply_unfused(self.handle, _ptr(x), _ptr(y), _stream(stream)))
+        return y
+
+    def qdata(self) -> torch.Tensor:
+        p, n = ctypes.c_void_p(), ctypes.c_longlong()
+        _check(lib().hofem_op_qdata(self.handle, ctypes.byref(p), ctypes.byref(n)))
+        return copy_device_to_tensor(p.value, n.value)
+
+    def rhs(self, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        out = torch.empty(self.mesh.n_local, dtype=torch.float64, device="cuda") if out is None else out
+        _check(lib().hofem_rhs_manufactured(self.handle, _ptr(out), _stream(stream)))
+        return out
+
+    def cg(self, b: torch.Tensor, x: torch.Tensor, rel_tol=1e-10, max_iter=1000,
+           fixed_iters=False, check_every=1, history=False, stream=None):
+        """Returns (status, stats, rr_history or None).  x is updated in place."""
+        stats = CGStats()
+        hist = (ctypes.c_double * (max_iter + 1))() if history else None
+        st = lib().hofem_cg(self.handle, _ptr(b), _ptr(x), rel_tol, max_iter, int(fixed_iters),
+                            check_every, hist, ctypes.byref(stats), _stream(stream))
+        if st not in (OK, NOT_CONVERGED):
+            _check(st)
+        rr = list(hist[: stats.iterations + 1]) if history else None
+        return st, stats, rr
+
+    def close(self):
+        if self.handle:
+            lib().hofem_op_destroy(self.handle)
+            self.handle = None
+
+
+def profile_enable(on: bool = True):
+    _check(lib().hofem_profile_enable(int(on)))
+
+
+def profile_read() -> ProfileStats:
+    s = ProfileStats()
+    _check(lib().hofem_profile_read(ctypes.byref(s)))
+    return s
+
+
+def launch_count() -> int:
+    return lib().hofem_launch_count()
+
+
+def launch_count_reset():
+    lib().hofem_launch_count_reset()
