@@ -58,7 +58,7 @@ def brick_direct_points(nx, ny, nz, p, B):
     return axis(nx, B[0]) * axis(ny, B[1]) * axis(nz, B[2])
 
 
-SHAPES = {2: (8, 4, 4), 3: (4, 4, 2), 4: (4, 2, 2), 5: (2, 2, 2), 6: (2, 2, 2), 7: (2, 2, 1),
+SHAPES = {2: (4, 4, 4), 3: (4, 4, 2), 4: (4, 2, 2), 5: (2, 2, 2), 6: (2, 2, 2), 7: (2, 2, 1),
           8: (2, 2, 1), 9: (2, 1, 1)}  # fused_impl.cuh Shape<P1>
 
 

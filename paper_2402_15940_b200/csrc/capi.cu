@@ -187,7 +187,7 @@ hofem_status hofem_op_create(void* mesh, hofem_kind kind, hofem_rule rule, int q
   op->qcount = m->elems * op->nc * (long long)Q * Q * Q;
   CK(dalloc(&op->d_B, Q * P1, "op tables"));
   CK(dalloc(&op->d_G, Q * P1, "op tables"));
-  CK(dalloc(&op->d_qdata, op->qcount, "qdata"));
+  CK(dalloc(&op->d_qdata, op->qcount + 2, "qdata"));  // +16 B: widened L2 prefetch
   CK(cuda_status(cudaMemcpyAsync(op->d_B, op->tab.B, sizeof(double) * Q * P1,
                                  cudaMemcpyHostToDevice, S(stream)), "upload B"));
   CK(cuda_status(cudaMemcpyAsync(op->d_G, op->tab.G, sizeof(double) * Q * P1,

@@ -1,7 +1,8 @@
-// fused.cu -- dispatch of the fused brick kernels (fused_impl.cuh) and the
+// fused.cu -- dispatch of the fused column kernels (fused_impl.cuh) and the
 // brick-interface fix-up kernel that completes the deterministic R^T
-// (SURVEY.md §8(a) row a8): every lattice point on an interior brick face sums
-// the partials of its 2, 4 or 8 bricks in ascending brick order.
+// (SURVEY.md §8(a) row a8): every lattice point on an interior x/y brick face or
+// a work-unit boundary plane sums the partials of its 2, 4 or 8 bricks in
+// ascending brick order.
 #include <vector>
 
 #include "fused_impl.cuh"
@@ -11,7 +12,7 @@ namespace hofem {
 #define HOFEM_FOR_P1(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9)
 #define HOFEM_DECL(P1)                                                                     \
   template <>                                                                              \
-  bool fused_launch<P1>(int, int, const double*, const double*, const FusedArgs&, int,     \
+  bool fused_launch<P1>(int, int, const double*, const double*, const ColArgs&, int,       \
                         cudaStream_t, cudaError_t*);                                       \
   template <>                                                                              \
   FusedLaunch fused_shape<P1>(int);
@@ -25,7 +26,7 @@ struct FixArgs {
   double* y;
   const double* bbuf;
   long long Nx, Ny, Nzl, K0, NzG;
-  int PX, PY, PZ, LX, LY, nbx, nby, nbz, bc;
+  int p, PX, PY, PZU, LX, LY, nbx, nby, nzl, bc;
   long long BLAT, nZ, nY, nX;
 };
 
@@ -47,27 +48,44 @@ __device__ __forceinline__ int axis_bricks(long long I, int P, int nb, long long
   return 1;
 }
 
+// z: bricks are single element layers; only work-unit boundary planes (every
+// PZU = p*zc lattice planes) are split between two bricks -- element faces
+// inside a unit were summed through the in-kernel carry into the upper brick.
+__device__ __forceinline__ int axis_bricks_z(long long K, int p, int PZU, int nzl, long long N,
+                                             int* br, int* loc) {
+  if (on_plane(K, PZU, N)) {
+    br[0] = (int)(K / p) - 1; loc[0] = p;
+    br[1] = (int)(K / p);     loc[1] = 0;
+    return 2;
+  }
+  int b = (int)(K / p);
+  if (b > nzl - 1) b = nzl - 1;
+  br[0] = b;
+  loc[0] = (int)(K - (long long)p * b);
+  return 1;
+}
+
 __global__ void fixup_kernel(FixArgs F) {
   long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   long long I, J, K;
   if (t < F.nZ) {
     long long m = t / (F.Nx * F.Ny) + 1, r = t % (F.Nx * F.Ny);
-    K = m * F.PZ; I = r % F.Nx; J = r / F.Nx;
+    K = m * F.PZU; I = r % F.Nx; J = r / F.Nx;
   } else if ((t -= F.nZ) < F.nY) {
     long long m = t / (F.Nx * F.Nzl) + 1, r = t % (F.Nx * F.Nzl);
     J = m * F.PY; I = r % F.Nx; K = r / F.Nx;
-    if (on_plane(K, F.PZ, F.Nzl)) return;
+    if (on_plane(K, F.PZU, F.Nzl)) return;
   } else if ((t -= F.nY) < F.nX) {
     long long m = t / (F.Ny * F.Nzl) + 1, r = t % (F.Ny * F.Nzl);
     I = m * F.PX; J = r % F.Ny; K = r / F.Ny;
-    if (on_plane(J, F.PY, F.Ny) || on_plane(K, F.PZ, F.Nzl)) return;
+    if (on_plane(J, F.PY, F.Ny) || on_plane(K, F.PZU, F.Nzl)) return;
   } else {
     return;
   }
   int bx[2], ix[2], by[2], iy[2], bz[2], iz[2];
   int nbxl = axis_bricks(I, F.PX, F.nbx, F.Nx, F.LX, bx, ix);
   int nbyl = axis_bricks(J, F.PY, F.nby, F.Ny, F.LY, by, iy);
-  int nbzl = axis_bricks(K, F.PZ, F.nbz, F.Nzl, F.PZ + 1, bz, iz);
+  int nbzl = axis_bricks_z(K, F.p, F.PZU, F.nzl, F.Nzl, bz, iz);
   double s = 0.0;
   for (int c = 0; c < nbzl; ++c)
     for (int b = 0; b < nbyl; ++b)
@@ -92,7 +110,7 @@ FusedLaunch shape_for(int P1, int kind) {
     HOFEM_FOR_P1(HOFEM_CASE)
 #undef HOFEM_CASE
   }
-  return FusedLaunch{0, 0, 0, 0};
+  return FusedLaunch{0, 0, 0};
 }
 
 int fused_kind(const Op* op) {
@@ -152,14 +170,47 @@ bool fused_supported(const Op* op) {
   return op->Q == P1 || op->Q == P1 + 1;
 }
 
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = kNumSMs;
+  }
+  return n;
+}
+
+// Split each column into chunks so that the units fill the persistent grid in
+// as few, as full, rounds as possible (fewer chunks on ties: each chunk boundary
+// is a plane the fix-up kernel has to sum).
+void choose_chunks(long long ncol, int nzl, int G, int* zc_out, int* nchunks_out) {
+  double best = -1.0;
+  int bz = nzl, bn = 1;
+  for (int want = 1; want <= 16 && want <= nzl; ++want) {
+    const int zc = (nzl + want - 1) / want, nch = (nzl + zc - 1) / zc;
+    const long long units = ncol * nch;
+    const long long rounds = (units + G - 1) / G;
+    const double eff = (double)units / (double)(rounds * G) - 0.002 * nch;
+    if (eff > best + 1e-12) { best = eff; bz = zc; bn = nch; }
+  }
+  *zc_out = bz;
+  *nchunks_out = bn;
+}
+
 hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s) {
   Mesh* m = op->mesh;
   const int P1 = m->P1, p = m->p, kind = fused_kind(op);
   FusedLaunch L = shape_for(P1, kind);
-  const int nbx = (m->nx + L.BX - 1) / L.BX, nby = (m->ny + L.BY - 1) / L.BY,
-            nbz = (m->nzl + L.BZ - 1) / L.BZ;
-  const long long nbricks = (long long)nbx * nby * nbz;
+  const int nbx = (m->nx + L.BX - 1) / L.BX, nby = (m->ny + L.BY - 1) / L.BY;
+  const long long ncol = (long long)nbx * nby;
+  const long long nbricks = ncol * m->nzl;
   if (nbricks == 0) return HOFEM_OK;
+  const int G0 = num_sms();
+  int zc = 1, nchunks = 1;
+  choose_chunks(ncol, m->nzl, G0, &zc, &nchunks);
+  const long long nunits = ncol * nchunks;
+  const int grid = (int)(nunits < G0 ? nunits : G0);
   const long long need = nbricks * L.blat;
   if (op->bbuf_len < need) {
     if (op->d_bbuf) cudaFree(op->d_bbuf);
@@ -172,10 +223,10 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s) {
     }
     op->bbuf_len = need;
   }
-  FusedArgs A;
+  ColArgs A;
   A.x = x; A.y = y; A.qd = op->d_qdata; A.bbuf = op->d_bbuf;
   A.nx = m->nx; A.ny = m->ny; A.nzl = m->nzl;
-  A.nbx = nbx; A.nby = nby; A.nbz = nbz;
+  A.nbx = nbx; A.nby = nby; A.zc = zc; A.nunits = (int)nunits;
   A.Nx = m->Nx; A.Ny = m->Ny; A.Nzl = m->Nzl;
   A.K0 = (long long)p * m->z0; A.NzG = m->NzG;
   A.bc = op->bc;
@@ -187,9 +238,9 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s) {
     cudaEventRecord(ev.first, s);
   }
   switch (P1) {
-#define HOFEM_CASE(P)                                                                   \
-  case P:                                                                               \
-    ok = fused_launch<P>(kind, op->Q, op->tab.B, op->tab.G, A, (int)nbricks, s, &err);  \
+#define HOFEM_CASE(P)                                                            \
+  case P:                                                                        \
+    ok = fused_launch<P>(kind, op->Q, op->tab.B, op->tab.G, A, grid, s, &err);   \
     break;
     HOFEM_FOR_P1(HOFEM_CASE)
 #undef HOFEM_CASE
@@ -199,7 +250,7 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s) {
     return HOFEM_ERR_ARG;
   }
   count_launch();
-  if (err != cudaSuccess) return cuda_status(err, "fused brick kernel launch");
+  if (err != cudaSuccess) return cuda_status(err, "fused column kernel launch");
   if (g_prof.on) {
     cudaEventRecord(ev.second, s);
     g_prof.brick.push_back(ev);
@@ -207,11 +258,11 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s) {
   FixArgs F;
   F.x = x; F.y = y; F.bbuf = op->d_bbuf;
   F.Nx = m->Nx; F.Ny = m->Ny; F.Nzl = m->Nzl; F.K0 = A.K0; F.NzG = m->NzG;
-  F.PX = p * L.BX; F.PY = p * L.BY; F.PZ = p * L.BZ;
+  F.p = p; F.PX = p * L.BX; F.PY = p * L.BY; F.PZU = p * zc;
   F.LX = F.PX + 1; F.LY = F.PY + 1;
-  F.nbx = nbx; F.nby = nby; F.nbz = nbz; F.bc = op->bc;
+  F.nbx = nbx; F.nby = nby; F.nzl = m->nzl; F.bc = op->bc;
   F.BLAT = L.blat;
-  F.nZ = (long long)(nbz - 1) * m->Nx * m->Ny;
+  F.nZ = (long long)(nchunks - 1) * m->Nx * m->Ny;
   F.nY = (long long)(nby - 1) * m->Nx * m->Nzl;
   F.nX = (long long)(nbx - 1) * m->Ny * m->Nzl;
   const long long nt = F.nZ + F.nY + F.nX;

@@ -1,26 +1,34 @@
 // fused_impl.cuh -- the fused sm_100a operator kernels (SURVEY.md §8(a) rows
 // a4-a9; north star "one fused sm_100a kernel per operator").
 //
-// One CTA owns a brick of BX*BY*BZ elements and does, for all of them:
-//   a4  gather R: the brick's (p*BX+1)(p*BY+1)(p*BZ+1) lattice of x is read once
-//       from HBM (rows coalesced along x) into shared memory, Dirichlet dofs
-//       zeroed (reading R6);
+// Persistent "column" kernel: one CTA per SM.  A work unit is a column of
+// bricks -- BX*BY elements in x,y by one element layer in z -- over a chunk of zc
+// element layers; the CTA streams the column bottom to top.  Per brick it does:
+//   a4  gather R: the brick's (p*BX+1)(p*BY+1)(p+1) lattice of x, read with
+//       asynchronous 8-byte copies into a double-buffered shared-memory lattice
+//       (the NEXT brick's lattice is in flight while this one computes);
+//       Dirichlet dofs and out-of-mesh points are zero-filled (reading R6);
 //   a5  B: the 1D B1d/G1d contractions dimension by dimension (x, then y in
 //       shared memory; z in registers, one thread per (qx,qy) quadrature column);
-//   a6  D: the pointwise qdata (streamed from HBM, coalesced, L2 evict-first);
+//   a6  D: the pointwise qdata.  Each stage-3 thread holds its column's qdata for
+//       the NEXT brick in registers, loaded (L2 evict-first, coalesced) right
+//       after it consumed the current one -- the dominant HBM stream is always
+//       one brick ahead of the math, without spending shared memory on it;
 //   a7  B^T: the transposed contractions (z in registers, then y, x in smem);
 //   a8  R^T: a deterministic in-brick sum -- every brick lattice point sums its
-//       1..8 element contributions in ascending element order.  Points strictly
-//       inside the brick (and on the domain boundary) are written to y directly;
-//       points on an interior brick face go to a per-brick partial buffer that
-//       fixup_kernel (fused.cu) sums in ascending brick order.
+//       1..4 element contributions in ascending element order; the top lattice
+//       plane is carried in shared memory and added (in fixed order) to the
+//       bottom plane of the next brick of the column, so z-faces inside a unit
+//       never leave the SM.  Points on an interior x/y brick face (or a unit
+//       boundary plane) go to a per-brick partial buffer that fixup_kernel
+//       (fused.cu) sums in ascending brick order; all others are written to y.
 //   a9  y[ess] = x[ess].
 // The 1D tables live in the kernel-parameter constant bank (every index is a
 // compile-time constant after unrolling, so DFMA takes them as uniform-register
 // operands: no shared-memory traffic for B/G).
 //
-// Shared-memory layouts are chosen so that consecutive lanes touch consecutive
-// or odd-strided doubles (conflict-free 64-bit accesses): see DESIGN.md §4.
+// Shared-memory layouts keep consecutive lanes on consecutive or odd-strided
+// doubles (conflict-free 64-bit accesses): see DESIGN.md §4.
 #pragma once
 
 #include "internal.h"
@@ -33,15 +41,16 @@ struct Tab {
   double G[Q * P1];
 };
 
-struct FusedArgs {
+struct ColArgs {
   const double* x;
   double* y;
   const double* qd;
   double* bbuf;
-  int nx, ny, nzl;       // local element counts
-  int nbx, nby, nbz;     // bricks per axis
-  long long Nx, Ny, Nzl; // local lattice sizes
-  long long K0, NzG;     // global index of local plane 0; global plane count
+  int nx, ny, nzl;        // local element counts
+  int nbx, nby;           // bricks per axis in x, y (a brick is BX x BY x 1 elements)
+  int zc, nunits;         // element layers per work unit; units = nbx*nby*chunks
+  long long Nx, Ny, Nzl;  // local lattice sizes
+  long long K0, NzG;      // global index of local plane 0; global plane count
   int bc;
 };
 
@@ -57,429 +66,689 @@ __device__ __forceinline__ double ld_stream(const double* p) {
   return v;
 }
 
-__device__ __forceinline__ bool ess_point(const FusedArgs& A, long long I, long long J,
-                                          long long K) {
-  long long Kg = K + A.K0;
-  return I == 0 || I == A.Nx - 1 || J == 0 || J == A.Ny - 1 || Kg == 0 || Kg == A.NzG - 1;
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = valid ? 8 : 0;  // src-size 0 => zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(n)
+               : "memory");
+}
+// threadIdx.x through a volatile read: per-brick index arithmetic is then
+// recomputed inside the persistent loop instead of being hoisted into
+// long-lived registers (which starves the contraction stages).
+__device__ __forceinline__ int vtid() {
+  int t;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
+  return t;
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
 }
 
-template <int KIND, int P1, int Q, int BX, int BY, int BZ>
+template <int KIND, int P1, int Q, int BX, int BY>
 struct Cfg {
   static constexpr int p = P1 - 1;
-  static constexpr int NE = BX * BY * BZ;
-  static constexpr int LX = p * BX + 1, LY = p * BY + 1, LZ = p * BZ + 1;
-  static constexpr int BLAT = LX * LY * LZ;                 // dense brick lattice
-  static constexpr int PS = ((LX * LY) % 2 == 0) ? LX * LY + 1 : LX * LY;  // odd plane stride
-  static constexpr int LAT = PS * LZ;
-  static constexpr int Qp = (Q % 2 == 0) ? Q + 1 : Q;        // odd c-stride in T1
-  static constexpr int S2 = Qp * P1;                         // b-stride in T1
+  static constexpr int NE = BX * BY;
+  static constexpr int LX = p * BX + 1, LY = p * BY + 1, LZ = P1;
+  static constexpr int BLAT = LX * LY * LZ;  // dense brick lattice (partial-buffer layout)
+  // x lattice in smem is x-SLOWEST: L[i][j][k] = k + LZ*j + LXS*i; stage 1 (lanes
+  // over (b,c), c fastest) reads nearly contiguous doubles; LXS odd.
+  static constexpr int LXS = ((LY * LZ) % 2 == 0) ? LY * LZ + 1 : LY * LZ;
+  static constexpr int LAT = LXS * LX;
+  static constexpr int Qp = (Q % 2 == 0) ? Q + 1 : Q;  // odd c-stride in T1
+  static constexpr int S2 = Qp * P1;                   // b-stride in T1
   static constexpr int NT1 = (KIND == KIND_MASS) ? 1 : 2;
   static constexpr int NT2 = (KIND == KIND_MASS) ? 1 : 3;
   static constexpr int T1N = NT1 * S2 * P1;
-  static constexpr int QQP = Q * Q * P1;
-  static constexpr int T2N = NT2 * QQP;
+  // T2[comp][qy][c][qx]: qy-stride RS >= Q*P1, RS == Q (mod 16): stage-2 writes
+  // (lanes over qx + Q c) and stage-3 reads (lanes over qx + Q qy) are both
+  // conflict-free.
+  static constexpr int RS = Q * P1 + (((Q - Q * P1) % 16) + 16) % 16;
+  static constexpr int T2C = Q * RS;
+  static constexpr int T2N = NT2 * T2C;
   static constexpr int SA = ((P1 * P1) % 2 == 0) ? P1 * P1 + 1 : P1 * P1;  // a-stride of y_e
   static constexpr int YEN = (KIND == KIND_COLLOC) ? P1 * P1 * P1 : SA * P1;
-  static constexpr int WN = 3 * P1 * P1 * P1;                // collocated: w per element
+  static constexpr int WN = 3 * P1 * P1 * P1;  // collocated: w per element
   static constexpr int cmax(int a, int b) { return a > b ? a : b; }
-  static constexpr int REGA =
-      (KIND == KIND_COLLOC) ? cmax(LAT, NE * YEN) : cmax(LAT, cmax(NE * T2N, NE * YEN));
+  static constexpr int REGA = (KIND == KIND_COLLOC) ? NE * YEN : cmax(NE * T2N, NE * YEN);
   static constexpr int REGB = (KIND == KIND_COLLOC) ? NE * WN : NE * T1N;
-  static constexpr int SMEM_BYTES = (REGA + REGB) * 8;
+  static constexpr int CARRY = LX * LY;
+  static constexpr int SMEM_BYTES = (REGA + REGB + 2 * LAT + 2 * CARRY) * 8;
   static constexpr int NC = (KIND == KIND_MASS) ? 1 : 6;
+  static constexpr int NQ1 = (KIND == KIND_COLLOC) ? P1 : Q;  // points per 1D direction
+  static constexpr int ITEMS3 = NE * NQ1 * NQ1;              // stage-3 items
+  __device__ static constexpr int lat(int i, int j, int k) { return k + LZ * j + LXS * i; }
 };
 
 // ---------------------------------------------------------------------------
-// Shared prologue / epilogue.
+// a4: items are (lattice row (j,k), element column s): a thread loads the row's
+// points i = p s .. p s + p - 1 (plus i = p BX for the last column) with
+// asynchronous 8-byte copies; the inner loop is unrolled so each point is a
+// compile-time offset from the row base.  Bricks that touch neither the mesh
+// boundary nor a ragged edge take a predicate-free path.
 // ---------------------------------------------------------------------------
-template <class C, int NT>
-__device__ __forceinline__ void load_brick_lattice(const FusedArgs& A, double* RA,
-                                                   long long I0, long long J0, long long K0l) {
-  for (int t = threadIdx.x; t < C::BLAT; t += NT) {
-    int i = t % C::LX, j = (t / C::LX) % C::LY, k = t / (C::LX * C::LY);
-    long long I = I0 + i, J = J0 + j, K = K0l + k;
-    double v = 0.0;
-    if (I < A.Nx && J < A.Ny && K < A.Nzl) {
-      v = A.x[I + A.Nx * (J + A.Ny * K)];
-      if (A.bc && ess_point(A, I, J, K)) v = 0.0;
-    }
-    RA[i + C::LX * j + C::PS * k] = v;
-  }
-}
-
-// Contributing local elements along one brick axis for brick-lattice index i.
-template <int p, int BN>
-__device__ __forceinline__ int local_elems(int i, int e0, int n, int* el, int* a) {
-  int q = i / p, r = i - q * p, k = 0;
-  if (r == 0 && q > 0 && e0 + q - 1 < n) { el[k] = q - 1; a[k] = p; ++k; }
-  if (q < BN && e0 + q < n) { el[k] = q; a[k] = r; ++k; }
-  return k;
-}
-
-// a8 + a9: in-brick deterministic sum; direct write or partial buffer.
-template <class C, int NT, int BX, int BY, int BZ, bool NATURAL>
-__device__ __forceinline__ void brick_sum_store(const FusedArgs& A, const double* RA, int brick,
-                                                int ex0, int ey0, int ez0, long long I0,
-                                                long long J0, long long K0l) {
-  constexpr int p = C::p, P1 = p + 1;
-  for (int t = threadIdx.x; t < C::BLAT; t += NT) {
-    int i = t % C::LX, j = (t / C::LX) % C::LY, k = t / (C::LX * C::LY);
-    long long I = I0 + i, J = J0 + j, K = K0l + k;
-    if (I >= A.Nx || J >= A.Ny || K >= A.Nzl) continue;
-    int exl[2], ax[2], eyl[2], ay[2], ezl[2], az[2];
-    int nxl = local_elems<p, BX>(i, ex0, A.nx, exl, ax);
-    int nyl = local_elems<p, BY>(j, ey0, A.ny, eyl, ay);
-    int nzl = local_elems<p, BZ>(k, ez0, A.nzl, ezl, az);
-    double s = 0.0;
-    for (int c = 0; c < nzl; ++c)
-      for (int b = 0; b < nyl; ++b)
-        for (int a = 0; a < nxl; ++a) {
-          int el = exl[a] + BX * (eyl[b] + BY * ezl[c]);
-          int off = NATURAL ? ax[a] + P1 * (ay[b] + P1 * az[c])
-                            : az[c] + P1 * ay[b] + C::SA * ax[a];
-          s += RA[el * C::YEN + off];
-        }
-    bool shared = (i == 0 && I > 0) || (i == C::LX - 1 && I < A.Nx - 1) ||
-                  (j == 0 && J > 0) || (j == C::LY - 1 && J < A.Ny - 1) ||
-                  (k == 0 && K > 0) || (k == C::LZ - 1 && K < A.Nzl - 1);
-    long long l = I + A.Nx * (J + A.Ny * K);
-    if (shared) {
-      A.bbuf[(long long)brick * C::BLAT + t] = s;
+template <class C, int NT, int BX>
+__device__ __forceinline__ void issue_lattice(const ColArgs& A, double* L, long long I0,
+                                              long long J0, long long K0l) {
+  constexpr int LX = C::LX, LY = C::LY, LZ = C::LZ, p = C::p;
+  const long long nvx = A.Nx - I0;  // lattice points of this brick inside the mesh along x
+  const long long Kg0 = K0l + A.K0;
+  const bool interior = I0 > 0 && I0 + LX < A.Nx && J0 > 0 && J0 + LY < A.Ny &&
+                        (!A.bc || (Kg0 > 0 && Kg0 + LZ < A.NzG));
+  for (int it = vtid(); it < LY * LZ * BX; it += NT) {
+    const int sx = it % BX, r = it / BX, j = r % LY, k = r / LY;
+    const long long J = J0 + j, K = K0l + k;
+    double* dst = L + C::lat(p * sx, j, k);
+    if (interior) {
+      const double* src = A.x + I0 + p * sx + A.Nx * (J + A.Ny * K);
+#pragma unroll
+      for (int ii = 0; ii < p; ++ii) cp_async8(dst + C::LXS * ii, src + ii, true);
+      if (sx == BX - 1) cp_async8(dst + C::LXS * p, src + p, true);
     } else {
-      if (A.bc && ess_point(A, I, J, K)) s = A.x[l];
-      A.y[l] = s;
+      const long long Kg = K + A.K0;
+      const bool rin = J < A.Ny;
+      const bool ress = A.bc && (J == 0 || J == A.Ny - 1 || Kg == 0 || Kg == A.NzG - 1);
+      const double* src = A.x + (rin ? I0 + A.Nx * (J + A.Ny * K) : 0);
+#pragma unroll
+      for (int ii = 0; ii <= p; ++ii) {
+        if (ii < p || sx == BX - 1) {
+          const long long i = p * sx + ii;
+          const bool valid = rin && !ress && i < nvx &&
+                             !(A.bc && ((I0 + i) == 0 || (I0 + i) == A.Nx - 1));
+          cp_async8(dst + C::LXS * ii, valid ? src + i : A.x, valid);
+        }
+      }
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// a8 + a9 for one brick (element layer ez of a column).  Items are (lattice
+// row (j,k), element column s) like issue_lattice.  Along x and y a lattice
+// index has a "lower" contribution (element q-1, local node p) on an element
+// face and a "primary" one (element q, node i - p q); along z there is one
+// element layer (node k).  Ascending element order: y outer, x inner.  k == 0
+// adds the carried top plane of the previous brick first; k == p stores into
+// the carry unless the brick ends the unit.
+// ---------------------------------------------------------------------------
+template <class C, int NT, int BX, int BY, bool NATURAL>
+__device__ __forceinline__ void brick_epilogue(const ColArgs& A, const double* RA,
+                                               const double* carry_in, double* carry_out,
+                                               long long brick, int ex0, int ey0, long long I0,
+                                               long long J0, long long K0l, bool first,
+                                               bool last) {
+  constexpr int p = C::p, P1 = p + 1, LX = C::LX, LY = C::LY, YEN = C::YEN;
+  const long long nvx = A.Nx - I0;
+  const bool xhi_sh = I0 + LX - 1 < A.Nx - 1;
+  for (int it = vtid(); it < LY * P1 * BX; it += NT) {
+    const int sx = it % BX, r = it / BX, j = r % LY, k = r / LY;
+    const long long J = J0 + j, K = K0l + k, Kg = K + A.K0;
+    if (J >= A.Ny) continue;
+    const int qj = j / p, rj = j - qj * p;
+    const bool vy[2] = {rj == 0 && qj > 0 && ey0 + qj - 1 < A.ny, qj < BY && ey0 + qj < A.ny};
+    int base[2];
+#pragma unroll
+    for (int cy = 0; cy < 2; ++cy) {
+      const int ely = cy ? qj : qj - 1, ay = cy ? rj : p;
+      base[cy] = BX * ely * YEN + (NATURAL ? P1 * (ay + P1 * k) : k + P1 * ay);
+    }
+    const bool ok_s = ex0 + sx < A.nx;                  // element column sx exists
+    const bool ok_l = sx > 0 && ex0 + sx - 1 < A.nx;    // element column sx-1 exists
+    const bool to_carry = (k == p) && !last;
+    const bool from_carry = (k == 0) && !first;
+    const bool row_sh = (j == 0 && J > 0) || (j == LY - 1 && J < A.Ny - 1) ||
+                        (k == 0 && first && K > 0) || (k == p && last && K < A.Nzl - 1);
+    const bool row_ess = A.bc && (J == 0 || J == A.Ny - 1 || Kg == 0 || Kg == A.NzG - 1);
+    const long long gl = I0 + A.Nx * (J + A.Ny * K);
+    double* bb = A.bbuf + brick * C::BLAT + LX * (j + LY * k);
+    const double* cin = carry_in + LX * j;
+    double* cout = carry_out + LX * j;
+#pragma unroll
+    for (int ii = 0; ii <= p; ++ii) {
+      // ii == p is the brick's last lattice column, handled by the last segment
+      const int i = p * sx + ii;
+      if ((ii < p || sx == BX - 1) && i < nvx) {
+        double s = from_carry ? cin[i] : 0.0;
+#pragma unroll
+        for (int cy = 0; cy < 2; ++cy) {
+          if (vy[cy]) {
+            if (ii == 0) {
+              if (ok_l) s += RA[base[cy] + (sx - 1) * YEN + (NATURAL ? p : C::SA * p)];
+              if (ok_s) s += RA[base[cy] + sx * YEN];
+            } else if (ii < p) {
+              if (ok_s) s += RA[base[cy] + sx * YEN + (NATURAL ? ii : C::SA * ii)];
+            } else {  // i = p*BX: lower contribution of the last element column
+              if (ok_s) s += RA[base[cy] + sx * YEN + (NATURAL ? p : C::SA * p)];
+            }
+          }
+        }
+        if (to_carry) {
+          cout[i] = s;
+        } else {
+          const bool sh = row_sh || (i == 0 && I0 > 0) || (i == LX - 1 && xhi_sh);
+          if (sh) {
+            bb[i] = s;
+          } else {
+            if (row_ess || (A.bc && (I0 + i == 0 || i == nvx - 1))) s = A.x[gl + i];
+            A.y[gl + i] = s;
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The CTA's brick sequence: units u = blockIdx.x, blockIdx.x + G, ...; within a
+// unit the element layers z0 .. z1-1 of one column.  Pipelining crosses unit
+// boundaries (the next brick may start a new unit).
+// ---------------------------------------------------------------------------
+struct Brick {
+  int u, bx, by, z0, z1, ez;  // u >= nunits => past the end
+};
+__device__ __forceinline__ Brick unit_first(const ColArgs& A, int u) {
+  Brick b;
+  b.u = u;
+  if (u >= A.nunits) { b.bx = b.by = b.z0 = b.z1 = b.ez = 0; return b; }
+  const int ncol = A.nbx * A.nby, col = u % ncol, chunk = u / ncol;
+  b.bx = col % A.nbx;
+  b.by = col / A.nbx;
+  b.z0 = chunk * A.zc;
+  b.z1 = min(A.nzl, b.z0 + A.zc);
+  b.ez = b.z0;
+  return b;
+}
+__device__ __forceinline__ Brick brick_next(const ColArgs& A, Brick b) {
+  if (b.ez + 1 < b.z1) { ++b.ez; return b; }
+  return unit_first(A, b.u + gridDim.x);
+}
+
+// mbarrier / bulk-copy (TMA) helpers.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{ .reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra LAB_WAIT;\n"
+      "}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// qdata staging slot per element: NC*NQ^3 doubles, widened to 16-byte
+// boundaries (+2 doubles) because bulk copies move 16-byte granules.
+template <class C>
+struct Stage {
+  static constexpr int PER = C::NC * C::NQ1 * C::NQ1 * C::NQ1;  // doubles per element
+  static constexpr int SLOT = ((PER + 2) + 1) / 2 * 2;
+};
+
+// Thread 0: one bulk copy per element of brick b into staging buffer qs;
+// arms the buffer's mbarrier with the byte count.  Elements outside the mesh
+// are skipped.
+template <class C, int BX, int BY>
+__device__ __forceinline__ void issue_qdata(const ColArgs& A, const Brick& b, double* qs,
+                                            unsigned long long* bar) {
+  if (threadIdx.x != 0 || b.u >= A.nunits) return;
+  constexpr long long per = (long long)Stage<C>::PER * 8;
+  unsigned total = 0;
+  long long lo[BX * BY], hi[BX * BY];
+#pragma unroll
+  for (int el = 0; el < BX * BY; ++el) {
+    const int ex = b.bx * BX + el % BX, ey = b.by * BY + el / BX;
+    lo[el] = hi[el] = 0;
+    if (ex < A.nx && ey < A.ny) {
+      const long long e = ex + (long long)A.nx * (ey + (long long)A.ny * b.ez);
+      lo[el] = (e * per) & ~15LL;
+      hi[el] = ((e + 1) * per + 15) & ~15LL;
+      total += (unsigned)(hi[el] - lo[el]);
+    }
+  }
+  fence_proxy_async();
+  mbar_expect_tx(bar, total);
+  const char* base = reinterpret_cast<const char*>(A.qd);
+#pragma unroll
+  for (int el = 0; el < BX * BY; ++el)
+    if (hi[el] > lo[el])
+      bulk_g2s(qs + el * Stage<C>::SLOT, base + lo[el], (unsigned)(hi[el] - lo[el]), bar);
+}
+
+// Offset (0 or 1 double) of element (ex,ey,ez)'s data inside its staging slot.
+template <class C>
+__device__ __forceinline__ int stage_off(const ColArgs& A, int ex, int ey, int ez) {
+  constexpr long long per = (long long)Stage<C>::PER * 8;
+  if (per % 16 == 0) return 0;
+  const long long e = ex + (long long)A.nx * (ey + (long long)A.ny * ez);
+  return (int)(((e * per) & 15LL) >> 3);
 }
 
 // ---------------------------------------------------------------------------
 // General kernel: mass (BP1) and diffusion (BP3) with any (P1, Q) tables.
+// NBUF = qdata staging buffers (2: next brick's copy overlaps the whole current
+// brick; 1: issued right after stage 3 consumed the buffer).
 // ---------------------------------------------------------------------------
-template <int KIND, int P1, int Q, int BX, int BY, int BZ, int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) fused_brick(const Tab<P1, Q> T, FusedArgs A) {
-  using C = Cfg<KIND, P1, Q, BX, BY, BZ>;
-  constexpr int p = P1 - 1, NE = C::NE, Qp = C::Qp, S2 = C::S2, QQP = C::QQP;
+template <int KIND, int P1, int Q, int BX, int BY, int NT, int NBUF, int MAXR>
+__global__ void __maxnreg__(MAXR) fused_column(const __grid_constant__ Tab<P1, Q> T, const __grid_constant__ ColArgs A) {
+  using C = Cfg<KIND, P1, Q, BX, BY>;
+  using SG = Stage<C>;
+  constexpr int p = P1 - 1, NE = C::NE, Qp = C::Qp, S2 = C::S2, NC = C::NC;
+  constexpr int Q2 = Q * Q, Q3 = Q * Q * Q;
   constexpr bool DIFF = KIND == KIND_DIFF;
-  extern __shared__ double smem[];
-  double* RA = smem;
-  double* RB = smem + C::REGA;
+  static_assert(NT >= C::ITEMS3, "one stage-3 item per thread");
+  static_assert(NBUF == 1 || NBUF == 2, "staging buffers");
+  extern __shared__ __align__(16) double smem[];
+  double* QS = smem;                     // NBUF x NE x SLOT (16-byte aligned)
+  double* RA = QS + NBUF * NE * SG::SLOT;
+  double* RB = RA + C::REGA;
+  double* LB = RB + C::REGB;
+  double* CY = LB + 2 * C::LAT;
+  __shared__ __align__(8) unsigned long long bars[2];
   const int tid = threadIdx.x;
-  const int brick = blockIdx.x;
-  const int ex0 = (brick % A.nbx) * BX;
-  const int ey0 = ((brick / A.nbx) % A.nby) * BY;
-  const int ez0 = (brick / (A.nbx * A.nby)) * BZ;
-  const long long I0 = (long long)p * ex0, J0 = (long long)p * ey0, K0l = (long long)p * ez0;
-
-  load_brick_lattice<C, NT>(A, RA, I0, J0, K0l);
-  __syncthreads();
-
-  // ---- stage 1: contract x.  item (el, b, c), c fastest.
-  for (int it = tid; it < NE * P1 * P1; it += NT) {
-    const int el = it / (P1 * P1), r = it % (P1 * P1), c = r % P1, b = r / P1;
-    const int exl = el % BX, eyl = (el / BX) % BY, ezl = el / (BX * BY);
-    const double* xl = RA + p * exl + C::LX * (p * eyl + b) + C::PS * (p * ezl + c);
-    double xa[P1];
-#pragma unroll
-    for (int a = 0; a < P1; ++a) xa[a] = xl[a];
-    double* t1 = RB + el * C::T1N + Qp * c + S2 * b;
-#pragma unroll
-    for (int qx = 0; qx < Q; ++qx) {
-      double sb = 0.0, sg = 0.0;
-#pragma unroll
-      for (int a = 0; a < P1; ++a) {
-        sb = fma(T.B[qx * P1 + a], xa[a], sb);
-        if (DIFF) sg = fma(T.G[qx * P1 + a], xa[a], sg);
-      }
-      t1[qx] = sb;                       // B_x x
-      if (DIFF) t1[S2 * P1 + qx] = sg;   // G_x x
-    }
+  const bool has3 = tid < C::ITEMS3;
+  const int el3 = tid / Q2, i3 = tid % Q2;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  // ---- stage 2: contract y.  item (el, qx, c), qx fastest.
-  for (int it = tid; it < NE * Q * P1; it += NT) {
-    const int el = it / (Q * P1), r = it % (Q * P1), qx = r % Q, c = r / Q;
-    const double* t1 = RB + el * C::T1N + qx + Qp * c;
-    double vb[P1], vg[P1];
-#pragma unroll
-    for (int b = 0; b < P1; ++b) {
-      vb[b] = t1[S2 * b];
-      if (DIFF) vg[b] = t1[S2 * P1 + S2 * b];
-    }
-    double* t2 = RA + el * C::T2N + qx + Q * Q * c;
-#pragma unroll
-    for (int qy = 0; qy < Q; ++qy) {
-      double bb = 0.0, gb = 0.0, bg = 0.0;
-#pragma unroll
-      for (int b = 0; b < P1; ++b) {
-        bb = fma(T.B[qy * P1 + b], vb[b], bb);
-        if (DIFF) {
-          gb = fma(T.B[qy * P1 + b], vg[b], gb);
-          bg = fma(T.G[qy * P1 + b], vb[b], bg);
-        }
-      }
-      if (DIFF) {
-        t2[Q * qy] = gb;            // G_x B_y
-        t2[QQP + Q * qy] = bg;      // B_x G_y
-        t2[2 * QQP + Q * qy] = bb;  // B_x B_y
-      } else {
-        t2[Q * qy] = bb;
-      }
-    }
-  }
+  Brick cur = unit_first(A, blockIdx.x);
+  if (cur.u >= A.nunits) return;
+  issue_qdata<C, BX, BY>(A, cur, QS, &bars[0]);
+  issue_lattice<C, NT, BX>(A, LB, (long long)p * cur.bx * BX, (long long)p * cur.by * BY,
+                       (long long)p * cur.ez);
+  cp_async_wait_all();
   __syncthreads();
+  unsigned phase = 0;  // bit b: parity of the next wait on bars[b]
 
-  // ---- stage 3: contract z in registers, pointwise D, z-transpose.
-  //      item (el, qx, qy), qx fastest: qdata reads are coalesced.
-  for (int it = tid; it < NE * Q * Q; it += NT) {
-    const int el = it / (Q * Q), i3 = it % (Q * Q);
-    const int exl = el % BX, eyl = (el / BX) % BY, ezl = el / (BX * BY);
-    const int ex = ex0 + exl, ey = ey0 + eyl, ez = ez0 + ezl;
-    if (ex >= A.nx || ey >= A.ny || ez >= A.nzl) continue;
-    const long long e = ex + (long long)A.nx * (ey + (long long)A.ny * ez);
-    const double* qd = A.qd + e * (C::NC * Q * Q * Q) + i3;
-    double* t2 = RA + el * C::T2N + i3;
-    if (DIFF) {
-      double g0[P1], g1[P1], g2[P1], s0[P1], s1[P1], s2[P1];
-#pragma unroll
-      for (int c = 0; c < P1; ++c) {
-        g0[c] = t2[Q * Q * c];
-        g1[c] = t2[QQP + Q * Q * c];
-        g2[c] = t2[2 * QQP + Q * Q * c];
-        s0[c] = s1[c] = s2[c] = 0.0;
-      }
-#pragma unroll
-      for (int qz = 0; qz < Q; ++qz) {
-        const double* d = qd + qz * Q * Q;
-        const double d00 = ld_stream(d), d01 = ld_stream(d + Q * Q * Q),
-                     d02 = ld_stream(d + 2 * Q * Q * Q), d11 = ld_stream(d + 3 * Q * Q * Q),
-                     d12 = ld_stream(d + 4 * Q * Q * Q), d22 = ld_stream(d + 5 * Q * Q * Q);
-        double u0 = 0.0, u1 = 0.0, u2 = 0.0;
-#pragma unroll
-        for (int c = 0; c < P1; ++c) {
-          u0 = fma(T.B[qz * P1 + c], g0[c], u0);
-          u1 = fma(T.B[qz * P1 + c], g1[c], u1);
-          u2 = fma(T.G[qz * P1 + c], g2[c], u2);
-        }
-        const double w0 = d00 * u0 + d01 * u1 + d02 * u2;
-        const double w1 = d01 * u0 + d11 * u1 + d12 * u2;
-        const double w2 = d02 * u0 + d12 * u1 + d22 * u2;
-#pragma unroll
-        for (int c = 0; c < P1; ++c) {
-          s0[c] = fma(T.B[qz * P1 + c], w0, s0[c]);
-          s1[c] = fma(T.B[qz * P1 + c], w1, s1[c]);
-          s2[c] = fma(T.G[qz * P1 + c], w2, s2[c]);
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < P1; ++c) {
-        t2[Q * Q * c] = s0[c];
-        t2[QQP + Q * Q * c] = s1[c];
-        t2[2 * QQP + Q * Q * c] = s2[c];
-      }
-    } else {
-      double g[P1], s[P1];
-#pragma unroll
-      for (int c = 0; c < P1; ++c) { g[c] = t2[Q * Q * c]; s[c] = 0.0; }
-#pragma unroll
-      for (int qz = 0; qz < Q; ++qz) {
-        const double d = ld_stream(qd + qz * Q * Q);
-        double u = 0.0;
-#pragma unroll
-        for (int c = 0; c < P1; ++c) u = fma(T.B[qz * P1 + c], g[c], u);
-        const double v = d * u;
-#pragma unroll
-        for (int c = 0; c < P1; ++c) s[c] = fma(T.B[qz * P1 + c], v, s[c]);
-      }
-#pragma unroll
-      for (int c = 0; c < P1; ++c) t2[Q * Q * c] = s[c];
+  for (int k = 0; cur.u < A.nunits; ++k) {
+    const int tid = vtid();
+    const Brick nxt = brick_next(A, cur);
+    const int ex0 = cur.bx * BX, ey0 = cur.by * BY, ez = cur.ez;
+    const long long I0 = (long long)p * ex0, J0 = (long long)p * ey0;
+    const int qb = NBUF == 2 ? (k & 1) : 0;
+    double* L = LB + (k & 1) * C::LAT;
+    if (nxt.u < A.nunits) {
+      issue_lattice<C, NT, BX>(A, LB + ((k + 1) & 1) * C::LAT, (long long)p * nxt.bx * BX,
+                           (long long)p * nxt.by * BY, (long long)p * nxt.ez);
+      if (NBUF == 2) issue_qdata<C, BX, BY>(A, nxt, QS + ((k + 1) & 1) * NE * SG::SLOT,
+                                            &bars[(k + 1) & 1]);
     }
-  }
-  __syncthreads();
 
-  // ---- stage 2^T: contract qy.  item (el, qx, c), qx fastest.
-  for (int it = tid; it < NE * Q * P1; it += NT) {
-    const int el = it / (Q * P1), r = it % (Q * P1), qx = r % Q, c = r / Q;
-    const double* t2 = RA + el * C::T2N + qx + Q * Q * c;
-    double* t1 = RB + el * C::T1N + qx + Qp * c;
-    if (DIFF) {
-      double v0[Q], v1[Q], v2[Q];
+    // ---- stage 1: contract x.  item (el, b, c), c fastest.
+    for (int it = tid; it < NE * P1 * P1; it += NT) {
+      const int el = it / (P1 * P1), r = it % (P1 * P1), c = r % P1, b = r / P1;
+      const double* xl = L + C::lat(p * (el % BX), p * (el / BX) + b, c);
+      double xa[P1];
 #pragma unroll
-      for (int qy = 0; qy < Q; ++qy) {
-        v0[qy] = t2[Q * qy];
-        v1[qy] = t2[QQP + Q * qy];
-        v2[qy] = t2[2 * QQP + Q * qy];
-      }
-#pragma unroll
-      for (int b = 0; b < P1; ++b) {
-        double rg = 0.0, rb = 0.0;
-#pragma unroll
-        for (int qy = 0; qy < Q; ++qy) {
-          rg = fma(T.B[qy * P1 + b], v0[qy], rg);
-          rb = fma(T.G[qy * P1 + b], v1[qy], rb);
-          rb = fma(T.B[qy * P1 + b], v2[qy], rb);
-        }
-        t1[S2 * b] = rg;            // -> G_x^T
-        t1[S2 * P1 + S2 * b] = rb;  // -> B_x^T
-      }
-    } else {
-      double v[Q];
-#pragma unroll
-      for (int qy = 0; qy < Q; ++qy) v[qy] = t2[Q * qy];
-#pragma unroll
-      for (int b = 0; b < P1; ++b) {
-        double rb = 0.0;
-#pragma unroll
-        for (int qy = 0; qy < Q; ++qy) rb = fma(T.B[qy * P1 + b], v[qy], rb);
-        t1[S2 * b] = rb;
-      }
-    }
-  }
-  __syncthreads();
-
-  // ---- stage 1^T: contract qx.  item (el, b, c), c fastest -> y_e[a][b][c].
-  for (int it = tid; it < NE * P1 * P1; it += NT) {
-    const int el = it / (P1 * P1), r = it % (P1 * P1), c = r % P1, b = r / P1;
-    const double* t1 = RB + el * C::T1N + Qp * c + S2 * b;
-    double rg[Q], rb[Q];
-#pragma unroll
-    for (int qx = 0; qx < Q; ++qx) {
-      if (DIFF) {
-        rg[qx] = t1[qx];
-        rb[qx] = t1[S2 * P1 + qx];
-      } else {
-        rb[qx] = t1[qx];
-      }
-    }
-    double* ye = RA + el * C::YEN + c + P1 * b;
-#pragma unroll
-    for (int a = 0; a < P1; ++a) {
-      double s = 0.0;
+      for (int a = 0; a < P1; ++a) xa[a] = xl[C::LXS * a];
+      double* t1 = RB + el * C::T1N + Qp * c + S2 * b;
 #pragma unroll
       for (int qx = 0; qx < Q; ++qx) {
-        s = fma(T.B[qx * P1 + a], rb[qx], s);
-        if (DIFF) s = fma(T.G[qx * P1 + a], rg[qx], s);
+        double sb = 0.0, sg = 0.0;
+#pragma unroll
+        for (int a = 0; a < P1; ++a) {
+          sb = fma(T.B[qx * P1 + a], xa[a], sb);
+          if (DIFF) sg = fma(T.G[qx * P1 + a], xa[a], sg);
+        }
+        t1[qx] = sb;                      // B_x x
+        if (DIFF) t1[S2 * P1 + qx] = sg;  // G_x x
       }
-      ye[C::SA * a] = s;
     }
-  }
-  __syncthreads();
+    __syncthreads();
 
-  brick_sum_store<C, NT, BX, BY, BZ, false>(A, RA, brick, ex0, ey0, ez0, I0, J0, K0l);
+    // ---- stage 2: contract y.  item (el, qx, c), qx fastest.
+    for (int it = tid; it < NE * Q * P1; it += NT) {
+      const int el = it / (Q * P1), r = it % (Q * P1), qx = r % Q, c = r / Q;
+      const double* t1 = RB + el * C::T1N + qx + Qp * c;
+      double vb[P1], vg[P1];
+#pragma unroll
+      for (int b = 0; b < P1; ++b) {
+        vb[b] = t1[S2 * b];
+        if (DIFF) vg[b] = t1[S2 * P1 + S2 * b];
+      }
+      double* t2 = RA + el * C::T2N + qx + Q * c;
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy) {
+        double bb = 0.0, gb = 0.0, bg = 0.0;
+#pragma unroll
+        for (int b = 0; b < P1; ++b) {
+          bb = fma(T.B[qy * P1 + b], vb[b], bb);
+          if (DIFF) {
+            gb = fma(T.B[qy * P1 + b], vg[b], gb);
+            bg = fma(T.G[qy * P1 + b], vb[b], bg);
+          }
+        }
+        if (DIFF) {
+          t2[C::RS * qy] = gb;               // G_x B_y
+          t2[C::T2C + C::RS * qy] = bg;      // B_x G_y
+          t2[2 * C::T2C + C::RS * qy] = bb;  // B_x B_y
+        } else {
+          t2[C::RS * qy] = bb;
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- stage 3: contract z in registers, pointwise D (staged in smem by the
+    //      bulk copy), z-transpose.  item (el, qx, qy) = this thread's column.
+    mbar_wait(&bars[qb], (phase >> qb) & 1);
+    phase ^= 1u << qb;
+    if (has3 && ex0 + el3 % BX < A.nx && ey0 + el3 / BX < A.ny) {
+      const int qx3 = i3 % Q, qy3 = i3 / Q;
+      double* t2 = RA + el3 * C::T2N + qx3 + C::RS * qy3;
+      const double* dq = QS + (qb * NE + el3) * SG::SLOT +
+                         stage_off<C>(A, ex0 + el3 % BX, ey0 + el3 / BX, ez) + i3;
+      if (DIFF) {
+        double g0[P1], g1[P1], g2[P1], s0[P1], s1[P1], s2[P1];
+#pragma unroll
+        for (int c = 0; c < P1; ++c) {
+          g0[c] = t2[Q * c];
+          g1[c] = t2[C::T2C + Q * c];
+          g2[c] = t2[2 * C::T2C + Q * c];
+          s0[c] = s1[c] = s2[c] = 0.0;
+        }
+#pragma unroll
+        for (int qz = 0; qz < Q; ++qz) {
+          const double* d = dq + qz * Q2;
+          double u0 = 0.0, u1 = 0.0, u2 = 0.0;
+#pragma unroll
+          for (int c = 0; c < P1; ++c) {
+            u0 = fma(T.B[qz * P1 + c], g0[c], u0);
+            u1 = fma(T.B[qz * P1 + c], g1[c], u1);
+            u2 = fma(T.G[qz * P1 + c], g2[c], u2);
+          }
+          const double d00 = d[0], d01 = d[Q3], d02 = d[2 * Q3], d11 = d[3 * Q3],
+                       d12 = d[4 * Q3], d22 = d[5 * Q3];
+          const double w0 = d00 * u0 + d01 * u1 + d02 * u2;
+          const double w1 = d01 * u0 + d11 * u1 + d12 * u2;
+          const double w2 = d02 * u0 + d12 * u1 + d22 * u2;
+#pragma unroll
+          for (int c = 0; c < P1; ++c) {
+            s0[c] = fma(T.B[qz * P1 + c], w0, s0[c]);
+            s1[c] = fma(T.B[qz * P1 + c], w1, s1[c]);
+            s2[c] = fma(T.G[qz * P1 + c], w2, s2[c]);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < P1; ++c) {
+          t2[Q * c] = s0[c];
+          t2[C::T2C + Q * c] = s1[c];
+          t2[2 * C::T2C + Q * c] = s2[c];
+        }
+      } else {
+        double g[P1], s[P1];
+#pragma unroll
+        for (int c = 0; c < P1; ++c) { g[c] = t2[Q * c]; s[c] = 0.0; }
+#pragma unroll
+        for (int qz = 0; qz < Q; ++qz) {
+          double uq = 0.0;
+#pragma unroll
+          for (int c = 0; c < P1; ++c) uq = fma(T.B[qz * P1 + c], g[c], uq);
+          const double v = dq[qz * Q2] * uq;
+#pragma unroll
+          for (int c = 0; c < P1; ++c) s[c] = fma(T.B[qz * P1 + c], v, s[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < P1; ++c) t2[Q * c] = s[c];
+      }
+    }
+    __syncthreads();
+    if (NBUF == 1 && nxt.u < A.nunits) issue_qdata<C, BX, BY>(A, nxt, QS, &bars[0]);
+
+    // ---- stage 2^T: contract qy.  item (el, qx, c), qx fastest.
+    for (int it = tid; it < NE * Q * P1; it += NT) {
+      const int el = it / (Q * P1), r = it % (Q * P1), qx = r % Q, c = r / Q;
+      const double* t2 = RA + el * C::T2N + qx + Q * c;
+      double* t1 = RB + el * C::T1N + qx + Qp * c;
+      if (DIFF) {
+        double v0[Q], v1[Q], v2[Q];
+#pragma unroll
+        for (int qy = 0; qy < Q; ++qy) {
+          v0[qy] = t2[C::RS * qy];
+          v1[qy] = t2[C::T2C + C::RS * qy];
+          v2[qy] = t2[2 * C::T2C + C::RS * qy];
+        }
+#pragma unroll
+        for (int b = 0; b < P1; ++b) {
+          double rg = 0.0, rb = 0.0;
+#pragma unroll
+          for (int qy = 0; qy < Q; ++qy) {
+            rg = fma(T.B[qy * P1 + b], v0[qy], rg);
+            rb = fma(T.G[qy * P1 + b], v1[qy], rb);
+            rb = fma(T.B[qy * P1 + b], v2[qy], rb);
+          }
+          t1[S2 * b] = rg;            // -> G_x^T
+          t1[S2 * P1 + S2 * b] = rb;  // -> B_x^T
+        }
+      } else {
+        double v[Q];
+#pragma unroll
+        for (int qy = 0; qy < Q; ++qy) v[qy] = t2[C::RS * qy];
+#pragma unroll
+        for (int b = 0; b < P1; ++b) {
+          double rb = 0.0;
+#pragma unroll
+          for (int qy = 0; qy < Q; ++qy) rb = fma(T.B[qy * P1 + b], v[qy], rb);
+          t1[S2 * b] = rb;
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- stage 1^T: contract qx.  item (el, b, c), c fastest -> y_e[a][b][c].
+    for (int it = tid; it < NE * P1 * P1; it += NT) {
+      const int el = it / (P1 * P1), r = it % (P1 * P1), c = r % P1, b = r / P1;
+      const double* t1 = RB + el * C::T1N + Qp * c + S2 * b;
+      double rg[Q], rb[Q];
+#pragma unroll
+      for (int qx = 0; qx < Q; ++qx) {
+        if (DIFF) {
+          rg[qx] = t1[qx];
+          rb[qx] = t1[S2 * P1 + qx];
+        } else {
+          rb[qx] = t1[qx];
+        }
+      }
+      double* ye = RA + el * C::YEN + c + P1 * b;
+#pragma unroll
+      for (int a = 0; a < P1; ++a) {
+        double s = 0.0;
+#pragma unroll
+        for (int qx = 0; qx < Q; ++qx) {
+          s = fma(T.B[qx * P1 + a], rb[qx], s);
+          if (DIFF) s = fma(T.G[qx * P1 + a], rg[qx], s);
+        }
+        ye[C::SA * a] = s;
+      }
+    }
+    __syncthreads();
+
+    const long long brick = cur.bx + (long long)A.nbx * (cur.by + (long long)A.nby * ez);
+    brick_epilogue<C, NT, BX, BY, false>(A, RA, CY + ((ez + 1) & 1) * C::CARRY,
+                                         CY + (ez & 1) * C::CARRY, brick, ex0, ey0, I0, J0,
+                                         (long long)p * ez, ez == cur.z0, ez + 1 == cur.z1);
+    cp_async_wait_all();
+    __syncthreads();
+    cur = nxt;
+  }
 }
 
 // ---------------------------------------------------------------------------
 // Collocated diffusion kernel (BP5: GLL points = nodes, B1d = I, Q = P1).
 // u_x = G_x x, u_y = G_y x, u_z = G_z x; w = D u; y = G_x^T w_x + G_y^T w_y + G_z^T w_z.
 // ---------------------------------------------------------------------------
-template <int P1, int BX, int BY, int BZ, int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) fused_brick_colloc(const Tab<P1, P1> T, FusedArgs A) {
-  using C = Cfg<KIND_COLLOC, P1, P1, BX, BY, BZ>;
+template <int P1, int BX, int BY, int NT, int NBUF, int MAXR>
+__global__ void __maxnreg__(MAXR) fused_column_colloc(const __grid_constant__ Tab<P1, P1> T, const __grid_constant__ ColArgs A) {
+  using C = Cfg<KIND_COLLOC, P1, P1, BX, BY>;
+  using SG = Stage<C>;
   constexpr int p = P1 - 1, NE = C::NE, N2 = P1 * P1, N3 = P1 * P1 * P1;
-  extern __shared__ double smem[];
-  double* RA = smem;
-  double* RB = smem + C::REGA;
+  static_assert(NT >= C::ITEMS3, "one item per thread");
+  extern __shared__ __align__(16) double smem[];
+  double* QS = smem;
+  double* RA = QS + NBUF * NE * SG::SLOT;
+  double* RB = RA + C::REGA;
+  double* LB = RB + C::REGB;
+  double* CY = LB + 2 * C::LAT;
+  __shared__ __align__(8) unsigned long long bars[2];
   const int tid = threadIdx.x;
-  const int brick = blockIdx.x;
-  const int ex0 = (brick % A.nbx) * BX;
-  const int ey0 = ((brick / A.nbx) % A.nby) * BY;
-  const int ez0 = (brick / (A.nbx * A.nby)) * BZ;
-  const long long I0 = (long long)p * ex0, J0 = (long long)p * ey0, K0l = (long long)p * ez0;
-
-  load_brick_lattice<C, NT>(A, RA, I0, J0, K0l);
+  const bool has3 = tid < C::ITEMS3;
+  const int el3 = tid / N2, item = tid % N2, i = item % P1, j = item / P1;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
 
-  // ---- forward: item (el, i, j), i fastest; z-column k in registers.
-  for (int it = tid; it < NE * N2; it += NT) {
-    const int el = it / N2, item = it % N2, i = item % P1, j = item / P1;
-    const int exl = el % BX, eyl = (el / BX) % BY, ezl = el / (BX * BY);
-    const int ex = ex0 + exl, ey = ey0 + eyl, ez = ez0 + ezl;
-    if (ex >= A.nx || ey >= A.ny || ez >= A.nzl) continue;
-    const long long e = ex + (long long)A.nx * (ey + (long long)A.ny * ez);
-    const double* qd = A.qd + e * (6 * N3) + item;
-    const double* xl = RA + p * exl + C::LX * (p * eyl) + C::PS * (p * ezl);
-    double Gi[P1], Gj[P1], xz[P1];
-#pragma unroll
-    for (int a = 0; a < P1; ++a) {
-      Gi[a] = T.G[i * P1 + a];
-      Gj[a] = T.G[j * P1 + a];
-      xz[a] = xl[i + C::LX * j + C::PS * a];
+  Brick cur = unit_first(A, blockIdx.x);
+  if (cur.u >= A.nunits) return;
+  issue_qdata<C, BX, BY>(A, cur, QS, &bars[0]);
+  issue_lattice<C, NT, BX>(A, LB, (long long)p * cur.bx * BX, (long long)p * cur.by * BY,
+                       (long long)p * cur.ez);
+  cp_async_wait_all();
+  __syncthreads();
+  unsigned phase = 0;
+
+  for (int k = 0; cur.u < A.nunits; ++k) {
+    const int tid = vtid();
+    const Brick nxt = brick_next(A, cur);
+    const int ex0 = cur.bx * BX, ey0 = cur.by * BY, ez = cur.ez;
+    const long long I0 = (long long)p * ex0, J0 = (long long)p * ey0;
+    const int qb = NBUF == 2 ? (k & 1) : 0;
+    double* L = LB + (k & 1) * C::LAT;
+    if (nxt.u < A.nunits) {
+      issue_lattice<C, NT, BX>(A, LB + ((k + 1) & 1) * C::LAT, (long long)p * nxt.bx * BX,
+                           (long long)p * nxt.by * BY, (long long)p * nxt.ez);
+      if (NBUF == 2) issue_qdata<C, BX, BY>(A, nxt, QS + ((k + 1) & 1) * NE * SG::SLOT,
+                                            &bars[(k + 1) & 1]);
     }
-    double* w = RB + el * C::WN + item;
-#pragma unroll
-    for (int k = 0; k < P1; ++k) {
-      double ux = 0.0, uy = 0.0, uz = 0.0;
+
+    // ---- forward: item (el, i, j), i fastest; z-column k in registers.
+    mbar_wait(&bars[qb], (phase >> qb) & 1);
+    phase ^= 1u << qb;
+    if (has3 && ex0 + el3 % BX < A.nx && ey0 + el3 / BX < A.ny) {
+      const double* xl = L + C::lat(p * (el3 % BX), p * (el3 / BX), 0);
+      const double* dq = QS + (qb * NE + el3) * SG::SLOT + item;
+      double Gi[P1], Gj[P1], xz[P1];
 #pragma unroll
       for (int a = 0; a < P1; ++a) {
-        ux = fma(Gi[a], xl[a + C::LX * j + C::PS * k], ux);
-        uy = fma(Gj[a], xl[i + C::LX * a + C::PS * k], uy);
-        uz = fma(T.G[k * P1 + a], xz[a], uz);
+        Gi[a] = T.G[i * P1 + a];
+        Gj[a] = T.G[j * P1 + a];
+        xz[a] = xl[C::lat(i, j, a)];
       }
-      const double* d = qd + k * N2;
-      const double d00 = ld_stream(d), d01 = ld_stream(d + N3), d02 = ld_stream(d + 2 * N3),
-                   d11 = ld_stream(d + 3 * N3), d12 = ld_stream(d + 4 * N3),
-                   d22 = ld_stream(d + 5 * N3);
-      w[N2 * k] = d00 * ux + d01 * uy + d02 * uz;
-      w[N3 + N2 * k] = d01 * ux + d11 * uy + d12 * uz;
-      w[2 * N3 + N2 * k] = d02 * ux + d12 * uy + d22 * uz;
-    }
-  }
-  __syncthreads();
-
-  // ---- transpose: item (el, a, b) -> y_e[a + P1 b + P1^2 c] for all c.
-  for (int it = tid; it < NE * N2; it += NT) {
-    const int el = it / N2, item = it % N2, a = item % P1, b = item / P1;
-    const double* w = RB + el * C::WN;
-    double Ga[P1], Gb[P1], wz[P1];
+      double* w = RB + el3 * C::WN + item;
 #pragma unroll
-    for (int k = 0; k < P1; ++k) {
-      Ga[k] = T.G[k * P1 + a];
-      Gb[k] = T.G[k * P1 + b];
-      wz[k] = w[2 * N3 + item + N2 * k];
-    }
-    double* ye = RA + el * C::YEN + item;
+      for (int kz = 0; kz < P1; ++kz) {
+        double ux = 0.0, uy = 0.0, uz = 0.0;
 #pragma unroll
-    for (int c = 0; c < P1; ++c) {
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < P1; ++k) {
-        s = fma(Ga[k], w[k + P1 * b + N2 * c], s);          // G_x^T w_x
-        s = fma(Gb[k], w[N3 + a + P1 * k + N2 * c], s);      // G_y^T w_y
-        s = fma(T.G[k * P1 + c], wz[k], s);                  // G_z^T w_z
+        for (int a = 0; a < P1; ++a) {
+          ux = fma(Gi[a], xl[C::lat(a, j, kz)], ux);
+          uy = fma(Gj[a], xl[C::lat(i, a, kz)], uy);
+          uz = fma(T.G[kz * P1 + a], xz[a], uz);
+        }
+        const double* d = dq + kz * N2;
+        const double d00 = d[0], d01 = d[N3], d02 = d[2 * N3], d11 = d[3 * N3], d12 = d[4 * N3],
+                     d22 = d[5 * N3];
+        w[N2 * kz] = d00 * ux + d01 * uy + d02 * uz;
+        w[N3 + N2 * kz] = d01 * ux + d11 * uy + d12 * uz;
+        w[2 * N3 + N2 * kz] = d02 * ux + d12 * uy + d22 * uz;
       }
-      ye[N2 * c] = s;
     }
-  }
-  __syncthreads();
+    __syncthreads();
+    if (NBUF == 1 && nxt.u < A.nunits) issue_qdata<C, BX, BY>(A, nxt, QS, &bars[0]);
 
-  brick_sum_store<C, NT, BX, BY, BZ, true>(A, RA, brick, ex0, ey0, ez0, I0, J0, K0l);
+    // ---- transpose: item (el, a, b) -> y_e[a + P1 b + P1^2 c] for all c.
+    for (int it = tid; it < NE * N2; it += NT) {
+      const int el = it / N2, itm = it % N2, a = itm % P1, b = itm / P1;
+      const double* w = RB + el * C::WN;
+      double Ga[P1], Gb[P1], wz[P1];
+#pragma unroll
+      for (int kz = 0; kz < P1; ++kz) {
+        Ga[kz] = T.G[kz * P1 + a];
+        Gb[kz] = T.G[kz * P1 + b];
+        wz[kz] = w[2 * N3 + itm + N2 * kz];
+      }
+      double* ye = RA + el * C::YEN + itm;
+#pragma unroll
+      for (int c = 0; c < P1; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int kz = 0; kz < P1; ++kz) {
+          s = fma(Ga[kz], w[kz + P1 * b + N2 * c], s);      // G_x^T w_x
+          s = fma(Gb[kz], w[N3 + a + P1 * kz + N2 * c], s);  // G_y^T w_y
+          s = fma(T.G[kz * P1 + c], wz[kz], s);              // G_z^T w_z
+        }
+        ye[N2 * c] = s;
+      }
+    }
+    __syncthreads();
+
+    const long long brick = cur.bx + (long long)A.nbx * (cur.by + (long long)A.nby * ez);
+    brick_epilogue<C, NT, BX, BY, true>(A, RA, CY + ((ez + 1) & 1) * C::CARRY,
+                                        CY + (ez & 1) * C::CARRY, brick, ex0, ey0, I0, J0,
+                                        (long long)p * ez, ez == cur.z0, ez + 1 == cur.z1);
+    cp_async_wait_all();
+    __syncthreads();
+    cur = nxt;
+  }
 }
 
 // ---------------------------------------------------------------------------
-// Per-P1 launch configurations (brick shape, threads per CTA, min CTAs/SM).
+// Per-P1 launch configuration: brick BX x BY x 1 elements, threads per CTA (one
+// stage-3 item per thread), qdata staging buffers.
 // ---------------------------------------------------------------------------
 template <int P1>
 struct Shape;
-//                                   BX BY BZ  NT  MINB
-template <> struct Shape<2> { static constexpr int BX = 8, BY = 4, BZ = 4, NT = 384, MINB = 1; };
-template <> struct Shape<3> { static constexpr int BX = 4, BY = 4, BZ = 2, NT = 512, MINB = 1; };
-template <> struct Shape<4> { static constexpr int BX = 4, BY = 2, BZ = 2, NT = 416, MINB = 1; };
-template <> struct Shape<5> { static constexpr int BX = 2, BY = 2, BZ = 2, NT = 288, MINB = 1; };
-template <> struct Shape<6> { static constexpr int BX = 2, BY = 2, BZ = 2, NT = 416, MINB = 1; };
-template <> struct Shape<7> { static constexpr int BX = 2, BY = 2, BZ = 1, NT = 256, MINB = 1; };
-template <> struct Shape<8> { static constexpr int BX = 2, BY = 2, BZ = 1, NT = 352, MINB = 1; };
-template <> struct Shape<9> { static constexpr int BX = 2, BY = 1, BZ = 1, NT = 224, MINB = 1; };
+//                                   BX BY  NT  NBUF  MAXR (registers per thread)
+template <> struct Shape<2> { static constexpr int BX = 8, BY = 4, NT = 288, NBUF = 2, MAXR = 128; };
+template <> struct Shape<3> { static constexpr int BX = 4, BY = 4, NT = 256, NBUF = 2, MAXR = 128; };
+template <> struct Shape<4> { static constexpr int BX = 4, BY = 2, NT = 224, NBUF = 2, MAXR = 128; };
+template <> struct Shape<5> { static constexpr int BX = 2, BY = 2, NT = 160, NBUF = 2, MAXR = 168; };
+template <> struct Shape<6> { static constexpr int BX = 2, BY = 2, NT = 224, NBUF = 2, MAXR = 168; };
+template <> struct Shape<7> { static constexpr int BX = 2, BY = 2, NT = 256, NBUF = 1, MAXR = 168; };
+template <> struct Shape<8> { static constexpr int BX = 2, BY = 1, NT = 192, NBUF = 2, MAXR = 232; };
+template <> struct Shape<9> { static constexpr int BX = 1, BY = 1, NT = 128, NBUF = 2, MAXR = 232; };
+
+template <int KIND, int P1, int Q, int BX, int BY, int NBUF>
+constexpr int smem_bytes() {
+  using C = Cfg<KIND, P1, Q, BX, BY>;
+  return C::SMEM_BYTES + NBUF * C::NE * Stage<C>::SLOT * 8;
+}
 
 struct FusedLaunch {
-  int BX, BY, BZ, blat;
+  int BX, BY, blat;
 };
 
-// Defined per P1 in fused_p*.cu: kind in {KIND_MASS, KIND_DIFF, KIND_COLLOC},
+// Defined per P1 in fused_p.cu: kind in {KIND_MASS, KIND_DIFF, KIND_COLLOC},
 // Q in {P1, P1+1} for MASS/DIFF and Q == P1 for COLLOC.  Returns false if the
 // combination is not instantiated.
 template <int P1>
-bool fused_launch(int kind, int Q, const double* B, const double* G, const FusedArgs& A,
-                  int nbricks, cudaStream_t s, cudaError_t* err);
+bool fused_launch(int kind, int Q, const double* B, const double* G, const ColArgs& A, int grid,
+                  cudaStream_t s, cudaError_t* err);
 template <int P1>
 FusedLaunch fused_shape(int kind);
 

@@ -1,4 +1,4 @@
-// fused_p.cu -- instantiation of the fused brick kernels for one P1 = p+1
+// fused_p.cu -- instantiation of the fused column kernels for one P1 = p+1
 // (compiled once per P1 with -DHOFEM_P1=<P1>, so the builds run in parallel).
 #include <string.h>
 
@@ -12,64 +12,64 @@ namespace hofem {
 
 namespace {
 
+template <class K>
+cudaError_t set_smem(K kern, int bytes, bool* done) {
+  if (*done) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) *done = true;
+  return e;
+}
+
 template <int KIND, int P1, int Q>
-cudaError_t launch_general(const double* B, const double* G, const FusedArgs& A, int nbricks,
+cudaError_t launch_general(const double* B, const double* G, const ColArgs& A, int grid,
                            cudaStream_t s) {
   using S = Shape<P1>;
-  using C = Cfg<KIND, P1, Q, S::BX, S::BY, S::BZ>;
+  constexpr int SMEM = smem_bytes<KIND, P1, Q, S::BX, S::BY, S::NBUF>();
   Tab<P1, Q> T;
   memcpy(T.B, B, sizeof(T.B));
   memcpy(T.G, G, sizeof(T.G));
-  auto kern = fused_brick<KIND, P1, Q, S::BX, S::BY, S::BZ, S::NT, S::MINB>;
+  auto kern = fused_column<KIND, P1, Q, S::BX, S::BY, S::NT, S::NBUF, S::MAXR>;
   static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
-  kern<<<nbricks, S::NT, C::SMEM_BYTES, s>>>(T, A);
+  cudaError_t e = set_smem(kern, SMEM, &attr_done);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, S::NT, SMEM, s>>>(T, A);
   return cudaPeekAtLastError();
 }
 
 template <int P1>
-cudaError_t launch_colloc(const double* G, const FusedArgs& A, int nbricks, cudaStream_t s) {
+cudaError_t launch_colloc(const double* G, const ColArgs& A, int grid, cudaStream_t s) {
   using S = Shape<P1>;
-  using C = Cfg<KIND_COLLOC, P1, P1, S::BX, S::BY, S::BZ>;
+  constexpr int SMEM = smem_bytes<KIND_COLLOC, P1, P1, S::BX, S::BY, S::NBUF>();
   Tab<P1, P1> T;
   memset(T.B, 0, sizeof(T.B));
   memcpy(T.G, G, sizeof(T.G));
-  auto kern = fused_brick_colloc<P1, S::BX, S::BY, S::BZ, S::NT, S::MINB>;
+  auto kern = fused_column_colloc<P1, S::BX, S::BY, S::NT, S::NBUF, S::MAXR>;
   static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
-  kern<<<nbricks, S::NT, C::SMEM_BYTES, s>>>(T, A);
+  cudaError_t e = set_smem(kern, SMEM, &attr_done);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, S::NT, SMEM, s>>>(T, A);
   return cudaPeekAtLastError();
 }
 
 }  // namespace
 
 template <>
-bool fused_launch<HOFEM_P1>(int kind, int Q, const double* B, const double* G,
-                            const FusedArgs& A, int nbricks, cudaStream_t s, cudaError_t* err) {
+bool fused_launch<HOFEM_P1>(int kind, int Q, const double* B, const double* G, const ColArgs& A,
+                            int grid, cudaStream_t s, cudaError_t* err) {
   constexpr int P1 = HOFEM_P1;
   if (kind == KIND_COLLOC) {
     if (Q != P1) return false;
-    *err = launch_colloc<P1>(G, A, nbricks, s);
+    *err = launch_colloc<P1>(G, A, grid, s);
     return true;
   }
   if (Q == P1 + 1) {
-    *err = kind == KIND_MASS ? launch_general<KIND_MASS, P1, P1 + 1>(B, G, A, nbricks, s)
-                             : launch_general<KIND_DIFF, P1, P1 + 1>(B, G, A, nbricks, s);
+    *err = kind == KIND_MASS ? launch_general<KIND_MASS, P1, P1 + 1>(B, G, A, grid, s)
+                             : launch_general<KIND_DIFF, P1, P1 + 1>(B, G, A, grid, s);
     return true;
   }
   if (Q == P1) {
-    *err = kind == KIND_MASS ? launch_general<KIND_MASS, P1, P1>(B, G, A, nbricks, s)
-                             : launch_general<KIND_DIFF, P1, P1>(B, G, A, nbricks, s);
+    *err = kind == KIND_MASS ? launch_general<KIND_MASS, P1, P1>(B, G, A, grid, s)
+                             : launch_general<KIND_DIFF, P1, P1>(B, G, A, grid, s);
     return true;
   }
   return false;
@@ -80,7 +80,7 @@ FusedLaunch fused_shape<HOFEM_P1>(int kind) {
   using S = Shape<HOFEM_P1>;
   constexpr int p = HOFEM_P1 - 1;
   (void)kind;
-  return FusedLaunch{S::BX, S::BY, S::BZ, (p * S::BX + 1) * (p * S::BY + 1) * (p * S::BZ + 1)};
+  return FusedLaunch{S::BX, S::BY, (p * S::BX + 1) * (p * S::BY + 1) * (p + 1)};
 }
 
 }  // namespace hofem
