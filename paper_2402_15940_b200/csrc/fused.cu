@@ -3,6 +3,8 @@
 // (SURVEY.md §8(a) row a8): every lattice point on an interior x/y brick face or
 // a work-unit boundary plane sums the partials of its 2, 4 or 8 bricks in
 // ascending brick order.
+#include <stdlib.h>
+
 #include <vector>
 
 #include "fused_impl.cuh"
@@ -110,7 +112,7 @@ FusedLaunch shape_for(int P1, int kind) {
     HOFEM_FOR_P1(HOFEM_CASE)
 #undef HOFEM_CASE
   }
-  return FusedLaunch{0, 0, 0};
+  return FusedLaunch{0, 0, 0, 1};
 }
 
 int fused_kind(const Op* op) {
@@ -206,7 +208,7 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s) {
   const long long ncol = (long long)nbx * nby;
   const long long nbricks = ncol * m->nzl;
   if (nbricks == 0) return HOFEM_OK;
-  const int G0 = num_sms();
+  const int G0 = num_sms() * L.ctas_per_sm;
   int zc = 1, nchunks = 1;
   choose_chunks(ncol, m->nzl, G0, &zc, &nchunks);
   const long long nunits = ncol * nchunks;
@@ -230,6 +232,11 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s) {
   A.Nx = m->Nx; A.Ny = m->Ny; A.Nzl = m->Nzl;
   A.K0 = (long long)p * m->z0; A.NzG = m->NzG;
   A.bc = op->bc;
+  static const int l2pf = [] {
+    const char* e = getenv("HOFEM_L2PF");  // tuning knob: 0 disables the L2 bulk prefetch
+    return e ? atoi(e) : 1;
+  }();
+  A.l2pf = l2pf;
   cudaError_t err = cudaSuccess;
   bool ok = false;
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};

@@ -33,6 +33,19 @@
 
 #include "internal.h"
 
+#ifndef HOFEM_QLD
+#define HOFEM_QLD 1  // qdata register loads: 1 = __ldg, 2 = L1 no-allocate, 0 = L2 evict-first
+#endif
+#ifndef HOFEM_DEARLY
+#define HOFEM_DEARLY 0  // 1: tile-0 D values loaded at brick start; 0: at stage-3 start
+#endif
+#ifndef HOFEM_DBG_SKIP
+#define HOFEM_DBG_SKIP 0  // timing ablation only (wrong results): 1 epilogue, 2 D loads, 4 DMMAs
+#endif
+#ifndef HOFEM_APF
+#define HOFEM_APF 0  // 1: stage 3 loads the next tile's A fragments before this tile's MMAs
+#endif
+
 namespace hofem {
 
 template <int P1, int Q>
@@ -52,6 +65,7 @@ struct ColArgs {
   long long Nx, Ny, Nzl;  // local lattice sizes
   long long K0, NzG;      // global index of local plane 0; global plane count
   int bc;
+  int l2pf;               // 1: bulk-prefetch the next brick's qdata into L2
 };
 
 enum { KIND_MASS = 0, KIND_DIFF = 1, KIND_COLLOC = 2 };
@@ -163,77 +177,143 @@ __device__ __forceinline__ void issue_lattice(const ColArgs& A, double* L, long 
 
 // ---------------------------------------------------------------------------
 // a8 + a9 for one brick (element layer ez of a column).  Items are (lattice
-// row (j,k), element column s) like issue_lattice.  Along x and y a lattice
-// index has a "lower" contribution (element q-1, local node p) on an element
-// face and a "primary" one (element q, node i - p q); along z there is one
-// element layer (node k).  Ascending element order: y outer, x inner.  k == 0
-// adds the carried top plane of the previous brick first; k == p stores into
+// row (j,k), element column sx); sx is dispatched to a compile-time template
+// argument so that, per point, which elements contribute and whether the point
+// lies on an x face of the brick are compile-time facts.  Along x and y a
+// lattice index has a "lower" contribution (element q-1, local node p) on an
+// element face and a "primary" one (element q, node i - p q); along z there is
+// one element layer (node k).  Ascending element order: y outer, x inner.
+// k == 0 adds the carried top plane of the previous brick first; k == p goes to
 // the carry unless the brick ends the unit.
 // ---------------------------------------------------------------------------
-template <class C, int NT, int BX, int BY, bool NATURAL>
+struct EpiRow {
+  const double* cin;
+  double* cout;
+  double* bb;
+  long long gl;
+  int base0, base1;  // y-element offsets of the lower / primary contributions
+  bool vy0, vy1, to_carry, from_carry, row_sh, row_ess;
+};
+
+template <class C, int BX, bool NATURAL, int ESTRIDE, int SX>
+__device__ __forceinline__ void epi_segment(const ColArgs& A, const double* RA, const EpiRow& R,
+                                            long long I0, long long nvx, long long iess,
+                                            bool exok_lo, bool exok, bool xlo_sh, bool xhi_sh,
+                                            bool xlo_ess) {
+  constexpr int p = C::p, LX = C::LX;
+  constexpr int NPT = (SX == BX - 1) ? p + 1 : p;  // the last column also owns i = p*BX
+  double v[NPT];
+#pragma unroll
+  for (int ii = 0; ii < NPT; ++ii) {
+    double s = R.from_carry ? R.cin[p * SX + ii] : 0.0;
+#pragma unroll
+    for (int cy = 0; cy < 2; ++cy) {
+      const bool vy = cy ? R.vy1 : R.vy0;
+      const int base = cy ? R.base1 : R.base0;
+      if (ii == 0 && SX > 0) {  // lower contribution: element SX-1, node p
+        if (vy && exok_lo) s += RA[base + (SX - 1) * ESTRIDE + (NATURAL ? p : C::SA * p)];
+      }
+      if (ii < p) {
+        if (vy && exok) s += RA[base + SX * ESTRIDE + (NATURAL ? ii : C::SA * ii)];
+      } else {
+        if (vy && exok) s += RA[base + SX * ESTRIDE + (NATURAL ? p : C::SA * p)];
+      }
+    }
+    v[ii] = s;
+  }
+  // Destinations: row-uniform cases first (carry, partial buffer), then the
+  // common interior case with compile-time x-face handling; the rare rows that
+  // touch the Dirichlet boundary or a ragged mesh edge take the general path.
+  const int nv = (int)(nvx < LX ? nvx : LX);
+  if (R.to_carry) {
+#pragma unroll
+    for (int ii = 0; ii < NPT; ++ii)
+      if (p * SX + ii < nv) R.cout[p * SX + ii] = v[ii];
+    return;
+  }
+  if (R.row_sh) {
+#pragma unroll
+    for (int ii = 0; ii < NPT; ++ii)
+      if (p * SX + ii < nv) R.bb[p * SX + ii] = v[ii];
+    return;
+  }
+  const int ie = (int)(iess >= 0 && iess < LX ? iess : -1);
+  if (!R.row_ess && nv == LX && ie < 0 && !xlo_ess) {
+#pragma unroll
+    for (int ii = 0; ii < NPT; ++ii) {
+      const bool lo = (SX == 0 && ii == 0), hi = (SX == BX - 1 && ii == p);
+      if ((lo && xlo_sh) || (hi && xhi_sh))
+        R.bb[p * SX + ii] = v[ii];
+      else
+        A.y[R.gl + p * SX + ii] = v[ii];
+    }
+    return;
+  }
+#pragma unroll
+  for (int ii = 0; ii < NPT; ++ii) {
+    const int i = p * SX + ii;
+    if (i >= nv) continue;
+    const bool lo = (SX == 0 && ii == 0), hi = (SX == BX - 1 && ii == p);
+    if ((lo && xlo_sh) || (hi && xhi_sh)) {
+      R.bb[i] = v[ii];
+    } else {
+      const bool ess = R.row_ess || (lo && xlo_ess) || (i == ie);
+      A.y[R.gl + i] = ess ? A.x[R.gl + i] : v[ii];
+    }
+  }
+}
+
+template <class C, int BX, bool NATURAL, int ESTRIDE, int SX>
+__device__ __forceinline__ void epi_dispatch(int sx, const ColArgs& A, const double* RA,
+                                             const EpiRow& R, long long I0, long long nvx,
+                                             long long iess, const bool* exok, bool xlo_sh,
+                                             bool xhi_sh, bool xlo_ess) {
+  if constexpr (SX < BX) {
+    if (sx == SX)
+      epi_segment<C, BX, NATURAL, ESTRIDE, SX>(A, RA, R, I0, nvx, iess, SX > 0 ? exok[SX > 0 ? SX - 1 : 0] : false,
+                                               exok[SX], xlo_sh, xhi_sh, xlo_ess);
+    else
+      epi_dispatch<C, BX, NATURAL, ESTRIDE, SX + 1>(sx, A, RA, R, I0, nvx, iess, exok, xlo_sh,
+                                                    xhi_sh, xlo_ess);
+  }
+}
+
+template <class C, int NT, int BX, int BY, bool NATURAL, int ESTRIDE = C::YEN, int EOFF = 0>
 __device__ __forceinline__ void brick_epilogue(const ColArgs& A, const double* RA,
                                                const double* carry_in, double* carry_out,
                                                long long brick, int ex0, int ey0, long long I0,
                                                long long J0, long long K0l, bool first,
                                                bool last) {
-  constexpr int p = C::p, P1 = p + 1, LX = C::LX, LY = C::LY, YEN = C::YEN;
+  constexpr int p = C::p, P1 = p + 1, LX = C::LX, LY = C::LY;
+  RA += EOFF;
   const long long nvx = A.Nx - I0;
-  const bool xhi_sh = I0 + LX - 1 < A.Nx - 1;
-  for (int it = vtid(); it < LY * P1 * BX; it += NT) {
+  const bool xlo_sh = I0 > 0, xhi_sh = I0 + LX - 1 < A.Nx - 1;
+  const bool xlo_ess = A.bc && I0 == 0;
+  const long long iess = A.bc ? A.Nx - 1 - I0 : -1;
+  bool exok[BX];
+#pragma unroll
+  for (int q = 0; q < BX; ++q) exok[q] = ex0 + q < A.nx;
+  for (int it = threadIdx.x; it < LY * P1 * BX; it += NT) {
     const int sx = it % BX, r = it / BX, j = r % LY, k = r / LY;
     const long long J = J0 + j, K = K0l + k, Kg = K + A.K0;
     if (J >= A.Ny) continue;
     const int qj = j / p, rj = j - qj * p;
-    const bool vy[2] = {rj == 0 && qj > 0 && ey0 + qj - 1 < A.ny, qj < BY && ey0 + qj < A.ny};
-    int base[2];
-#pragma unroll
-    for (int cy = 0; cy < 2; ++cy) {
-      const int ely = cy ? qj : qj - 1, ay = cy ? rj : p;
-      base[cy] = BX * ely * YEN + (NATURAL ? P1 * (ay + P1 * k) : k + P1 * ay);
-    }
-    const bool ok_s = ex0 + sx < A.nx;                  // element column sx exists
-    const bool ok_l = sx > 0 && ex0 + sx - 1 < A.nx;    // element column sx-1 exists
-    const bool to_carry = (k == p) && !last;
-    const bool from_carry = (k == 0) && !first;
-    const bool row_sh = (j == 0 && J > 0) || (j == LY - 1 && J < A.Ny - 1) ||
-                        (k == 0 && first && K > 0) || (k == p && last && K < A.Nzl - 1);
-    const bool row_ess = A.bc && (J == 0 || J == A.Ny - 1 || Kg == 0 || Kg == A.NzG - 1);
-    const long long gl = I0 + A.Nx * (J + A.Ny * K);
-    double* bb = A.bbuf + brick * C::BLAT + LX * (j + LY * k);
-    const double* cin = carry_in + LX * j;
-    double* cout = carry_out + LX * j;
-#pragma unroll
-    for (int ii = 0; ii <= p; ++ii) {
-      // ii == p is the brick's last lattice column, handled by the last segment
-      const int i = p * sx + ii;
-      if ((ii < p || sx == BX - 1) && i < nvx) {
-        double s = from_carry ? cin[i] : 0.0;
-#pragma unroll
-        for (int cy = 0; cy < 2; ++cy) {
-          if (vy[cy]) {
-            if (ii == 0) {
-              if (ok_l) s += RA[base[cy] + (sx - 1) * YEN + (NATURAL ? p : C::SA * p)];
-              if (ok_s) s += RA[base[cy] + sx * YEN];
-            } else if (ii < p) {
-              if (ok_s) s += RA[base[cy] + sx * YEN + (NATURAL ? ii : C::SA * ii)];
-            } else {  // i = p*BX: lower contribution of the last element column
-              if (ok_s) s += RA[base[cy] + sx * YEN + (NATURAL ? p : C::SA * p)];
-            }
-          }
-        }
-        if (to_carry) {
-          cout[i] = s;
-        } else {
-          const bool sh = row_sh || (i == 0 && I0 > 0) || (i == LX - 1 && xhi_sh);
-          if (sh) {
-            bb[i] = s;
-          } else {
-            if (row_ess || (A.bc && (I0 + i == 0 || i == nvx - 1))) s = A.x[gl + i];
-            A.y[gl + i] = s;
-          }
-        }
-      }
-    }
+    EpiRow R;
+    R.vy0 = rj == 0 && qj > 0 && ey0 + qj - 1 < A.ny;
+    R.vy1 = qj < BY && ey0 + qj < A.ny;
+    R.base0 = BX * (qj - 1) * ESTRIDE + (NATURAL ? P1 * (p + P1 * k) : k + P1 * p);
+    R.base1 = BX * qj * ESTRIDE + (NATURAL ? P1 * (rj + P1 * k) : k + P1 * rj);
+    R.to_carry = (k == p) && !last;
+    R.from_carry = (k == 0) && !first;
+    R.row_sh = (j == 0 && J > 0) || (j == LY - 1 && J < A.Ny - 1) ||
+               (k == 0 && first && K > 0) || (k == p && last && K < A.Nzl - 1);
+    R.row_ess = A.bc && (J == 0 || J == A.Ny - 1 || Kg == 0 || Kg == A.NzG - 1);
+    R.gl = I0 + A.Nx * (J + A.Ny * K);
+    R.bb = A.bbuf + brick * C::BLAT + LX * (j + LY * k);
+    R.cin = carry_in + LX * j;
+    R.cout = carry_out + LX * j;
+    epi_dispatch<C, BX, NATURAL, ESTRIDE, 0>(sx, A, RA, R, I0, nvx, iess, exok, xlo_sh, xhi_sh,
+                                             xlo_ess);
   }
 }
 
@@ -598,6 +678,565 @@ __global__ void __maxnreg__(MAXR) fused_column(const __grid_constant__ Tab<P1, Q
 }
 
 // ---------------------------------------------------------------------------
+// Tensor-core (DMMA) kernel: mass (BP1) and diffusion (BP3), any (P1, Q).
+//
+// Each 1D contraction of the sum factorization is a small FP64 GEMM on the
+// tensor cores (mma.sync.m16n8k8.f64): rows = the brick's element "lines" (the
+// two untouched axes, batched over its NE elements), k = the contracted axis,
+// n = the output axis; the 1D matrix is the B operand (fragments built once per
+// stage from the constant bank).  Stage outputs go through shared memory in
+// [k][row] layouts whose k-stride is 4 (mod 16) doubles, so A-fragment loads are
+// bank-conflict-free.  Stage 3 keeps the z forward contraction, the pointwise D
+// and the z backward contraction in registers: the accumulator fragment of the
+// forward GEMM is reused as the A fragment of the backward GEMM by relabelling
+// its k index (qz = 2t, 2t+1 -> k = t, t+4), with the backward B operand
+// permuted accordingly.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma(double (&d)[4], const double (&a)[4], const double (&b)[2]) {
+  if (HOFEM_DBG_SKIP & 4) {
+    d[0] += a[0] * b[0]; d[1] += a[1] * b[1]; d[2] += a[2]; d[3] += a[3];
+    return;
+  }
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+
+constexpr int mod16_4(int n) { return n + (((4 - n) % 16) + 16) % 16; }  // >= n, == 4 (mod 16)
+
+template <int KIND, int P1, int Q, int BX, int BY>
+struct CfgM {
+  static constexpr int p = P1 - 1, P = P1, NE = BX * BY;
+  static constexpr int LX = p * BX + 1, LY = p * BY + 1, LZ = P1;
+  static constexpr int BLAT = LX * LY * LZ;
+  static constexpr int LXS = mod16_4(LY * LZ);  // x-stride of the smem lattice
+  static constexpr int LAT = LXS * LX;
+  static constexpr int NR1 = NE * P * P, NR2 = NE * Q * P, NR3 = NE * Q * Q;  // GEMM rows
+  static constexpr int MT1 = (NR1 + 15) / 16, MT2 = (NR2 + 15) / 16, MT3 = (NR3 + 15) / 16;
+  static constexpr int KS1 = mod16_4(NR1), KS2 = mod16_4(NR2), KS3 = mod16_4(NR3);
+  static constexpr int NA = (KIND == KIND_MASS) ? 1 : 2;  // stage-1 outputs / stage-2T outputs
+  static constexpr int NB = (KIND == KIND_MASS) ? 1 : 3;  // stage-2 outputs / stage-3 outputs
+  static constexpr int cmax(int a, int b) { return a > b ? a : b; }
+  static constexpr int T1A = cmax(P * KS2, Q * KS1);      // one array of the T1 region
+  static constexpr int T2A = P * KS3;                      // one array of the T2 region
+  static constexpr int SA = ((P * P) % 2 == 0) ? P * P + 1 : P * P;
+  static constexpr int YEN = SA * P;
+  static constexpr int REG1 = NA * T1A;
+  static constexpr int REG2 = cmax(NB * T2A, NE * YEN);
+  static constexpr int CARRY = LX * LY;
+  static constexpr int SMEM_BYTES = (REG1 + REG2 + 2 * LAT + 2 * CARRY) * 8;
+  static constexpr int NC = (KIND == KIND_MASS) ? 1 : 6;
+  static constexpr int NQ1 = Q;
+  __device__ static constexpr int lat(int i, int j, int k) { return k + LZ * j + LXS * i; }
+};
+
+// B-operand fragment of a 1D table M (rows x cols, row-major) for GEMM n index
+// `n` and k index `k`: value M[n][k] if TRANS == false (k runs over the table's
+// columns), M[k][n] if TRANS.  Out-of-range entries are zero padding.
+template <int ROWS, int COLS, bool TRANS>
+__device__ __forceinline__ double tabv(const double* M, int n, int k) {
+  const int r = TRANS ? k : n, c = TRANS ? n : k;
+  return (r < ROWS && c < COLS) ? M[r * COLS + c] : 0.0;
+}
+
+// Thread 0: warm L2 with brick b's qdata (one bulk prefetch per element).
+template <class C, int BX, int BY>
+__device__ __forceinline__ void prefetch_qdata_l2(const ColArgs& A, const Brick& b) {
+  if (threadIdx.x != 0 || b.u >= A.nunits || !A.l2pf) return;
+  constexpr long long per = (long long)C::NC * C::NQ1 * C::NQ1 * C::NQ1 * 8;
+  const char* base = reinterpret_cast<const char*>(A.qd);
+#pragma unroll
+  for (int el = 0; el < BX * BY; ++el) {
+    const int ex = b.bx * BX + el % BX, ey = b.by * BY + el / BX;
+    if (ex < A.nx && ey < A.ny) {
+      const long long e = ex + (long long)A.nx * (ey + (long long)A.ny * b.ez);
+      const long long lo = (e * per) & ~15LL, hi = ((e + 1) * per + 15) & ~15LL;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + lo),
+                   "r"((unsigned)(hi - lo))
+                   : "memory");
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-per-element tensor-core kernel (mass / diffusion).
+//
+// One warp runs ITS element's whole pipeline; stage outputs live in the warp's
+// private shared-memory region, so stages are separated by __syncwarp only.
+// GEMM rows are element-aligned and padded to 16 (compile-time tile
+// structure); every lane's shared-memory offsets are brick-invariant.  All
+// padding (rows, k slots, lattice columns) is zero-initialised once and never
+// written, so fragment loads need no predicates -- only stores are guarded.
+// ---------------------------------------------------------------------------
+template <int KIND, int P1, int Q, int BX, int BY>
+struct CfgE {
+  static constexpr int p = P1 - 1, P = P1, NE = BX * BY;
+  static constexpr int LX = p * BX + 1, LY = p * BY + 1, LZ = P1;
+  static constexpr int BLAT = LX * LY * LZ;
+  static constexpr int KP = (P + 7) / 8, KQ = (Q + 7) / 8;  // k-steps over P / Q
+  static constexpr int LXS = mod16_4(LY * LZ);               // lattice x-stride
+  static constexpr int LAT = LXS * LX;
+  static constexpr int R1 = P * P, R2 = Q * P, R3 = Q * Q;   // GEMM rows per element
+  static constexpr int M1 = (R1 + 15) / 16, M2 = (R2 + 15) / 16, M3 = (R3 + 15) / 16;
+  static constexpr int cmax(int a, int b) { return a > b ? a : b; }
+  // k-major arrays [k][row]: row stride == 4 (mod 16) doubles; padded rows are
+  // clamped on load and never stored, padded k slots are predicated to zero.
+  static constexpr int KS1 = mod16_4(R1);                    // R  [qx][r1]
+  static constexpr int KS2 = mod16_4(R2);                    // T1 [b][r2]
+  static constexpr int KS3 = mod16_4(R3);                    // T2 [c][r3]
+  static constexpr int NA = (KIND == KIND_MASS) ? 1 : 2;
+  static constexpr int NB = (KIND == KIND_MASS) ? 1 : 3;
+  static constexpr int T1A = cmax(P * KS2, Q * KS1);
+  static constexpr int T2A = P * KS3;
+  static constexpr int SA = ((P * P) % 2 == 0) ? P * P + 1 : P * P;
+  static constexpr int YEN = SA * P;
+  static constexpr int W1 = NA * T1A, W2 = cmax(NB * T2A, YEN);
+  static constexpr int WS = W1 + W2;  // doubles per warp (element)
+  static constexpr int CARRY = LX * LY;
+  static constexpr int SMEM_DOUBLES = NE * WS + 2 * LAT + 2 * CARRY;
+  static constexpr int SMEM_BYTES = SMEM_DOUBLES * 8;
+  static constexpr int NC = (KIND == KIND_MASS) ? 1 : 6;
+  static constexpr int NQ1 = Q;
+  __device__ static constexpr int lat(int i, int j, int k) { return k + LZ * j + LXS * i; }
+};
+
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ double ld_policy(const double* ptr, unsigned long long pol) {
+#if HOFEM_QLD == 1
+  (void)pol;
+  return __ldg(ptr);  // L1-allocating read-only load, normal L2 priority
+#elif HOFEM_QLD == 2
+  double v;
+  (void)pol;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(ptr));
+  return v;
+#else
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v)
+               : "l"(ptr), "l"(pol));
+  return v;
+#endif
+}
+
+template <int KIND, int P1, int Q, int BX, int BY, int MINB>
+__global__ void __launch_bounds__(32 * BX * BY, MINB)
+    fused_elem_mma(const __grid_constant__ Tab<P1, Q> T, const __grid_constant__ ColArgs A) {
+  using C = CfgE<KIND, P1, Q, BX, BY>;
+  constexpr int NE = C::NE, NT = 32 * NE;
+  constexpr int P = P1, p = P1 - 1;
+  constexpr int KP = C::KP, KQ = C::KQ, NPT = KP, NQT = KQ;
+  constexpr int Q2 = Q * Q, Q3 = Q * Q * Q;
+  constexpr bool DIFF = KIND == KIND_DIFF;
+  constexpr int NA = C::NA, NB = C::NB, NC = C::NC;
+  constexpr int M1 = C::M1, M2 = C::M2, M3 = C::M3;
+  extern __shared__ __align__(16) double smem[];
+  double* LB = smem + NE * C::WS;
+  double* CY = LB + 2 * C::LAT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  double* W1 = smem + warp * C::WS;  // T1 / R arrays
+  double* W2 = W1 + C::W1;           // T2 / S arrays; y_e
+  const int exl = warp % BX, eyl = warp / BX;
+  const unsigned long long pol = evict_first_policy();
+
+  for (int i = tid; i < C::SMEM_DOUBLES; i += NT) smem[i] = 0.0;
+  __syncthreads();
+
+  Brick cur = unit_first(A, blockIdx.x);
+  if (cur.u >= A.nunits) return;
+  prefetch_qdata_l2<C, BX, BY>(A, cur);
+  issue_lattice<C, NT, BX>(A, LB, (long long)p * cur.bx * BX, (long long)p * cur.by * BY,
+                           (long long)p * cur.ez);
+  cp_async_wait_all();
+  __syncthreads();
+
+  for (int kb = 0; cur.u < A.nunits; ++kb) {
+    const Brick nxt = brick_next(A, cur);
+    const int ex0 = cur.bx * BX, ey0 = cur.by * BY, ez = cur.ez;
+    const long long I0 = (long long)p * ex0, J0 = (long long)p * ey0;
+    const double* L = LB + (kb & 1) * C::LAT;
+    if (nxt.u < A.nunits) {
+      issue_lattice<C, NT, BX>(A, LB + ((kb + 1) & 1) * C::LAT, (long long)p * nxt.bx * BX,
+                               (long long)p * nxt.by * BY, (long long)p * nxt.ez);
+      prefetch_qdata_l2<C, BX, BY>(A, nxt);
+    }
+    const int ex = ex0 + exl, ey = ey0 + eyl;
+    if (ex < A.nx && ey < A.ny) {
+      const double* qde =
+          A.qd + (ex + (long long)A.nx * (ey + (long long)A.ny * ez)) * (long long)(NC * Q3);
+      // D at this lane's stage-3 fragment positions of tile 0 (L2 hits)
+      double dn[NQT][4][NC];
+      auto load_d = [&](int tt, double (&d)[NQT][4][NC]) {
+#pragma unroll
+        for (int nt = 0; nt < NQT; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = min(16 * tt + g + 8 * (q >> 1), C::R3 - 1);
+            const int qz = min(8 * nt + 2 * t + (q & 1), Q - 1);
+#pragma unroll
+            for (int m = 0; m < NC; ++m)
+              d[nt][q][m] = (HOFEM_DBG_SKIP & 2) ? 1.0 + m * 1e-3 : ld_policy(qde + m * Q3 + qz * Q2 + r, pol);
+          }
+      };
+      if (HOFEM_DEARLY) load_d(0, dn);
+
+      // ---- stage 1: contract x.  rows r1 = (b, c), k = a, n = qx.
+      {
+        double fb[NQT][KP][2], fg[NQT][KP][2];
+#pragma unroll
+        for (int nt = 0; nt < NQT; ++nt)
+#pragma unroll
+          for (int ks = 0; ks < KP; ++ks)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              fb[nt][ks][h] = tabv<Q, P, false>(T.B, 8 * nt + g, 8 * ks + t + 4 * h);
+              fg[nt][ks][h] = DIFF ? tabv<Q, P, false>(T.G, 8 * nt + g, 8 * ks + t + 4 * h) : 0.0;
+            }
+#pragma unroll
+        for (int tt = 0; tt < M1; ++tt) {
+          int lb[2], sb[2];
+          bool ok[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = 16 * tt + g + 8 * h, rc = min(r, C::R1 - 1);
+            const int b = rc / P, c = rc % P;
+            ok[h] = r < C::R1;
+            lb[h] = C::lat(p * exl + t, p * eyl + b, c);
+            sb[h] = b * C::KS2 + c + 2 * t * P;
+          }
+          double a[KP][4];
+#pragma unroll
+          for (int ks = 0; ks < KP; ++ks)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int k = 8 * ks + t + 4 * (q >> 1);
+              a[ks][q] = k < P ? L[lb[q & 1] + C::LXS * (8 * ks + 4 * (q >> 1))] : 0.0;
+            }
+#pragma unroll
+          for (int m = 0; m < NA; ++m)
+#pragma unroll
+            for (int nt = 0; nt < NQT; ++nt) {
+              double d[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+              for (int ks = 0; ks < KP; ++ks) dmma(d, a[ks], m == 0 ? fb[nt][ks] : fg[nt][ks]);
+              double* out = W1 + m * C::T1A;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int h = q >> 1, qx = 8 * nt + 2 * t + (q & 1);
+                if (ok[h] && qx < Q) out[sb[h] + P * (8 * nt + (q & 1))] = d[q];
+              }
+            }
+        }
+      }
+      __syncwarp();
+
+      // ---- stage 2: contract y.  rows r2 = (qx, c), k = b, n = qy.
+      {
+        double fb[NQT][KP][2], fg[NQT][KP][2];
+#pragma unroll
+        for (int nt = 0; nt < NQT; ++nt)
+#pragma unroll
+          for (int ks = 0; ks < KP; ++ks)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              fb[nt][ks][h] = tabv<Q, P, false>(T.B, 8 * nt + g, 8 * ks + t + 4 * h);
+              fg[nt][ks][h] = DIFF ? tabv<Q, P, false>(T.G, 8 * nt + g, 8 * ks + t + 4 * h) : 0.0;
+            }
+#pragma unroll
+        for (int tt = 0; tt < M2; ++tt) {
+          int sb[2];
+          bool ok[2];
+          const int r0 = min(16 * tt + g, C::R2 - 1), r1 = min(16 * tt + g + 8, C::R2 - 1);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = 16 * tt + g + 8 * h, rc = min(r, C::R2 - 1);
+            const int qx = rc / P, c = rc % P;
+            ok[h] = r < C::R2;
+            sb[h] = c * C::KS3 + qx + 2 * t * Q;
+          }
+          double aB[KP][4], aG[KP][4];
+#pragma unroll
+          for (int ks = 0; ks < KP; ++ks)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int k = 8 * ks + t + 4 * (q >> 1);
+              const int o = k * C::KS2 + ((q & 1) ? r1 : r0);
+              aB[ks][q] = k < P ? W1[o] : 0.0;
+              aG[ks][q] = (DIFF && k < P) ? W1[C::T1A + o] : 0.0;
+            }
+#pragma unroll
+          for (int nt = 0; nt < NQT; ++nt) {
+            double dBB[4] = {0, 0, 0, 0}, dBG[4] = {0, 0, 0, 0}, dGB[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int ks = 0; ks < KP; ++ks) {
+              dmma(dBB, aB[ks], fb[nt][ks]);
+              if (DIFF) {
+                dmma(dBG, aB[ks], fg[nt][ks]);
+                dmma(dGB, aG[ks], fb[nt][ks]);
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int h = q >> 1, qy = 8 * nt + 2 * t + (q & 1);
+              if (ok[h] && qy < Q) {
+                const int o = sb[h] + Q * (8 * nt + (q & 1));
+                if (DIFF) {
+                  W2[o] = dGB[q];              // G_x B_y  (-> u_x)
+                  W2[C::T2A + o] = dBG[q];     // B_x G_y  (-> u_y)
+                  W2[2 * C::T2A + o] = dBB[q]; // B_x B_y  (-> u_z)
+                } else {
+                  W2[o] = dBB[q];
+                }
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+
+      // ---- stage 3: contract z, pointwise D, contract back -- in registers.
+      //      rows r3 = (qy, qx) (qx fastest), k = c / permuted qz.
+      {
+        double ff[NQT][KP][2], fz[NQT][KP][2];  // forward: n = qz, k = c
+        double bf[NPT][KQ][2], bz[NPT][KQ][2];  // backward: n = c, k = permuted qz
+#pragma unroll
+        for (int nt = 0; nt < NQT; ++nt)
+#pragma unroll
+          for (int ks = 0; ks < KP; ++ks)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              ff[nt][ks][h] = tabv<Q, P, false>(T.B, 8 * nt + g, 8 * ks + t + 4 * h);
+              fz[nt][ks][h] = DIFF ? tabv<Q, P, false>(T.G, 8 * nt + g, 8 * ks + t + 4 * h) : 0.0;
+            }
+#pragma unroll
+        for (int nt = 0; nt < NPT; ++nt)
+#pragma unroll
+          for (int ks = 0; ks < KQ; ++ks)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              bf[nt][ks][h] = tabv<Q, P, false>(T.B, 8 * ks + 2 * t + h, 8 * nt + g);
+              bz[nt][ks][h] = DIFF ? tabv<Q, P, false>(T.G, 8 * ks + 2 * t + h, 8 * nt + g) : 0.0;
+            }
+        if (!HOFEM_DEARLY) load_d(0, dn);
+        auto load_a = [&](int tt, double (&a)[NB][KP][4]) {
+          const int r0 = min(16 * tt + g, C::R3 - 1), r1 = min(16 * tt + g + 8, C::R3 - 1);
+#pragma unroll
+          for (int m = 0; m < NB; ++m)
+#pragma unroll
+            for (int ks = 0; ks < KP; ++ks)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int k = 8 * ks + t + 4 * (q >> 1);
+                a[m][ks][q] = k < P ? W2[m * C::T2A + k * C::KS3 + ((q & 1) ? r1 : r0)] : 0.0;
+              }
+        };
+        double an[NB][KP][4];
+        if (HOFEM_APF) load_a(0, an);
+#pragma unroll
+        for (int tt = 0; tt < M3; ++tt) {
+          double dc[NQT][4][NC];
+#pragma unroll
+          for (int nt = 0; nt < NQT; ++nt)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+              for (int m = 0; m < NC; ++m) dc[nt][q][m] = dn[nt][q][m];
+          if (tt + 1 < M3) load_d(tt + 1, dn);
+          const int r0 = min(16 * tt + g, C::R3 - 1), r1 = min(16 * tt + g + 8, C::R3 - 1);
+          const bool ok0 = 16 * tt + g < C::R3, ok1 = 16 * tt + g + 8 < C::R3;
+          double a[NB][KP][4];
+          if (HOFEM_APF) {
+#pragma unroll
+            for (int m = 0; m < NB; ++m)
+#pragma unroll
+              for (int ks = 0; ks < KP; ++ks)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) a[m][ks][q] = an[m][ks][q];
+            if (tt + 1 < M3) load_a(tt + 1, an);
+          } else {
+            load_a(tt, a);
+          }
+          double w[NB][NQT][4];
+#pragma unroll
+          for (int nt = 0; nt < NQT; ++nt) {
+            double u[NB][4];
+#pragma unroll
+            for (int m = 0; m < NB; ++m) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) u[m][q] = 0.0;
+#pragma unroll
+              for (int ks = 0; ks < KP; ++ks)
+                dmma(u[m], a[m][ks], (DIFF && m == 2) ? fz[nt][ks] : ff[nt][ks]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const double* dd = dc[nt][q];
+              if (DIFF) {
+                w[0][nt][q] = dd[0] * u[0][q] + dd[1] * u[1][q] + dd[2] * u[2][q];
+                w[1][nt][q] = dd[1] * u[0][q] + dd[3] * u[1][q] + dd[4] * u[2][q];
+                w[2][nt][q] = dd[2] * u[0][q] + dd[4] * u[1][q] + dd[5] * u[2][q];
+              } else {
+                w[0][nt][q] = dd[0] * u[0][q];
+              }
+            }
+          }
+#pragma unroll
+          for (int nt = 0; nt < NPT; ++nt)
+#pragma unroll
+            for (int m = 0; m < NB; ++m) {
+              double sacc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+              for (int ks = 0; ks < KQ; ++ks) {
+                const double aw[4] = {w[m][ks][0], w[m][ks][2], w[m][ks][1], w[m][ks][3]};
+                dmma(sacc, aw, (DIFF && m == 2) ? bz[nt][ks] : bf[nt][ks]);
+              }
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int c = 8 * nt + 2 * t + (q & 1);
+                if (((q >> 1) ? ok1 : ok0) && c < P)
+                  W2[m * C::T2A + c * C::KS3 + ((q >> 1) ? r1 : r0)] = sacc[q];
+              }
+            }
+        }
+      }
+      __syncwarp();
+
+      // ---- stage 2^T: contract qy.  rows r2 = (qx, c), k = qy, n = b.
+      {
+        double fb[NPT][KQ][2], fg[NPT][KQ][2];
+#pragma unroll
+        for (int nt = 0; nt < NPT; ++nt)
+#pragma unroll
+          for (int ks = 0; ks < KQ; ++ks)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              fb[nt][ks][h] = tabv<Q, P, true>(T.B, 8 * nt + g, 8 * ks + t + 4 * h);
+              fg[nt][ks][h] = DIFF ? tabv<Q, P, true>(T.G, 8 * nt + g, 8 * ks + t + 4 * h) : 0.0;
+            }
+#pragma unroll
+        for (int tt = 0; tt < M2; ++tt) {
+          int lb[2], sb[2];
+          bool ok[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = 16 * tt + g + 8 * h, rc = min(r, C::R2 - 1);
+            const int qx = rc / P, c = rc % P;
+            ok[h] = r < C::R2;
+            lb[h] = c * C::KS3 + qx + t * Q;
+            sb[h] = qx * C::KS1 + c + 2 * t * P;
+          }
+          double a[NB][KQ][4];
+#pragma unroll
+          for (int m = 0; m < NB; ++m)
+#pragma unroll
+            for (int ks = 0; ks < KQ; ++ks)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int k = 8 * ks + t + 4 * (q >> 1);
+                a[m][ks][q] = k < Q ? W2[m * C::T2A + lb[q & 1] + Q * (8 * ks + 4 * (q >> 1))] : 0.0;
+              }
+#pragma unroll
+          for (int nt = 0; nt < NPT; ++nt) {
+            double rg[4] = {0, 0, 0, 0}, rb[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int ks = 0; ks < KQ; ++ks) {
+              if (DIFF) {
+                dmma(rg, a[0][ks], fb[nt][ks]);  // S_x B_y^T  (-> G_x^T)
+                dmma(rb, a[1][ks], fg[nt][ks]);  // S_y G_y^T  (-> B_x^T)
+                dmma(rb, a[2][ks], fb[nt][ks]);  // S_z B_y^T  (-> B_x^T)
+              } else {
+                dmma(rb, a[0][ks], fb[nt][ks]);
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int h = q >> 1, b = 8 * nt + 2 * t + (q & 1);
+              if (ok[h] && b < P) {
+                const int o = sb[h] + P * (8 * nt + (q & 1));
+                W1[o] = rb[q];
+                if (DIFF) W1[C::T1A + o] = rg[q];
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+
+      // ---- stage 1^T: contract qx.  rows r1 = (b, c), k = qx, n = a -> y_e.
+      {
+        double fb[NPT][KQ][2], fg[NPT][KQ][2];
+#pragma unroll
+        for (int nt = 0; nt < NPT; ++nt)
+#pragma unroll
+          for (int ks = 0; ks < KQ; ++ks)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              fb[nt][ks][h] = tabv<Q, P, true>(T.B, 8 * nt + g, 8 * ks + t + 4 * h);
+              fg[nt][ks][h] = DIFF ? tabv<Q, P, true>(T.G, 8 * nt + g, 8 * ks + t + 4 * h) : 0.0;
+            }
+#pragma unroll
+        for (int tt = 0; tt < M1; ++tt) {
+          int sb[2];
+          bool ok[2];
+          const int r0 = min(16 * tt + g, C::R1 - 1), r1 = min(16 * tt + g + 8, C::R1 - 1);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = 16 * tt + g + 8 * h, rc = min(r, C::R1 - 1);
+            const int b = rc / P, c = rc % P;
+            ok[h] = r < C::R1;
+            sb[h] = c + P * b + 2 * t * C::SA;
+          }
+          double aB[KQ][4], aG[KQ][4];
+#pragma unroll
+          for (int ks = 0; ks < KQ; ++ks)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int k = 8 * ks + t + 4 * (q >> 1);
+              const int o = k * C::KS1 + ((q & 1) ? r1 : r0);
+              aB[ks][q] = k < Q ? W1[o] : 0.0;
+              aG[ks][q] = (DIFF && k < Q) ? W1[C::T1A + o] : 0.0;
+            }
+#pragma unroll
+          for (int nt = 0; nt < NPT; ++nt) {
+            double y[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int ks = 0; ks < KQ; ++ks) {
+              dmma(y, aB[ks], fb[nt][ks]);
+              if (DIFF) dmma(y, aG[ks], fg[nt][ks]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int h = q >> 1, a = 8 * nt + 2 * t + (q & 1);
+              if (ok[h] && a < P) W2[sb[h] + C::SA * (8 * nt + (q & 1))] = y[q];
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+
+    const long long brick = cur.bx + (long long)A.nbx * (cur.by + (long long)A.nby * ez);
+    if (!(HOFEM_DBG_SKIP & 1)) brick_epilogue<C, NT, BX, BY, false, C::WS, C::W1>(
+        A, smem, CY + ((ez + 1) & 1) * C::CARRY, CY + (ez & 1) * C::CARRY, brick, ex0, ey0, I0,
+        J0, (long long)p * ez, ez == cur.z0, ez + 1 == cur.z1);
+    cp_async_wait_all();
+    __syncthreads();
+    cur = nxt;
+  }
+}
+
+template <int KIND, int P1, int Q, int BX, int BY>
+constexpr int smem_bytes_elem() {
+  return CfgE<KIND, P1, Q, BX, BY>::SMEM_BYTES;
+}
+
+// ---------------------------------------------------------------------------
 // Collocated diffusion kernel (BP5: GLL points = nodes, B1d = I, Q = P1).
 // u_x = G_x x, u_y = G_y x, u_z = G_z x; w = D u; y = G_x^T w_x + G_y^T w_y + G_z^T w_z.
 // ---------------------------------------------------------------------------
@@ -739,8 +1378,25 @@ constexpr int smem_bytes() {
   return C::SMEM_BYTES + NBUF * C::NE * Stage<C>::SLOT * 8;
 }
 
+// Tensor-core kernel shapes (mass / diffusion): brick = one warp per element,
+// CTAs per SM.
+template <int P1>
+struct ShapeE;
+//                                    BX BY MINB
+template <> struct ShapeE<2> { static constexpr int BX = 4, BY = 2, MINB = 2; };
+template <> struct ShapeE<3> { static constexpr int BX = 4, BY = 2, MINB = 2; };
+template <> struct ShapeE<4> { static constexpr int BX = 4, BY = 2, MINB = 2; };
+template <> struct ShapeE<5> { static constexpr int BX = 2, BY = 2, MINB = 3; };
+#ifndef HOFEM_MINB6
+#define HOFEM_MINB6 3
+#endif
+template <> struct ShapeE<6> { static constexpr int BX = 2, BY = 2, MINB = HOFEM_MINB6; };
+template <> struct ShapeE<7> { static constexpr int BX = 2, BY = 2, MINB = 2; };
+template <> struct ShapeE<8> { static constexpr int BX = 2, BY = 1, MINB = 3; };
+template <> struct ShapeE<9> { static constexpr int BX = 2, BY = 1, MINB = 2; };
+
 struct FusedLaunch {
-  int BX, BY, blat;
+  int BX, BY, blat, ctas_per_sm;
 };
 
 // Defined per P1 in fused_p.cu: kind in {KIND_MASS, KIND_DIFF, KIND_COLLOC},

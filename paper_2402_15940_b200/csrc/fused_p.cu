@@ -23,16 +23,16 @@ cudaError_t set_smem(K kern, int bytes, bool* done) {
 template <int KIND, int P1, int Q>
 cudaError_t launch_general(const double* B, const double* G, const ColArgs& A, int grid,
                            cudaStream_t s) {
-  using S = Shape<P1>;
-  constexpr int SMEM = smem_bytes<KIND, P1, Q, S::BX, S::BY, S::NBUF>();
+  using S = ShapeE<P1>;
+  constexpr int SMEM = smem_bytes_elem<KIND, P1, Q, S::BX, S::BY>();
   Tab<P1, Q> T;
   memcpy(T.B, B, sizeof(T.B));
   memcpy(T.G, G, sizeof(T.G));
-  auto kern = fused_column<KIND, P1, Q, S::BX, S::BY, S::NT, S::NBUF, S::MAXR>;
+  auto kern = fused_elem_mma<KIND, P1, Q, S::BX, S::BY, S::MINB>;
   static bool attr_done = false;
   cudaError_t e = set_smem(kern, SMEM, &attr_done);
   if (e != cudaSuccess) return e;
-  kern<<<grid, S::NT, SMEM, s>>>(T, A);
+  kern<<<grid, S::BX * S::BY * 32, SMEM, s>>>(T, A);
   return cudaPeekAtLastError();
 }
 
@@ -77,10 +77,13 @@ bool fused_launch<HOFEM_P1>(int kind, int Q, const double* B, const double* G, c
 
 template <>
 FusedLaunch fused_shape<HOFEM_P1>(int kind) {
-  using S = Shape<HOFEM_P1>;
   constexpr int p = HOFEM_P1 - 1;
-  (void)kind;
-  return FusedLaunch{S::BX, S::BY, (p * S::BX + 1) * (p * S::BY + 1) * (p + 1)};
+  if (kind == KIND_COLLOC) {
+    using S = Shape<HOFEM_P1>;
+    return FusedLaunch{S::BX, S::BY, (p * S::BX + 1) * (p * S::BY + 1) * (p + 1), 1};
+  }
+  using S = ShapeE<HOFEM_P1>;
+  return FusedLaunch{S::BX, S::BY, (p * S::BX + 1) * (p * S::BY + 1) * (p + 1), S::MINB};
 }
 
 }  // namespace hofem
