@@ -48,18 +48,7 @@ def alg_bytes(nx, ny, nz, p, Q, nc):
     return 16 * N + 8 * nc * E * Q ** 3, N, E
 
 
-def brick_direct_points(nx, ny, nz, p, B):
-    """Lattice points NOT on an interior brick face (written by the brick kernel
-    itself; the rest go through the fix-up kernel)."""
-    def axis(n, b):
-        N = p * n + 1
-        nb = -(-n // b)
-        return N - (nb - 1)
-    return axis(nx, B[0]) * axis(ny, B[1]) * axis(nz, B[2])
-
-
-SHAPES = {2: (4, 4, 4), 3: (4, 4, 2), 4: (4, 2, 2), 5: (2, 2, 2), 6: (2, 2, 2), 7: (2, 2, 1),
-          8: (2, 2, 1), 9: (2, 1, 1)}  # fused_impl.cuh Shape<P1>
+KERNEL_NAMES = {0: "fused_elem_mma", 1: "fused_elem_simt", 2: "fused_column_colloc"}
 
 
 class ClockSampler:
@@ -247,7 +236,8 @@ def run_ours(args):
     t_fix = prof.fixup_ms / 1e3 / max(prof.fixup_launches, 1)
     nzl = n
     bytes_apply, N_l, E_l = alg_bytes(nx, ny, nzl, p, Q, 6)
-    nd = brick_direct_points(nx, ny, nzl, p, SHAPES[p + 1])
+    info = op.fused_info()
+    nd = info.direct_points
     bytes_brick = 8 * N_l + 8 * 6 * E_l * Q ** 3 + 8 * nd
     peak, peak_src = load_peaks()
     achieved = bytes_brick / t_brick / 1e9
@@ -312,7 +302,8 @@ def run_ours(args):
             "apply_ms": 1e3 * t_apply,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": f"fused_brick<DIFF,P1={p + 1},Q={Q}>",
+                         "kernel": f"{KERNEL_NAMES.get(info.variant, '?')}<DIFF,P1={p + 1},Q={Q}>"
+                                   f" brick {info.bx}x{info.by}x1, {info.grid} CTAs",
                          "alg_bytes_per_launch": bytes_brick, "launch_ms": 1e3 * t_brick,
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
                          "apply_frac": bytes_apply / t_apply / 1e9 / peak,

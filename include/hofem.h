@@ -176,6 +176,27 @@ typedef struct {
 hofem_status hofem_profile_enable(int enable);
 hofem_status hofem_profile_read(hofem_profile_stats* out);
 
+/* How hofem_op_apply runs this operator (for the bench's roofline figure):
+ * fused kernel variant (0 tensor-core DMMA, 1 SIMT, 2 collocated SIMT; -1 the
+ * operator has no fused kernel and apply uses the unfused path), brick shape,
+ * work-unit z chunking, and the number of local lattice points the fused
+ * kernel writes to y directly vs. through the fix-up kernel (interior brick
+ * faces).  Host-only, no device work.  The variant follows the per-p default
+ * unless the environment variable HOFEM_FUSED=mma|simt overrides it. */
+typedef struct {
+  int variant;
+  int bx, by;            /* elements per brick in x, y (one element layer in z) */
+  int zc, nchunks;       /* element layers per work unit; units per column */
+  int grid;              /* persistent CTAs launched */
+  long long direct_points, fixup_points;
+} hofem_fused_info;
+hofem_status hofem_op_fused_info(const void* op, hofem_fused_info* out);
+/* Select the fused kernel of hofem_op_apply for this operator: -1 default
+ * (HOFEM_FUSED env or the measured per-p choice), 0 DMMA, 1 SIMT.  Both
+ * compute the same operator (parity-tested); only the schedule differs.
+ * Ignored for the collocated BP5 kernel.  HOFEM_ERR_ARG if out of range. */
+hofem_status hofem_op_set_fused_variant(void* op, int variant);
+
 /* Number of kernel launches the library issued since the last reset (for the
  * bench's gpu_launches claim); counts every <<<>>> launch of this library. */
 long long hofem_launch_count(void);

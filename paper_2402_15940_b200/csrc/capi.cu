@@ -89,6 +89,20 @@ hofem_status hofem_profile_read(hofem_profile_stats* out) {
   return profile_read(out);
 }
 
+hofem_status hofem_op_set_fused_variant(void* op, int variant) {
+  if (!op || variant < -1 || variant > 1) {
+    set_error("hofem_op_set_fused_variant: need op != NULL and variant in {-1, 0, 1}");
+    return HOFEM_ERR_ARG;
+  }
+  static_cast<Op*>(op)->fused_variant = variant;
+  return HOFEM_OK;
+}
+
+hofem_status hofem_op_fused_info(const void* op, hofem_fused_info* out) {
+  if (!op || !out) { set_error("hofem_op_fused_info: NULL"); return HOFEM_ERR_ARG; }
+  return fused_info(static_cast<const Op*>(op), out);
+}
+
 long long hofem_launch_count(void) { return g_launches.load(); }
 void hofem_launch_count_reset(void) { g_launches.store(0); }
 
@@ -129,7 +143,7 @@ hofem_status hofem_mesh_create(const hofem_mesh_desc* d, void* comm, void* strea
 #define CK(x) do { st = (x); if (st != HOFEM_OK) { free_mesh(m); return st; } } while (0)
   CK(dalloc(&m->d_xi, m->P1, "mesh"));
   CK(dalloc(&m->d_coords, 3 * m->n_local, "mesh coords"));
-  CK(dalloc(&m->d_partials, 2 * kNumSMs + 64, "mesh"));
+  CK(dalloc(&m->d_partials, 4 * kNumSMs + 64, "mesh"));
   CK(dalloc(&m->d_counter, 4, "mesh"));
   CK(dalloc(&m->d_scalars, 16, "mesh"));
   if (R > 1) CK(dalloc(&m->d_recv, 2 * m->plane, "mesh planes"));

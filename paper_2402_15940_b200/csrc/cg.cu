@@ -18,7 +18,7 @@
 
 namespace hofem {
 
-constexpr int kDotBlocks = 2 * kNumSMs;  // fixed grid => fixed reduction order
+constexpr int kDotBlocks = 4 * kNumSMs;  // fixed grid => fixed reduction order
 constexpr int kDotThreads = 512;
 
 namespace {
@@ -64,15 +64,41 @@ __device__ __forceinline__ void finish_reduction(double v, double* partials,
   }
 }
 
+// The vector kernels walk [0, n) in 16-byte pairs (torch allocations are
+// 256-byte aligned), two pairs per thread per iteration for memory-level
+// parallelism; an odd tail element is handled by the last pair's owner.  The
+// traversal order of every thread is fixed, so reductions are deterministic.
+struct Span {
+  long long npair, stride, i0;
+};
+__device__ __forceinline__ Span span(long long n) {
+  Span s;
+  s.npair = n >> 1;
+  s.stride = (long long)gridDim.x * blockDim.x;
+  s.i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  return s;
+}
+
 __global__ void __launch_bounds__(kDotThreads) dot_kernel(long long n, const double* __restrict__ a,
                                                           const double* __restrict__ b,
                                                           double* partials, unsigned int* counter,
                                                           double* out) {
-  double s = 0.0;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
-    s = fma(a[i], b[i], s);
-  finish_reduction(s, partials, counter, out);
+  const Span S = span(n);
+  const double2* a2 = reinterpret_cast<const double2*>(a);
+  const double2* b2 = reinterpret_cast<const double2*>(b);
+  double s0 = 0.0, s1 = 0.0;
+  for (long long i = S.i0; i < S.npair; i += 2 * S.stride) {
+    const double2 x0 = a2[i], y0 = b2[i];
+    s0 = fma(x0.x, y0.x, s0);
+    s0 = fma(x0.y, y0.y, s0);
+    if (i + S.stride < S.npair) {
+      const double2 x1 = a2[i + S.stride], y1 = b2[i + S.stride];
+      s1 = fma(x1.x, y1.x, s1);
+      s1 = fma(x1.y, y1.y, s1);
+    }
+  }
+  if ((n & 1) && S.i0 == 0) s0 = fma(a[n - 1], b[n - 1], s0);
+  finish_reduction(s0 + s1, partials, counter, out);
 }
 
 // r = b - Ax; p = r; rr0 = r.r (owned prefix)
@@ -94,37 +120,85 @@ __global__ void __launch_bounds__(kDotThreads) init_kernel(long long n, long lon
   finish_reduction(s, partials, counter, out);
 }
 
-// alpha = rr/pAp; x += alpha p; r -= alpha Ap; rr' = r.r (owned prefix).
-// sc[0] = rr_k, sc[1] = pAp, out = rr_{k+1}; flag set if pAp <= 0.
-__global__ void __launch_bounds__(kDotThreads) update_kernel(
-    long long n, long long n_owned, const double* __restrict__ p, const double* __restrict__ Ap,
-    double* __restrict__ x, double* __restrict__ r, const double* sc_rr, const double* sc_pAp,
-    double* partials, unsigned int* counter, double* out, double* flag) {
+// alpha = rr/pAp; r -= alpha Ap; rr' = r.r (owned prefix).  The x update is
+// deferred to pupdate_kernel, which reads p anyway (one stream less per
+// iteration; x_{k+1} = x_k + alpha p_k is the same fma either way).
+__device__ __forceinline__ double cg_alpha(const double* sc_rr, const double* sc_pAp) {
   const double pAp = *sc_pAp;
-  double alpha = *sc_rr / pAp;
-  if (!(pAp > 0.0)) {
-    alpha = 0.0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) *flag = 1.0;
-  }
-  double s = 0.0;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
-    x[i] = fma(alpha, p[i], x[i]);
-    double v = fma(-alpha, Ap[i], r[i]);
-    r[i] = v;
-    if (i < n_owned) s = fma(v, v, s);
-  }
-  finish_reduction(s, partials, counter, out);
+  return pAp > 0.0 ? *sc_rr / pAp : 0.0;
 }
 
-// beta = rr_{k+1}/rr_k; p = r + beta p
-__global__ void pupdate_kernel(long long n, const double* __restrict__ r, double* __restrict__ p,
-                               const double* sc_new, const double* sc_old) {
+__global__ void __launch_bounds__(kDotThreads) update_kernel(
+    long long n, long long n_owned, const double* __restrict__ Ap, double* __restrict__ r,
+    const double* sc_rr, const double* sc_pAp, double* partials, unsigned int* counter,
+    double* out, double* flag) {
+  if (!(*sc_pAp > 0.0) && blockIdx.x == 0 && threadIdx.x == 0) *flag = 1.0;
+  const double alpha = cg_alpha(sc_rr, sc_pAp);
+  const Span S = span(n);
+  const double2* A2 = reinterpret_cast<const double2*>(Ap);
+  double2* r2 = reinterpret_cast<double2*>(r);
+  double s0 = 0.0, s1 = 0.0;
+  for (long long i = S.i0; i < S.npair; i += 2 * S.stride) {
+    const long long j = i + S.stride;
+    const bool has1 = j < S.npair;
+    const double2 aa = A2[i], ra = r2[i];
+    double2 ab, rb;
+    if (has1) { ab = A2[j]; rb = r2[j]; }
+    double2 ro;
+    ro.x = fma(-alpha, aa.x, ra.x); ro.y = fma(-alpha, aa.y, ra.y);
+    r2[i] = ro;
+    if (2 * i < n_owned) s0 = fma(ro.x, ro.x, s0);
+    if (2 * i + 1 < n_owned) s0 = fma(ro.y, ro.y, s0);
+    if (has1) {
+      ro.x = fma(-alpha, ab.x, rb.x); ro.y = fma(-alpha, ab.y, rb.y);
+      r2[j] = ro;
+      if (2 * j < n_owned) s1 = fma(ro.x, ro.x, s1);
+      if (2 * j + 1 < n_owned) s1 = fma(ro.y, ro.y, s1);
+    }
+  }
+  if ((n & 1) && S.i0 == 0) {
+    const long long i = n - 1;
+    const double v = fma(-alpha, Ap[i], r[i]);
+    r[i] = v;
+    if (i < n_owned) s0 = fma(v, v, s0);
+  }
+  finish_reduction(s0 + s1, partials, counter, out);
+}
+
+// x += alpha_k p; beta = rr_{k+1}/rr_k; p = r + beta p
+__global__ void __launch_bounds__(kDotThreads) pupdate_kernel(
+    long long n, const double* __restrict__ r, double* __restrict__ p, double* __restrict__ x,
+    const double* sc_new, const double* sc_old, const double* sc_pAp) {
+  const double alpha = cg_alpha(sc_old, sc_pAp);
   const double rn = *sc_new, ro = *sc_old;
   const double beta = ro > 0.0 ? rn / ro : 0.0;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
-    p[i] = fma(beta, p[i], r[i]);
+  const Span S = span(n);
+  const double2* r2 = reinterpret_cast<const double2*>(r);
+  double2* p2 = reinterpret_cast<double2*>(p);
+  double2* x2 = reinterpret_cast<double2*>(x);
+  for (long long i = S.i0; i < S.npair; i += 2 * S.stride) {
+    const long long j = i + S.stride;
+    const bool has1 = j < S.npair;
+    const double2 ra = r2[i], pa = p2[i], xa = x2[i];
+    double2 rb, pb, xb;
+    if (has1) { rb = r2[j]; pb = p2[j]; xb = x2[j]; }
+    double2 o;
+    o.x = fma(alpha, pa.x, xa.x); o.y = fma(alpha, pa.y, xa.y);
+    x2[i] = o;
+    o.x = fma(beta, pa.x, ra.x); o.y = fma(beta, pa.y, ra.y);
+    p2[i] = o;
+    if (has1) {
+      o.x = fma(alpha, pb.x, xb.x); o.y = fma(alpha, pb.y, xb.y);
+      x2[j] = o;
+      o.x = fma(beta, pb.x, rb.x); o.y = fma(beta, pb.y, rb.y);
+      p2[j] = o;
+    }
+  }
+  if ((n & 1) && S.i0 == 0) {
+    const double pv = p[n - 1];
+    x[n - 1] = fma(alpha, pv, x[n - 1]);
+    p[n - 1] = fma(beta, pv, r[n - 1]);
+  }
 }
 
 }  // namespace
@@ -187,12 +261,13 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
                                                   m->d_counter, pAp);
     HOFEM_LAUNCHED();
     HOFEM_TRY(allreduce_sum(m, pAp, 1, s));
-    update_kernel<<<kDotBlocks, kDotThreads, 0, s>>>(n, no, op->d_p, op->d_Ap, x, op->d_r, rr + k,
-                                                     pAp, m->d_partials, m->d_counter,
-                                                     rr + k + 1, flag);
+    update_kernel<<<kDotBlocks, kDotThreads, 0, s>>>(n, no, op->d_Ap, op->d_r, rr + k, pAp,
+                                                     m->d_partials, m->d_counter, rr + k + 1,
+                                                     flag);
     HOFEM_LAUNCHED();
     HOFEM_TRY(allreduce_sum(m, rr + k + 1, 1, s));
-    pupdate_kernel<<<vgrid, 256, 0, s>>>(n, op->d_r, op->d_p, rr + k + 1, rr + k);
+    pupdate_kernel<<<vgrid, kDotThreads, 0, s>>>(n, op->d_r, op->d_p, x, rr + k + 1, rr + k,
+                                                 pAp);
     HOFEM_LAUNCHED();
     ++k;
     if ((!fixed_iters && k % check_every == 0) || k == max_iter) {

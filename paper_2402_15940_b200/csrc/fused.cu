@@ -4,7 +4,9 @@
 // a work-unit boundary plane sums the partials of its 2, 4 or 8 bricks in
 // ascending brick order.
 #include <stdlib.h>
+#include <string.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "fused_impl.cuh"
@@ -14,10 +16,12 @@ namespace hofem {
 #define HOFEM_FOR_P1(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9)
 #define HOFEM_DECL(P1)                                                                     \
   template <>                                                                              \
-  bool fused_launch<P1>(int, int, const double*, const double*, const ColArgs&, int,       \
+  bool fused_launch<P1>(int, int, int, const double*, const double*, const ColArgs&, int,  \
                         cudaStream_t, cudaError_t*);                                       \
   template <>                                                                              \
-  FusedLaunch fused_shape<P1>(int);
+  FusedLaunch fused_shape<P1>(int, int);                                                   \
+  template <>                                                                              \
+  int fused_default_variant<P1>();
 HOFEM_FOR_P1(HOFEM_DECL)
 #undef HOFEM_DECL
 
@@ -27,88 +31,125 @@ struct FixArgs {
   const double* x;
   double* y;
   const double* bbuf;
-  long long Nx, Ny, Nzl, K0, NzG;
+  long long K0, NzG;
+  int Nx, Ny, Nzl;
   int p, PX, PY, PZU, LX, LY, nbx, nby, nzl, bc;
-  long long BLAT, nZ, nY, nX;
+  int FB, OY, OZ, FXS, FYS, FZS;  // FaceLayout<> of the launched kernel
+  int nplZ, nplY, nplX;           // interior brick-boundary planes per axis
 };
 
-__device__ __forceinline__ bool on_plane(long long I, int P, long long N) {
+__device__ __forceinline__ bool on_plane(int I, int P, int N) {
   return I % P == 0 && I > 0 && I < N - 1;
 }
 
-__device__ __forceinline__ int axis_bricks(long long I, int P, int nb, long long N, int L,
-                                           int* br, int* loc) {
-  if (on_plane(I, P, N)) {
-    br[0] = (int)(I / P) - 1; loc[0] = L - 1;
-    br[1] = (int)(I / P);     loc[1] = 0;
+__device__ __forceinline__ int axis_bricks(int I, int P, int nb, int L, bool split, int* br,
+                                           int* loc) {
+  if (split) {
+    br[0] = I / P - 1; loc[0] = L - 1;
+    br[1] = I / P;     loc[1] = 0;
     return 2;
   }
-  int b = (int)(I / P);
+  int b = I / P;
   if (b > nb - 1) b = nb - 1;
   br[0] = b;
-  loc[0] = (int)(I - (long long)P * b);
+  loc[0] = I - P * b;
   return 1;
 }
 
 // z: bricks are single element layers; only work-unit boundary planes (every
 // PZU = p*zc lattice planes) are split between two bricks -- element faces
 // inside a unit were summed through the in-kernel carry into the upper brick.
-__device__ __forceinline__ int axis_bricks_z(long long K, int p, int PZU, int nzl, long long N,
-                                             int* br, int* loc) {
-  if (on_plane(K, PZU, N)) {
-    br[0] = (int)(K / p) - 1; loc[0] = p;
-    br[1] = (int)(K / p);     loc[1] = 0;
+__device__ __forceinline__ int axis_bricks_z(int K, int p, int nzl, bool split, int* br,
+                                             int* loc) {
+  if (split) {
+    br[0] = K / p - 1; loc[0] = p;
+    br[1] = K / p;     loc[1] = 0;
     return 2;
   }
-  int b = (int)(K / p);
+  int b = K / p;
   if (b > nzl - 1) b = nzl - 1;
   br[0] = b;
-  loc[0] = (int)(K - (long long)p * b);
+  loc[0] = K - p * b;
   return 1;
 }
 
-__global__ void fixup_kernel(FixArgs F) {
-  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long I, J, K;
-  if (t < F.nZ) {
-    long long m = t / (F.Nx * F.Ny) + 1, r = t % (F.Nx * F.Ny);
+// grid (ceil(max plane size / 256), max planes, 3): blockIdx.z = 0 z-unit
+// planes, 1 y planes, 2 x planes; a point on several planes is summed once, by
+// the first of them.  The threads of a warp walk the fastest face-block index
+// of the plane type, so the partial reads come in runs.
+__global__ void __launch_bounds__(256) fixup_kernel(FixArgs F) {
+  const int type = blockIdx.z, m = blockIdx.y + 1;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  int I, J, K;
+  if (type == 0) {
+    if (m > F.nplZ || r >= F.Nx * F.Ny) return;
     K = m * F.PZU; I = r % F.Nx; J = r / F.Nx;
-  } else if ((t -= F.nZ) < F.nY) {
-    long long m = t / (F.Nx * F.Nzl) + 1, r = t % (F.Nx * F.Nzl);
+  } else if (type == 1) {
+    if (m > F.nplY || r >= F.Nx * F.Nzl) return;
     J = m * F.PY; I = r % F.Nx; K = r / F.Nx;
     if (on_plane(K, F.PZU, F.Nzl)) return;
-  } else if ((t -= F.nY) < F.nX) {
-    long long m = t / (F.Ny * F.Nzl) + 1, r = t % (F.Ny * F.Nzl);
+  } else {
+    if (m > F.nplX || r >= F.Ny * F.Nzl) return;
     I = m * F.PX; J = r % F.Ny; K = r / F.Ny;
     if (on_plane(J, F.PY, F.Ny) || on_plane(K, F.PZU, F.Nzl)) return;
-  } else {
-    return;
   }
+  const bool zs = on_plane(K, F.PZU, F.Nzl), ys = on_plane(J, F.PY, F.Ny),
+             xs = on_plane(I, F.PX, F.Nx);
   int bx[2], ix[2], by[2], iy[2], bz[2], iz[2];
-  int nbxl = axis_bricks(I, F.PX, F.nbx, F.Nx, F.LX, bx, ix);
-  int nbyl = axis_bricks(J, F.PY, F.nby, F.Ny, F.LY, by, iy);
-  int nbzl = axis_bricks_z(K, F.p, F.PZU, F.nzl, F.Nzl, bz, iz);
+  const int nbxl = axis_bricks(I, F.PX, F.nbx, F.LX, xs, bx, ix);
+  const int nbyl = axis_bricks(J, F.PY, F.nby, F.LY, ys, by, iy);
+  const int nbzl = axis_bricks_z(K, F.p, F.nzl, zs, bz, iz);
   double s = 0.0;
   for (int c = 0; c < nbzl; ++c)
     for (int b = 0; b < nbyl; ++b)
       for (int a = 0; a < nbxl; ++a) {
-        long long brick = bx[a] + (long long)F.nbx * (by[b] + (long long)F.nby * bz[c]);
-        s += F.bbuf[brick * F.BLAT + ix[a] + F.LX * (iy[b] + (long long)F.LY * iz[c])];
+        const long long brick = bx[a] + (long long)F.nbx * (by[b] + (long long)F.nby * bz[c]);
+        int off;
+        if (zs)
+          off = F.OZ + (c == 0) * F.FZS + iy[b] * F.LX + ix[a];
+        else if (ys)
+          off = F.OY + (b == 0) * F.FYS + iz[c] * F.LX + ix[a];
+        else
+          off = (a == 0) * F.FXS + iz[c] * F.LY + iy[b];
+        s += F.bbuf[brick * F.FB + off];
       }
-  long long l = I + F.Nx * (J + F.Ny * K);
+  const long long l = I + (long long)F.Nx * (J + (long long)F.Ny * K);
   if (F.bc) {
-    long long Kg = K + F.K0;
+    const long long Kg = K + F.K0;
     if (I == 0 || I == F.Nx - 1 || J == 0 || J == F.Ny - 1 || Kg == 0 || Kg == F.NzG - 1)
       s = F.x[l];
   }
   F.y[l] = s;
 }
 
-FusedLaunch shape_for(int P1, int kind) {
+// Tuning knob HOFEM_FUSED = "mma" | "simt" overrides the per-p default kernel.
+int fused_variant() {
+  static const int v = [] {
+    const char* e = getenv("HOFEM_FUSED");
+    if (!e) return -1;
+    if (!strcmp(e, "mma")) return 0;
+    if (!strcmp(e, "simt")) return 1;
+    return -1;
+  }();
+  return v;
+}
+
+int default_variant(int P1) {
   switch (P1) {
 #define HOFEM_CASE(P) \
   case P:             \
-    return fused_shape<P>(kind);
+    return fused_default_variant<P>();
+    HOFEM_FOR_P1(HOFEM_CASE)
+#undef HOFEM_CASE
+  }
+  return 0;
+}
+
+FusedLaunch shape_for(int P1, int kind, int variant) {
+  switch (P1) {
+#define HOFEM_CASE(P) \
+  case P:             \
+    return fused_shape<P>(kind, variant);
     HOFEM_FOR_P1(HOFEM_CASE)
 #undef HOFEM_CASE
   }
@@ -200,20 +241,61 @@ void choose_chunks(long long ncol, int nzl, int G, int* zc_out, int* nchunks_out
   *nchunks_out = bn;
 }
 
+namespace {
+struct Plan {
+  int variant, kind;
+  FusedLaunch L;
+  int nbx, nby, zc, nchunks, grid;
+  long long ncol, nbricks, nunits;
+};
+Plan make_plan(const Op* op) {
+  const Mesh* m = op->mesh;
+  Plan P;
+  P.kind = fused_kind(op);
+  const int v = op->fused_variant >= 0 ? op->fused_variant : fused_variant();
+  P.variant = P.kind == KIND_COLLOC ? 2 : (v < 0 ? default_variant(m->P1) : v);
+  P.L = shape_for(m->P1, P.kind, P.variant == 2 ? 0 : P.variant);
+  P.nbx = (m->nx + P.L.BX - 1) / P.L.BX;
+  P.nby = (m->ny + P.L.BY - 1) / P.L.BY;
+  P.ncol = (long long)P.nbx * P.nby;
+  P.nbricks = P.ncol * m->nzl;
+  const int G0 = num_sms() * P.L.ctas_per_sm;
+  P.zc = 1;
+  P.nchunks = 1;
+  choose_chunks(P.ncol, m->nzl, G0, &P.zc, &P.nchunks);
+  P.nunits = P.ncol * P.nchunks;
+  P.grid = (int)(P.nunits < G0 ? P.nunits : G0);
+  return P;
+}
+}  // namespace
+
+hofem_status fused_info(const Op* op, hofem_fused_info* out) {
+  if (!fused_supported(op)) {
+    *out = hofem_fused_info{-1, 0, 0, 0, 0, 0, 0, 0};
+    return HOFEM_OK;
+  }
+  const Mesh* m = op->mesh;
+  const Plan P = make_plan(op);
+  out->variant = P.variant;
+  out->bx = P.L.BX; out->by = P.L.BY; out->zc = P.zc; out->nchunks = P.nchunks;
+  out->grid = P.grid;
+  const long long N = m->Nx * m->Ny * m->Nzl;
+  const long long inner = (m->Nx - (P.nbx - 1)) * (m->Ny - (P.nby - 1)) * (m->Nzl - (P.nchunks - 1));
+  out->fixup_points = N - inner;
+  out->direct_points = inner;
+  return HOFEM_OK;
+}
+
 hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s) {
   Mesh* m = op->mesh;
-  const int P1 = m->P1, p = m->p, kind = fused_kind(op);
-  FusedLaunch L = shape_for(P1, kind);
-  const int nbx = (m->nx + L.BX - 1) / L.BX, nby = (m->ny + L.BY - 1) / L.BY;
-  const long long ncol = (long long)nbx * nby;
-  const long long nbricks = ncol * m->nzl;
+  const int P1 = m->P1, p = m->p;
+  const Plan PL = make_plan(op);
+  const int kind = PL.kind, variant = PL.variant == 2 ? 0 : PL.variant;
+  const FusedLaunch L = PL.L;
+  const int nbx = PL.nbx, nby = PL.nby, zc = PL.zc, nchunks = PL.nchunks, grid = PL.grid;
+  const long long nbricks = PL.nbricks, nunits = PL.nunits;
   if (nbricks == 0) return HOFEM_OK;
-  const int G0 = num_sms() * L.ctas_per_sm;
-  int zc = 1, nchunks = 1;
-  choose_chunks(ncol, m->nzl, G0, &zc, &nchunks);
-  const long long nunits = ncol * nchunks;
-  const int grid = (int)(nunits < G0 ? nunits : G0);
-  const long long need = nbricks * L.blat;
+  const long long need = nbricks * L.face_block;
   if (op->bbuf_len < need) {
     if (op->d_bbuf) cudaFree(op->d_bbuf);
     op->d_bbuf = nullptr;
@@ -247,7 +329,7 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s) {
   switch (P1) {
 #define HOFEM_CASE(P)                                                            \
   case P:                                                                        \
-    ok = fused_launch<P>(kind, op->Q, op->tab.B, op->tab.G, A, grid, s, &err);   \
+    ok = fused_launch<P>(kind, variant, op->Q, op->tab.B, op->tab.G, A, grid, s, &err); \
     break;
     HOFEM_FOR_P1(HOFEM_CASE)
 #undef HOFEM_CASE
@@ -264,21 +346,28 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s) {
   }
   FixArgs F;
   F.x = x; F.y = y; F.bbuf = op->d_bbuf;
-  F.Nx = m->Nx; F.Ny = m->Ny; F.Nzl = m->Nzl; F.K0 = A.K0; F.NzG = m->NzG;
+  F.Nx = (int)m->Nx; F.Ny = (int)m->Ny; F.Nzl = (int)m->Nzl; F.K0 = A.K0; F.NzG = m->NzG;
   F.p = p; F.PX = p * L.BX; F.PY = p * L.BY; F.PZU = p * zc;
   F.LX = F.PX + 1; F.LY = F.PY + 1;
   F.nbx = nbx; F.nby = nby; F.nzl = m->nzl; F.bc = op->bc;
-  F.BLAT = L.blat;
-  F.nZ = (long long)(nchunks - 1) * m->Nx * m->Ny;
-  F.nY = (long long)(nby - 1) * m->Nx * m->Nzl;
-  F.nX = (long long)(nbx - 1) * m->Ny * m->Nzl;
-  const long long nt = F.nZ + F.nY + F.nX;
-  if (nt > 0) {
+  F.FXS = (p + 1) * F.LY; F.OY = 2 * F.FXS;
+  F.FYS = (p + 1) * F.LX; F.OZ = F.OY + 2 * F.FYS;
+  F.FZS = F.LX * F.LY; F.FB = F.OZ + 2 * F.FZS;
+  if (F.FB != L.face_block) {
+    set_error("fused apply: face-block layout mismatch (%d vs %d)", F.FB, L.face_block);
+    return HOFEM_ERR_ARG;
+  }
+  F.nplZ = nchunks - 1; F.nplY = nby - 1; F.nplX = nbx - 1;
+  const int npl = std::max(F.nplZ, std::max(F.nplY, F.nplX));
+  const long long psz = std::max((long long)F.Nx * F.Ny,
+                                 std::max((long long)F.Nx * F.Nzl, (long long)F.Ny * F.Nzl));
+  if (npl > 0) {
     if (g_prof.on) {
       ev = {prof_event(), prof_event()};
       cudaEventRecord(ev.first, s);
     }
-    fixup_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(F);
+    const dim3 fg((unsigned)((psz + 255) / 256), (unsigned)npl, 3);
+    fixup_kernel<<<fg, 256, 0, s>>>(F);
     HOFEM_LAUNCHED();
     if (g_prof.on) {
       cudaEventRecord(ev.second, s);

@@ -31,6 +31,8 @@
 // doubles (conflict-free 64-bit accesses): see DESIGN.md §4.
 #pragma once
 
+#include <type_traits>
+
 #include "internal.h"
 
 #ifndef HOFEM_QLD
@@ -186,10 +188,30 @@ __device__ __forceinline__ void issue_lattice(const ColArgs& A, double* L, long 
 // k == 0 adds the carried top plane of the previous brick first; k == p goes to
 // the carry unless the brick ends the unit.
 // ---------------------------------------------------------------------------
+// Brick face block in the partial buffer (one per brick): the values of the
+// lattice points the brick shares with a neighbour brick, stored by face so the
+// fix-up kernel reads them in runs: x faces [xs][k][j], y faces [ys][k][i],
+// z-unit faces [zs][j][i].  A point on several shared faces is stored once, by
+// the priority z > y > x (the fix-up applies the same rule).
+template <int p, int LX, int LY>
+struct FaceLayout {
+  static constexpr int P1 = p + 1;
+  static constexpr int FXS = P1 * LY;           // x face stride (xs)
+  static constexpr int OY = 2 * FXS;            // y faces
+  static constexpr int FYS = P1 * LX;
+  static constexpr int OZ = OY + 2 * FYS;       // z faces
+  static constexpr int FZS = LX * LY;
+  static constexpr int FB = OZ + 2 * FZS;       // doubles per brick
+  __device__ __forceinline__ static int xf(int xs, int k, int j) { return xs * FXS + k * LY + j; }
+  __device__ __forceinline__ static int yf(int ys, int k) { return OY + ys * FYS + k * LX; }
+  __device__ __forceinline__ static int zf(int zs, int j) { return OZ + zs * FZS + j * LX; }
+};
+
 struct EpiRow {
   const double* cin;
   double* cout;
-  double* bb;
+  double* bb;   // shared-face row (z-unit or y face) in the brick's face block
+  double* bxf;  // x-face slot (xs = 0) of this row; xs = 1 at + FXS
   long long gl;
   int base0, base1;  // y-element offsets of the lower / primary contributions
   bool vy0, vy1, to_carry, from_carry, row_sh, row_ess;
@@ -242,8 +264,10 @@ __device__ __forceinline__ void epi_segment(const ColArgs& A, const double* RA, 
 #pragma unroll
     for (int ii = 0; ii < NPT; ++ii) {
       const bool lo = (SX == 0 && ii == 0), hi = (SX == BX - 1 && ii == p);
-      if ((lo && xlo_sh) || (hi && xhi_sh))
-        R.bb[p * SX + ii] = v[ii];
+      if (lo && xlo_sh)
+        R.bxf[0] = v[ii];
+      else if (hi && xhi_sh)
+        R.bxf[FaceLayout<p, LX, C::LY>::FXS] = v[ii];
       else
         A.y[R.gl + p * SX + ii] = v[ii];
     }
@@ -254,8 +278,10 @@ __device__ __forceinline__ void epi_segment(const ColArgs& A, const double* RA, 
     const int i = p * SX + ii;
     if (i >= nv) continue;
     const bool lo = (SX == 0 && ii == 0), hi = (SX == BX - 1 && ii == p);
-    if ((lo && xlo_sh) || (hi && xhi_sh)) {
-      R.bb[i] = v[ii];
+    if (lo && xlo_sh) {
+      R.bxf[0] = v[ii];
+    } else if (hi && xhi_sh) {
+      R.bxf[FaceLayout<p, LX, C::LY>::FXS] = v[ii];
     } else {
       const bool ess = R.row_ess || (lo && xlo_ess) || (i == ie);
       A.y[R.gl + i] = ess ? A.x[R.gl + i] : v[ii];
@@ -309,7 +335,17 @@ __device__ __forceinline__ void brick_epilogue(const ColArgs& A, const double* R
                (k == 0 && first && K > 0) || (k == p && last && K < A.Nzl - 1);
     R.row_ess = A.bc && (J == 0 || J == A.Ny - 1 || Kg == 0 || Kg == A.NzG - 1);
     R.gl = I0 + A.Nx * (J + A.Ny * K);
-    R.bb = A.bbuf + brick * C::BLAT + LX * (j + LY * k);
+    {
+      using FL = FaceLayout<p, LX, LY>;
+      double* fb = A.bbuf + brick * FL::FB;
+      if (k == 0 && first && K > 0)
+        R.bb = fb + FL::zf(0, j);
+      else if (k == p && last && K < A.Nzl - 1)
+        R.bb = fb + FL::zf(1, j);
+      else
+        R.bb = fb + FL::yf(j == 0 ? 0 : 1, k);
+      R.bxf = fb + FL::xf(0, k, j);
+    }
     R.cin = carry_in + LX * j;
     R.cout = carry_out + LX * j;
     epi_dispatch<C, BX, NATURAL, ESTRIDE, 0>(sx, A, RA, R, I0, nvx, iess, exok, xlo_sh, xhi_sh,
@@ -1237,6 +1273,364 @@ constexpr int smem_bytes_elem() {
 }
 
 // ---------------------------------------------------------------------------
+// SIMT kernel (mass / diffusion): thread-per-line sum factorization.
+//
+// Every 1D contraction is an item = one line of the element tensor held in
+// registers: a thread loads the line's P (or Q) inputs and produces all Q (or P)
+// outputs of every product at once, so the FP64 FMA chains are independent
+// (ILP 7..21) and the table operands are compile-time constant-bank entries
+// (uniform-register DFMA operands; no shared traffic for B/G).  Items of all
+// NE elements of the brick are spread over the CTA's threads; stages are
+// separated by __syncthreads.  Stage 3 (z, pointwise D, z back) runs entirely
+// in registers with D read straight from L2 (prefetched one brick ahead).
+//   S1  item (b,c):  T1[m][qx][b][c]   m: 0 = B_x x, 1 = G_x x
+//   S2  item (qx,c): T2[m][qy][qx][c]  m: 0 = G_x B_y, 1 = B_x G_y, 2 = B_x B_y
+//   S3  item (qx,qy): in place in T2: z contraction, D, z back-contraction
+//   S2T item (qx,c): T1[0] = B_y^T (.. y,z parts), T1[1] = B_y^T (x part)
+//   S1T item (b,c):  y_e[a][b][c] (aliases T2)
+// Strides: S1 == P (mod 16) and c-fastest S2 items make S2/S2T's T1 accesses
+// conflict-free; SP (the T2 point stride) is odd so S3 is conflict-free
+// (scripts/simt_layout.py checks the layouts).
+// ---------------------------------------------------------------------------
+// Volatile read-only load: stays in program order w.r.t. the other volatile
+// loads, so a register pipeline written in the source is kept.
+__device__ __forceinline__ double ld_nc_v(const double* ptr) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(ptr));
+  return v;
+}
+
+template <int KIND, int P1, int Q, int BX, int BY>
+struct CfgS {
+  static constexpr int p = P1 - 1, P = P1, NE = BX * BY;
+  static constexpr int LX = p * BX + 1, LY = p * BY + 1, LZ = P1;
+  static constexpr int LXS = ((LY * LZ) % 2 == 0) ? LY * LZ + 1 : LY * LZ;
+  static constexpr int LAT = LXS * LX;
+  static constexpr int cmax(int a, int b) { return a > b ? a : b; }
+  static constexpr int NA = (KIND == KIND_MASS) ? 1 : 2;
+  static constexpr int NB = (KIND == KIND_MASS) ? 1 : 3;
+  static constexpr int NC = (KIND == KIND_MASS) ? 1 : 6;
+  static constexpr int S1 = P * P + (((P - P * P) % 16) + 16) % 16;
+  static constexpr int T1M = Q * S1, T1SZ = NA * T1M;
+  static constexpr int SP = (P % 2) ? P : P + 1;
+  static constexpr int T2M = Q * Q * SP;
+  static constexpr int SA = ((P * P) % 2 == 0) ? P * P + 1 : P * P;
+  static constexpr int YEN = SA * P;
+  static constexpr int EB0 = T1SZ + cmax(NB * T2M, YEN);
+  static constexpr int EB = EB0 + ((7 - EB0) % 16 + 16) % 16;  // == 7 (mod 16)
+  static constexpr int CARRY = LX * LY;
+  static constexpr int PR = P + (P & 1);  // table row stride
+  static constexpr int TOFF0 = NE * EB + 2 * LAT + 2 * CARRY;
+  static constexpr int TOFF = TOFF0 + (TOFF0 & 1);  // tables 16-byte aligned
+  static constexpr int SMEM_DOUBLES = TOFF + 2 * Q * PR;
+  static constexpr int SMEM_BYTES = SMEM_DOUBLES * 8;
+  static constexpr int NQ1 = Q;
+  __device__ static constexpr int lat(int i, int j, int k) { return k + LZ * j + LXS * i; }
+};
+
+// One row of the shared-memory tables (B or G, row stride PR even) into
+// registers with 16-byte broadcast loads.
+template <int P, int PR>
+__device__ __forceinline__ void ld_row(const double* row, double (&r)[P]) {
+#pragma unroll
+  for (int c = 0; c + 1 < P; c += 2) {
+    const double2 v = *reinterpret_cast<const double2*>(row + c);
+    r[c] = v.x;
+    r[c + 1] = v.y;
+  }
+  if (P & 1) r[P - 1] = row[P - 1];
+}
+
+template <int KIND, int P1, int Q, int BX, int BY, int NT, int MAXR>
+__global__ void __maxnreg__(MAXR)
+    fused_elem_simt(const __grid_constant__ Tab<P1, Q> T, const __grid_constant__ ColArgs A) {
+  using C = CfgS<KIND, P1, Q, BX, BY>;
+  constexpr int P = P1, p = P1 - 1, NE = C::NE;
+  constexpr int Q2 = Q * Q, Q3 = Q * Q * Q;
+  constexpr bool DIFF = KIND == KIND_DIFF;
+  constexpr int EB = C::EB, S1 = C::S1, T1M = C::T1M, T1SZ = C::T1SZ, SP = C::SP,
+                T2M = C::T2M, PR = C::PR;
+  extern __shared__ __align__(16) double smem[];
+  double* LB = smem + NE * EB;
+  double* CY = LB + 2 * C::LAT;
+  double* TBs = smem + C::TOFF;  // B[q][c], row stride PR (16-byte aligned)
+  double* TGs = TBs + Q * PR;
+
+  for (int i = threadIdx.x; i < C::SMEM_DOUBLES; i += NT) smem[i] = 0.0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < Q * P; i += NT) {
+    TBs[(i / P) * PR + i % P] = T.B[i];
+    TGs[(i / P) * PR + i % P] = T.G[i];
+  }
+  __syncthreads();
+
+  Brick cur = unit_first(A, blockIdx.x);
+  if (cur.u >= A.nunits) return;
+  prefetch_qdata_l2<C, BX, BY>(A, cur);
+  issue_lattice<C, NT, BX>(A, LB, (long long)p * cur.bx * BX, (long long)p * cur.by * BY,
+                           (long long)p * cur.ez);
+  cp_async_wait_all();
+  __syncthreads();
+
+  for (int kb = 0; cur.u < A.nunits; ++kb) {
+    const int tid = vtid();
+    const Brick nxt = brick_next(A, cur);
+    const int ex0 = cur.bx * BX, ey0 = cur.by * BY, ez = cur.ez;
+    const long long I0 = (long long)p * ex0, J0 = (long long)p * ey0;
+    const double* L = LB + (kb & 1) * C::LAT;
+    if (nxt.u < A.nunits) {
+      issue_lattice<C, NT, BX>(A, LB + ((kb + 1) & 1) * C::LAT, (long long)p * nxt.bx * BX,
+                               (long long)p * nxt.by * BY, (long long)p * nxt.ez);
+      prefetch_qdata_l2<C, BX, BY>(A, nxt);
+    }
+
+    // ---- S1: contract x.  item (el, b, c), c fastest.
+    for (int it = tid; it < NE * P * P; it += NT) {
+      const int el = it / (P * P), r = it % (P * P), b = r / P, c = r % P;
+      const double* xl = L + C::lat(p * (el % BX), p * (el / BX) + b, c);
+      double xa[P];
+#pragma unroll
+      for (int a = 0; a < P; ++a) xa[a] = xl[C::LXS * a];
+      double* t1 = smem + el * EB + r;
+#pragma unroll
+      for (int qx = 0; qx < Q; ++qx) {
+        double br[P], gr[P];
+        ld_row<P, PR>(TBs + qx * PR, br);
+        if (DIFF) ld_row<P, PR>(TGs + qx * PR, gr);
+        double sb = 0.0, sg = 0.0;
+#pragma unroll
+        for (int a = 0; a < P; ++a) {
+          sb = fma(br[a], xa[a], sb);
+          if (DIFF) sg = fma(gr[a], xa[a], sg);
+        }
+        t1[qx * S1] = sb;
+        if (DIFF) t1[T1M + qx * S1] = sg;
+      }
+    }
+    __syncthreads();
+
+    // ---- S2: contract y.  item (el, qx, c), c fastest.
+    for (int it = tid; it < NE * Q * P; it += NT) {
+      const int el = it / (Q * P), r = it % (Q * P), qx = r / P, c = r % P;
+      const double* t1 = smem + el * EB + qx * S1 + c;
+      double vb[P], vg[P];
+#pragma unroll
+      for (int b = 0; b < P; ++b) {
+        vb[b] = t1[b * P];
+        vg[b] = DIFF ? t1[T1M + b * P] : 0.0;
+      }
+      double* t2 = smem + el * EB + T1SZ + qx * SP + c;
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy) {
+        double br[P], gr[P];
+        ld_row<P, PR>(TBs + qy * PR, br);
+        if (DIFF) ld_row<P, PR>(TGs + qy * PR, gr);
+        double bb = 0.0, gb = 0.0, bg = 0.0;
+#pragma unroll
+        for (int b = 0; b < P; ++b) {
+          bb = fma(br[b], vb[b], bb);
+          if (DIFF) {
+            gb = fma(br[b], vg[b], gb);
+            bg = fma(gr[b], vb[b], bg);
+          }
+        }
+        if (DIFF) {
+          t2[qy * Q * SP] = gb;            // G_x B_y  (-> u_x)
+          t2[T2M + qy * Q * SP] = bg;      // B_x G_y  (-> u_y)
+          t2[2 * T2M + qy * Q * SP] = bb;  // B_x B_y  (-> u_z)
+        } else {
+          t2[qy * Q * SP] = bb;
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- S3: z contraction, pointwise D, z back-contraction; item (el, pt).
+    //      Streamed over qz: u(qz) -> w(qz) = D u -> s += B/G(qz) w.  D(qz+1)
+    //      is loaded (volatile, in program order) while qz computes.
+    for (int it = tid; it < NE * Q2; it += NT) {
+      const int el = it / Q2, pt = it % Q2;
+      const int ex = ex0 + el % BX, ey = ey0 + el / BX;
+      if (ex >= A.nx || ey >= A.ny) continue;
+      const double* qde = A.qd +
+                          (ex + (long long)A.nx * (ey + (long long)A.ny * ez)) *
+                              (long long)(C::NC * Q3) + pt;
+      double* t2 = smem + el * EB + T1SZ + pt * SP;
+      if (DIFF) {
+        double g0[P], g1[P], g2[P], s0[P], s1[P], s2[P];
+#pragma unroll
+        for (int c = 0; c < P; ++c) {
+          g0[c] = t2[c];
+          g1[c] = t2[T2M + c];
+          g2[c] = t2[2 * T2M + c];
+          s0[c] = s1[c] = s2[c] = 0.0;
+        }
+        double dn[6];
+#pragma unroll
+        for (int m = 0; m < 6; ++m) dn[m] = ld_nc_v(qde + m * Q3);
+#pragma unroll
+        for (int qz = 0; qz < Q; ++qz) {
+          double dc[6];
+#pragma unroll
+          for (int m = 0; m < 6; ++m) dc[m] = dn[m];
+          if (qz + 1 < Q) {
+#pragma unroll
+            for (int m = 0; m < 6; ++m) dn[m] = ld_nc_v(qde + m * Q3 + (qz + 1) * Q2);
+          }
+          double br[P], gr[P];
+          ld_row<P, PR>(TBs + qz * PR, br);
+          ld_row<P, PR>(TGs + qz * PR, gr);
+          double u0 = 0.0, u1 = 0.0, u2 = 0.0;
+#pragma unroll
+          for (int c = 0; c < P; ++c) {
+            u0 = fma(br[c], g0[c], u0);
+            u1 = fma(br[c], g1[c], u1);
+            u2 = fma(gr[c], g2[c], u2);
+          }
+          const double w0 = dc[0] * u0 + dc[1] * u1 + dc[2] * u2;
+          const double w1 = dc[1] * u0 + dc[3] * u1 + dc[4] * u2;
+          const double w2 = dc[2] * u0 + dc[4] * u1 + dc[5] * u2;
+#pragma unroll
+          for (int c = 0; c < P; ++c) {
+            s0[c] = fma(br[c], w0, s0[c]);
+            s1[c] = fma(br[c], w1, s1[c]);
+            s2[c] = fma(gr[c], w2, s2[c]);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < P; ++c) {
+          t2[c] = s0[c];
+          t2[T2M + c] = s1[c];
+          t2[2 * T2M + c] = s2[c];
+        }
+      } else {
+        double g[P], s[P];
+#pragma unroll
+        for (int c = 0; c < P; ++c) { g[c] = t2[c]; s[c] = 0.0; }
+        double dn = ld_nc_v(qde);
+#pragma unroll
+        for (int qz = 0; qz < Q; ++qz) {
+          const double dc = dn;
+          if (qz + 1 < Q) dn = ld_nc_v(qde + (qz + 1) * Q2);
+          double br[P];
+          ld_row<P, PR>(TBs + qz * PR, br);
+          double u = 0.0;
+#pragma unroll
+          for (int c = 0; c < P; ++c) u = fma(br[c], g[c], u);
+          const double v = dc * u;
+#pragma unroll
+          for (int c = 0; c < P; ++c) s[c] = fma(br[c], v, s[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < P; ++c) t2[c] = s[c];
+      }
+    }
+    __syncthreads();
+
+    // ---- S2T: contract qy.  item (el, qx, c), c fastest.
+    for (int it = tid; it < NE * Q * P; it += NT) {
+      const int el = it / (Q * P), r = it % (Q * P), qx = r / P, c = r % P;
+      const double* t2 = smem + el * EB + T1SZ + qx * SP + c;
+      double* t1 = smem + el * EB + qx * S1 + c;
+      double rb[P], rg[P];
+#pragma unroll
+      for (int b = 0; b < P; ++b) rb[b] = rg[b] = 0.0;
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy) {
+        double br[P], gr[P];
+        ld_row<P, PR>(TBs + qy * PR, br);
+        if (DIFF) {
+          ld_row<P, PR>(TGs + qy * PR, gr);
+          const double v0 = t2[qy * Q * SP], v1 = t2[T2M + qy * Q * SP],
+                       v2 = t2[2 * T2M + qy * Q * SP];
+#pragma unroll
+          for (int b = 0; b < P; ++b) {
+            rg[b] = fma(br[b], v0, rg[b]);
+            rb[b] = fma(gr[b], v1, rb[b]);
+            rb[b] = fma(br[b], v2, rb[b]);
+          }
+        } else {
+          const double v = t2[qy * Q * SP];
+#pragma unroll
+          for (int b = 0; b < P; ++b) rb[b] = fma(br[b], v, rb[b]);
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < P; ++b) {
+        t1[b * P] = rb[b];                  // -> B_x^T
+        if (DIFF) t1[T1M + b * P] = rg[b];  // -> G_x^T
+      }
+    }
+    __syncthreads();
+
+    // ---- S1T: contract qx.  item (el, b, c) -> y_e[a][b][c] (aliases T2).
+    for (int it = tid; it < NE * P * P; it += NT) {
+      const int el = it / (P * P), r = it % (P * P);
+      const double* t1 = smem + el * EB + r;
+      double ye[P];
+#pragma unroll
+      for (int a = 0; a < P; ++a) ye[a] = 0.0;
+#pragma unroll
+      for (int qx = 0; qx < Q; ++qx) {
+        double br[P], gr[P];
+        ld_row<P, PR>(TBs + qx * PR, br);
+        const double vb = t1[qx * S1];
+        if (DIFF) {
+          ld_row<P, PR>(TGs + qx * PR, gr);
+          const double vg = t1[T1M + qx * S1];
+#pragma unroll
+          for (int a = 0; a < P; ++a) ye[a] = fma(gr[a], vg, fma(br[a], vb, ye[a]));
+        } else {
+#pragma unroll
+          for (int a = 0; a < P; ++a) ye[a] = fma(br[a], vb, ye[a]);
+        }
+      }
+      double* yo = smem + el * EB + T1SZ + r;
+#pragma unroll
+      for (int a = 0; a < P; ++a) yo[C::SA * a] = ye[a];
+    }
+    __syncthreads();
+
+    const long long brick = cur.bx + (long long)A.nbx * (cur.by + (long long)A.nby * ez);
+    brick_epilogue<C, NT, BX, BY, false, C::EB, C::T1SZ>(
+        A, smem, CY + ((ez + 1) & 1) * C::CARRY, CY + (ez & 1) * C::CARRY, brick, ex0, ey0, I0,
+        J0, (long long)p * ez, ez == cur.z0, ez + 1 == cur.z1);
+    cp_async_wait_all();
+    __syncthreads();
+    cur = nxt;
+  }
+}
+
+// SIMT kernel shapes: brick BX x BY elements, NT threads (>= the stage-3 item
+// count NE*Q^2 for Gauss Q where possible, so every stage is one round),
+// register cap, CTAs per SM.
+template <int P1>
+struct ShapeSD;
+//                                     BX BY  NT  MAXR  CTAs/SM
+template <> struct ShapeSD<2> { static constexpr int BX = 4, BY = 4, NT = 160, MAXR = 96, CPS = 4; };
+template <> struct ShapeSD<3> { static constexpr int BX = 4, BY = 2, NT = 128, MAXR = 128, CPS = 4; };
+template <> struct ShapeSD<4> { static constexpr int BX = 2, BY = 2, NT = 128, MAXR = 144, CPS = 3; };
+template <> struct ShapeSD<5> { static constexpr int BX = 2, BY = 2, NT = 160, MAXR = 128, CPS = 3; };
+template <> struct ShapeSD<6> { static constexpr int BX = 2, BY = 1, NT = 128, MAXR = 168, CPS = 3; };
+template <> struct ShapeSD<7> { static constexpr int BX = 2, BY = 1, NT = 128, MAXR = 168, CPS = 3; };
+template <> struct ShapeSD<8> { static constexpr int BX = 2, BY = 1, NT = 192, MAXR = 168, CPS = 2; };
+template <> struct ShapeSD<9> { static constexpr int BX = 1, BY = 1, NT = 128, MAXR = 232, CPS = 2; };
+
+// Tuning override (scripts/build_variant.py): -DHOFEM_SS_P1=6 -DHOFEM_SS_BX=2
+// -DHOFEM_SS_BY=2 -DHOFEM_SS_NT=224 -DHOFEM_SS_MAXR=144 -DHOFEM_SS_CPS=2.
+#ifdef HOFEM_SS_P1
+struct ShapeSOverride {
+  static constexpr int BX = HOFEM_SS_BX, BY = HOFEM_SS_BY, NT = HOFEM_SS_NT,
+                       MAXR = HOFEM_SS_MAXR, CPS = HOFEM_SS_CPS;
+};
+template <int P1>
+struct ShapeS : std::conditional_t<P1 == HOFEM_SS_P1, ShapeSOverride, ShapeSD<P1>> {};
+#else
+template <int P1>
+struct ShapeS : ShapeSD<P1> {};
+#endif
+
+// ---------------------------------------------------------------------------
 // Collocated diffusion kernel (BP5: GLL points = nodes, B1d = I, Q = P1).
 // u_x = G_x x, u_y = G_y x, u_z = G_z x; w = D u; y = G_x^T w_x + G_y^T w_y + G_z^T w_z.
 // ---------------------------------------------------------------------------
@@ -1396,16 +1790,20 @@ template <> struct ShapeE<8> { static constexpr int BX = 2, BY = 1, MINB = 3; };
 template <> struct ShapeE<9> { static constexpr int BX = 2, BY = 1, MINB = 2; };
 
 struct FusedLaunch {
-  int BX, BY, blat, ctas_per_sm;
+  int BX, BY, face_block, ctas_per_sm;  // face_block = FaceLayout<>::FB
 };
 
 // Defined per P1 in fused_p.cu: kind in {KIND_MASS, KIND_DIFF, KIND_COLLOC},
 // Q in {P1, P1+1} for MASS/DIFF and Q == P1 for COLLOC.  Returns false if the
 // combination is not instantiated.
+// variant: 0 = tensor-core kernel (fused_elem_mma), 1 = SIMT (fused_elem_simt);
+// ignored for COLLOC.
 template <int P1>
-bool fused_launch(int kind, int Q, const double* B, const double* G, const ColArgs& A, int grid,
-                  cudaStream_t s, cudaError_t* err);
+bool fused_launch(int kind, int variant, int Q, const double* B, const double* G,
+                  const ColArgs& A, int grid, cudaStream_t s, cudaError_t* err);
 template <int P1>
-FusedLaunch fused_shape(int kind);
+FusedLaunch fused_shape(int kind, int variant);
+template <int P1>
+int fused_default_variant();
 
 }  // namespace hofem

@@ -36,6 +36,36 @@ cudaError_t launch_general(const double* B, const double* G, const ColArgs& A, i
   return cudaPeekAtLastError();
 }
 
+template <int KIND, int P1, int Q>
+cudaError_t launch_simt(const double* B, const double* G, const ColArgs& A, int grid,
+                        cudaStream_t s) {
+  using S = ShapeS<P1>;
+  constexpr int SMEM = CfgS<KIND, P1, Q, S::BX, S::BY>::SMEM_BYTES;
+  Tab<P1, Q> T;
+  memcpy(T.B, B, sizeof(T.B));
+  memcpy(T.G, G, sizeof(T.G));
+  auto kern = fused_elem_simt<KIND, P1, Q, S::BX, S::BY, S::NT, S::MAXR>;
+  static bool attr_done = false;
+  cudaError_t e = set_smem(kern, SMEM, &attr_done);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, S::NT, SMEM, s>>>(T, A);
+  return cudaPeekAtLastError();
+}
+
+// Default fused variant per P1 (measured): 0 tensor-core, 1 SIMT.
+constexpr int kDefaultVariant = (HOFEM_P1 == 6) ? 0 : 1;
+
+int pick(int variant) { return variant < 0 ? kDefaultVariant : variant; }
+
+}  // namespace
+
+template <>
+int fused_default_variant<HOFEM_P1>() {
+  return kDefaultVariant;
+}
+
+namespace {
+
 template <int P1>
 cudaError_t launch_colloc(const double* G, const ColArgs& A, int grid, cudaStream_t s) {
   using S = Shape<P1>;
@@ -54,13 +84,26 @@ cudaError_t launch_colloc(const double* G, const ColArgs& A, int grid, cudaStrea
 }  // namespace
 
 template <>
-bool fused_launch<HOFEM_P1>(int kind, int Q, const double* B, const double* G, const ColArgs& A,
-                            int grid, cudaStream_t s, cudaError_t* err) {
+bool fused_launch<HOFEM_P1>(int kind, int variant, int Q, const double* B, const double* G,
+                            const ColArgs& A, int grid, cudaStream_t s, cudaError_t* err) {
   constexpr int P1 = HOFEM_P1;
   if (kind == KIND_COLLOC) {
     if (Q != P1) return false;
     *err = launch_colloc<P1>(G, A, grid, s);
     return true;
+  }
+  if (pick(variant) == 1) {
+    if (Q == P1 + 1) {
+      *err = kind == KIND_MASS ? launch_simt<KIND_MASS, P1, P1 + 1>(B, G, A, grid, s)
+                               : launch_simt<KIND_DIFF, P1, P1 + 1>(B, G, A, grid, s);
+      return true;
+    }
+    if (Q == P1) {
+      *err = kind == KIND_MASS ? launch_simt<KIND_MASS, P1, P1>(B, G, A, grid, s)
+                               : launch_simt<KIND_DIFF, P1, P1>(B, G, A, grid, s);
+      return true;
+    }
+    return false;
   }
   if (Q == P1 + 1) {
     *err = kind == KIND_MASS ? launch_general<KIND_MASS, P1, P1 + 1>(B, G, A, grid, s)
@@ -76,14 +119,18 @@ bool fused_launch<HOFEM_P1>(int kind, int Q, const double* B, const double* G, c
 }
 
 template <>
-FusedLaunch fused_shape<HOFEM_P1>(int kind) {
+FusedLaunch fused_shape<HOFEM_P1>(int kind, int variant) {
   constexpr int p = HOFEM_P1 - 1;
   if (kind == KIND_COLLOC) {
     using S = Shape<HOFEM_P1>;
-    return FusedLaunch{S::BX, S::BY, (p * S::BX + 1) * (p * S::BY + 1) * (p + 1), 1};
+    return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB, 1};
+  }
+  if (pick(variant) == 1) {
+    using S = ShapeS<HOFEM_P1>;
+    return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB, S::CPS};
   }
   using S = ShapeE<HOFEM_P1>;
-  return FusedLaunch{S::BX, S::BY, (p * S::BX + 1) * (p * S::BY + 1) * (p + 1), S::MINB};
+  return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB, S::MINB};
 }
 
 }  // namespace hofem

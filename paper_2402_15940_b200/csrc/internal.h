@@ -90,6 +90,7 @@ struct Op {
   // fused brick scratch (boundary partials)
   double* d_bbuf = nullptr;
   long long bbuf_len = 0;
+  int fused_variant = -1;   // -1: HOFEM_FUSED env / per-p default; 0 DMMA; 1 SIMT
   // CG scratch
   double *d_r = nullptr, *d_p = nullptr, *d_Ap = nullptr;
   double* d_cg = nullptr;   // device CG scalars / history
@@ -108,6 +109,7 @@ hofem_status build_rhs(Op* op, double* b, cudaStream_t s);
 // ---- operator apply paths
 hofem_status apply_unfused(Op* op, const double* x, double* y, cudaStream_t s);
 hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s);
+hofem_status fused_info(const Op* op, hofem_fused_info* out);
 bool fused_supported(const Op* op);
 
 // ---- comm (comm.cu): sum duplicated interface planes, fix BC there

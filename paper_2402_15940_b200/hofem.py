@@ -48,6 +48,12 @@ class ProfileStats(ctypes.Structure):
                 ("fixup_launches", ctypes.c_longlong), ("fixup_ms", ctypes.c_double)]
 
 
+class FusedInfo(ctypes.Structure):
+    _fields_ = [("variant", ctypes.c_int), ("bx", ctypes.c_int), ("by", ctypes.c_int),
+                ("zc", ctypes.c_int), ("nchunks", ctypes.c_int), ("grid", ctypes.c_int),
+                ("direct_points", ctypes.c_longlong), ("fixup_points", ctypes.c_longlong)]
+
+
 class CGStats(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int), ("converged", ctypes.c_int),
                 ("r0_norm", ctypes.c_double), ("final_rel_res", ctypes.c_double)]
@@ -75,6 +81,8 @@ SIGNATURES = {
     "hofem_op_destroy": (None, [_V]),
     "hofem_cg": (_I, [_V, _V, _V, _D, _I, _I, _I, _V, ctypes.POINTER(CGStats), _V]),
     "hofem_dot": (_I, [_V, _V, _V, ctypes.POINTER(_D), _V]),
+    "hofem_op_fused_info": (_I, [_V, ctypes.POINTER(FusedInfo)]),
+    "hofem_op_set_fused_variant": (_I, [_V, _I]),
     "hofem_profile_enable": (_I, [_I]),
     "hofem_profile_read": (_I, [ctypes.POINTER(ProfileStats)]),
     "hofem_launch_count": (_LL, []),
@@ -221,6 +229,17 @@ class Operator:
         y = torch.empty_like(x) if y is None else y
         _check(lib().hofem_op_apply(self.handle, _ptr(x), _ptr(y), _stream(stream)))
         return y
+
+    def fused_info(self) -> FusedInfo:
+        """How apply() runs: fused kernel variant (0 DMMA, 1 SIMT, 2 collocated,
+        -1 unfused), brick shape, chunking, direct vs fix-up lattice points."""
+        s = FusedInfo()
+        _check(lib().hofem_op_fused_info(self.handle, ctypes.byref(s)))
+        return s
+
+    def set_fused_variant(self, variant: int):
+        """-1 default, 0 DMMA tensor-core kernel, 1 SIMT kernel."""
+        _check(lib().hofem_op_set_fused_variant(self.handle, int(variant)))
 
     def apply_unfused(self, x: torch.Tensor, y: torch.Tensor | None = None, stream=None):
         y = torch.empty_like(x) if y is None else y

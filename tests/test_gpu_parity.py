@@ -100,13 +100,18 @@ def oracle_apply(om, kind, rule, x, bc, p, Q=None):
 @pytest.mark.parametrize("nx,ny,nz,p,bench", CASES)
 @pytest.mark.parametrize("bc", [0, 1])
 def test_fused_and_unfused_match_oracle(hf, nx, ny, nz, p, bench, bc):
+    """Both fused kernels (DMMA and SIMT; BP5 has its own collocated kernel)
+    and the unfused path against the oracle."""
     m, op, om, kind, rule = make(hf, nx, ny, nz, p, bench, bc=bc)
+    variants = (0, 1) if bench != "bp5" else (-1,)
     for seed in (1, 2):
         x = m.random(seed)
-        yf = host(op.apply(x))
-        yu = host(op.apply_unfused(x))
         ref = oracle_apply(om, kind, rule, host(x), bc, p)
-        assert rel(yf, ref) <= APPLY_TOL, rel(yf, ref)
+        for v in variants:
+            op.set_fused_variant(v)
+            yf = host(op.apply(x))
+            assert rel(yf, ref) <= APPLY_TOL, (v, rel(yf, ref))
+        yu = host(op.apply_unfused(x))
         assert rel(yu, ref) <= APPLY_TOL, rel(yu, ref)
 
 
@@ -117,17 +122,36 @@ def test_q_override(hf, p, q, bench):
     m, op, om, kind, rule = make(hf, 3, 2, 2, p, bench, q=q)
     x = m.random(5)
     ref = O.apply_dense(om, kind, rule, host(x), Q=q)
-    assert rel(host(op.apply(x)), ref) <= APPLY_TOL
+    for v in (0, 1):
+        op.set_fused_variant(v)
+        assert rel(host(op.apply(x)), ref) <= APPLY_TOL, v
     assert rel(host(op.apply_unfused(x)), ref) <= APPLY_TOL
 
 
-def test_fused_bitwise_deterministic(hf):
+@pytest.mark.parametrize("variant", [0, 1])
+def test_fused_bitwise_deterministic(hf, variant):
     m, op, _, _, _ = make(hf, 7, 5, 6, 5, "bp3", bc=1)
+    op.set_fused_variant(variant)
     x = m.random(3)
     y1 = host(op.apply(x))
     for _ in range(3):
         y2 = host(op.apply(x))
         assert np.array_equal(y1.view(np.uint64), y2.view(np.uint64))
+
+
+@pytest.mark.parametrize("bench,p,variant", [("bp3", 5, 0), ("bp3", 5, 1), ("bp1", 3, 1),
+                                             ("bp5", 4, -1), ("bp3", 2, 1)])
+def test_fused_info_partition(hf, bench, p, variant):
+    """hofem_op_fused_info: the direct / fix-up split covers every lattice point
+    once, and the reported variant is the one that ran."""
+    m, op, _, _, _ = make(hf, 7, 5, 6, p, bench, bc=1)
+    op.set_fused_variant(variant)
+    info = op.fused_info()
+    assert info.direct_points + info.fixup_points == m.n_local
+    assert info.variant == (2 if bench == "bp5" else variant)
+    assert info.grid >= 1 and info.zc * info.nchunks >= 6
+    with pytest.raises(hf.HofemError):
+        op.set_fused_variant(7)
 
 
 def test_affine_extents_and_volume(hf):
