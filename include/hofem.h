@@ -180,8 +180,9 @@ hofem_status hofem_profile_read(hofem_profile_stats* out);
  * fused kernel variant (0 tensor-core DMMA, 1 SIMT, 2 collocated SIMT; -1 the
  * operator has no fused kernel and apply uses the unfused path), brick shape,
  * work-unit z chunking, and the number of local lattice points the fused
- * kernel writes to y directly vs. through the fix-up kernel (interior brick
- * faces).  Host-only, no device work.  The variant follows the per-p default
+ * kernel completes itself (interior points, and single-face points by two
+ * order-independent reductions) vs. through the fix-up kernel (edge lines of
+ * the brick grid).  Host-only, no device work.  The variant follows the per-p default
  * unless the environment variable HOFEM_FUSED=mma|simt overrides it. */
 typedef struct {
   int variant;

@@ -34,8 +34,8 @@ struct FixArgs {
   long long K0, NzG;
   int Nx, Ny, Nzl;
   int p, PX, PY, PZU, LX, LY, nbx, nby, nzl, bc;
-  int FB, OY, OZ, FXS, FYS, FZS;  // FaceLayout<> of the launched kernel
-  int nplZ, nplY, nplX;           // interior brick-boundary planes per axis
+  int FB, OY, OZ, FYS, FZS;  // FaceLayout<> of the launched kernel
+  int nplZ, nplY, nplX;      // interior brick-boundary planes per axis
 };
 
 __device__ __forceinline__ bool on_plane(int I, int P, int N) {
@@ -73,25 +73,27 @@ __device__ __forceinline__ int axis_bricks_z(int K, int p, int nzl, bool split, 
   return 1;
 }
 
-// grid (ceil(max plane size / 256), max planes, 3): blockIdx.z = 0 z-unit
-// planes, 1 y planes, 2 x planes; a point on several planes is summed once, by
-// the first of them.  The threads of a warp walk the fastest face-block index
-// of the plane type, so the partial reads come in runs.
+// The edge lines of the brick grid: lattice points on two or three interior
+// brick-boundary planes (4 or 8 contributions).  grid (ceil(line length/256),
+// line count, 3): blockIdx.z = 0 x-y lines (along z), 1 x-z lines (along y,
+// skipping y planes), 2 y-z lines (along x, skipping x planes).  Each point sums
+// its partials in ascending brick order (deterministic).  Points on a single
+// plane were completed in the fused kernel by two-term reductions.
 __global__ void __launch_bounds__(256) fixup_kernel(FixArgs F) {
-  const int type = blockIdx.z, m = blockIdx.y + 1;
+  const int type = blockIdx.z, line = blockIdx.y;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   int I, J, K;
   if (type == 0) {
-    if (m > F.nplZ || r >= F.Nx * F.Ny) return;
-    K = m * F.PZU; I = r % F.Nx; J = r / F.Nx;
+    if (line >= F.nplX * F.nplY || r >= F.Nzl) return;
+    I = (line % F.nplX + 1) * F.PX; J = (line / F.nplX + 1) * F.PY; K = r;
   } else if (type == 1) {
-    if (m > F.nplY || r >= F.Nx * F.Nzl) return;
-    J = m * F.PY; I = r % F.Nx; K = r / F.Nx;
-    if (on_plane(K, F.PZU, F.Nzl)) return;
+    if (line >= F.nplX * F.nplZ || r >= F.Ny) return;
+    I = (line % F.nplX + 1) * F.PX; K = (line / F.nplX + 1) * F.PZU; J = r;
+    if (on_plane(J, F.PY, F.Ny)) return;
   } else {
-    if (m > F.nplX || r >= F.Ny * F.Nzl) return;
-    I = m * F.PX; J = r % F.Ny; K = r / F.Ny;
-    if (on_plane(J, F.PY, F.Ny) || on_plane(K, F.PZU, F.Nzl)) return;
+    if (line >= F.nplY * F.nplZ || r >= F.Nx) return;
+    J = (line % F.nplY + 1) * F.PY; K = (line / F.nplY + 1) * F.PZU; I = r;
+    if (on_plane(I, F.PX, F.Nx)) return;
   }
   const bool zs = on_plane(K, F.PZU, F.Nzl), ys = on_plane(J, F.PY, F.Ny),
              xs = on_plane(I, F.PX, F.Nx);
@@ -104,13 +106,8 @@ __global__ void __launch_bounds__(256) fixup_kernel(FixArgs F) {
     for (int b = 0; b < nbyl; ++b)
       for (int a = 0; a < nbxl; ++a) {
         const long long brick = bx[a] + (long long)F.nbx * (by[b] + (long long)F.nby * bz[c]);
-        int off;
-        if (zs)
-          off = F.OZ + (c == 0) * F.FZS + iy[b] * F.LX + ix[a];
-        else if (ys)
-          off = F.OY + (b == 0) * F.FYS + iz[c] * F.LX + ix[a];
-        else
-          off = (a == 0) * F.FXS + iz[c] * F.LY + iy[b];
+        const int off = zs ? F.OZ + (c == 0) * F.FZS + iy[b] * F.LX + ix[a]
+                           : F.OY + (b == 0) * F.FYS + iz[c] * F.LX + ix[a];
         s += F.bbuf[brick * F.FB + off];
       }
   const long long l = I + (long long)F.Nx * (J + (long long)F.Ny * K);
@@ -279,10 +276,11 @@ hofem_status fused_info(const Op* op, hofem_fused_info* out) {
   out->variant = P.variant;
   out->bx = P.L.BX; out->by = P.L.BY; out->zc = P.zc; out->nchunks = P.nchunks;
   out->grid = P.grid;
+  // points on >= 2 interior brick planes (edge lines) go through fixup_kernel
   const long long N = m->Nx * m->Ny * m->Nzl;
-  const long long inner = (m->Nx - (P.nbx - 1)) * (m->Ny - (P.nby - 1)) * (m->Nzl - (P.nchunks - 1));
-  out->fixup_points = N - inner;
-  out->direct_points = inner;
+  const long long ax = P.nbx - 1, ay = P.nby - 1, az = P.nchunks - 1;
+  out->fixup_points = ax * ay * m->Nzl + ax * az * m->Ny + ay * az * m->Nx - 2 * ax * ay * az;
+  out->direct_points = N - out->fixup_points;
   return HOFEM_OK;
 }
 
@@ -322,6 +320,10 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s) {
   cudaError_t err = cudaSuccess;
   bool ok = false;
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (nbx > 1 || nby > 1 || nchunks > 1) {
+    // single-face points are completed by two-term reductions onto zero
+    HOFEM_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * m->Nx * m->Ny * m->Nzl, s));
+  }
   if (g_prof.on) {
     ev = {prof_event(), prof_event()};
     cudaEventRecord(ev.first, s);
@@ -350,23 +352,21 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s) {
   F.p = p; F.PX = p * L.BX; F.PY = p * L.BY; F.PZU = p * zc;
   F.LX = F.PX + 1; F.LY = F.PY + 1;
   F.nbx = nbx; F.nby = nby; F.nzl = m->nzl; F.bc = op->bc;
-  F.FXS = (p + 1) * F.LY; F.OY = 2 * F.FXS;
-  F.FYS = (p + 1) * F.LX; F.OZ = F.OY + 2 * F.FYS;
+  F.FYS = (p + 1) * F.LX; F.OY = 0; F.OZ = 2 * F.FYS;
   F.FZS = F.LX * F.LY; F.FB = F.OZ + 2 * F.FZS;
   if (F.FB != L.face_block) {
     set_error("fused apply: face-block layout mismatch (%d vs %d)", F.FB, L.face_block);
     return HOFEM_ERR_ARG;
   }
   F.nplZ = nchunks - 1; F.nplY = nby - 1; F.nplX = nbx - 1;
-  const int npl = std::max(F.nplZ, std::max(F.nplY, F.nplX));
-  const long long psz = std::max((long long)F.Nx * F.Ny,
-                                 std::max((long long)F.Nx * F.Nzl, (long long)F.Ny * F.Nzl));
-  if (npl > 0) {
+  const int nlines = std::max(F.nplX * F.nplY, std::max(F.nplX * F.nplZ, F.nplY * F.nplZ));
+  const int llen = std::max(F.Nzl, std::max(F.Ny, F.Nx));
+  if (nlines > 0) {
     if (g_prof.on) {
       ev = {prof_event(), prof_event()};
       cudaEventRecord(ev.first, s);
     }
-    const dim3 fg((unsigned)((psz + 255) / 256), (unsigned)npl, 3);
+    const dim3 fg((unsigned)((llen + 255) / 256), (unsigned)nlines, 3);
     fixup_kernel<<<fg, 256, 0, s>>>(F);
     HOFEM_LAUNCHED();
     if (g_prof.on) {

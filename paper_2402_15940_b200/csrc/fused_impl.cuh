@@ -44,6 +44,15 @@
 #ifndef HOFEM_DBG_SKIP
 #define HOFEM_DBG_SKIP 0  // timing ablation only (wrong results): 1 epilogue, 2 D loads, 4 DMMAs
 #endif
+#ifndef HOFEM_SIMT_MERGE
+#define HOFEM_SIMT_MERGE 0  // SIMT kernel: brick k's epilogue in the barrier interval of S1(k+1)
+#endif
+#ifndef HOFEM_SIMT_DSMEM
+#define HOFEM_SIMT_DSMEM -1  // SIMT: D staged in smem (1), from L2 in registers (0), per p (-1)
+#endif
+#ifndef HOFEM_SIMT_DPF
+#define HOFEM_SIMT_DPF 0  // SIMT stage 3: qz-steps of D loads in flight (0: per p, measured)
+#endif
 #ifndef HOFEM_APF
 #define HOFEM_APF 0  // 1: stage 3 loads the next tile's A fragments before this tile's MMAs
 #endif
@@ -188,33 +197,39 @@ __device__ __forceinline__ void issue_lattice(const ColArgs& A, double* L, long 
 // k == 0 adds the carried top plane of the previous brick first; k == p goes to
 // the carry unless the brick ends the unit.
 // ---------------------------------------------------------------------------
-// Brick face block in the partial buffer (one per brick): the values of the
-// lattice points the brick shares with a neighbour brick, stored by face so the
-// fix-up kernel reads them in runs: x faces [xs][k][j], y faces [ys][k][i],
-// z-unit faces [zs][j][i].  A point on several shared faces is stored once, by
-// the priority z > y > x (the fix-up applies the same rule).
+// Interior brick faces.  A lattice point on exactly ONE shared face (x, y or
+// z-unit plane) has exactly two contributions, a (this brick) and b (the
+// neighbour); y is zeroed before the kernel and both bricks add with an FP64
+// reduction: 0 + a + b == 0 + b + a bitwise (IEEE addition is commutative and
+// 0 + a is exact), so the result is deterministic in any order.  Points on two
+// or three shared faces (the edge lines of the brick grid) have 4 or 8
+// contributions; they go to the brick's face block in the partial buffer and
+// fixup_kernel (fused.cu) sums them in ascending brick order.  Face block: y
+// faces [ys][k][i], z-unit faces [zs][j][i]; a point on a z-unit face is stored
+// in the z face, otherwise in the y face (x-only points never get here).
 template <int p, int LX, int LY>
 struct FaceLayout {
   static constexpr int P1 = p + 1;
-  static constexpr int FXS = P1 * LY;           // x face stride (xs)
-  static constexpr int OY = 2 * FXS;            // y faces
+  static constexpr int OY = 0;                  // y faces
   static constexpr int FYS = P1 * LX;
   static constexpr int OZ = OY + 2 * FYS;       // z faces
   static constexpr int FZS = LX * LY;
   static constexpr int FB = OZ + 2 * FZS;       // doubles per brick
-  __device__ __forceinline__ static int xf(int xs, int k, int j) { return xs * FXS + k * LY + j; }
   __device__ __forceinline__ static int yf(int ys, int k) { return OY + ys * FYS + k * LX; }
   __device__ __forceinline__ static int zf(int zs, int j) { return OZ + zs * FZS + j * LX; }
 };
+
+__device__ __forceinline__ void red_add(double* p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
 
 struct EpiRow {
   const double* cin;
   double* cout;
   double* bb;   // shared-face row (z-unit or y face) in the brick's face block
-  double* bxf;  // x-face slot (xs = 0) of this row; xs = 1 at + FXS
   long long gl;
   int base0, base1;  // y-element offsets of the lower / primary contributions
-  bool vy0, vy1, to_carry, from_carry, row_sh, row_ess;
+  bool vy0, vy1, to_carry, from_carry, row_sh, row_multi, row_ess;
 };
 
 template <class C, int BX, bool NATURAL, int ESTRIDE, int SX>
@@ -253,21 +268,28 @@ __device__ __forceinline__ void epi_segment(const ColArgs& A, const double* RA, 
       if (p * SX + ii < nv) R.cout[p * SX + ii] = v[ii];
     return;
   }
-  if (R.row_sh) {
+  const int ie = (int)(iess >= 0 && iess < LX ? iess : -1);
+  if (R.row_sh) {  // row on a y face or a z-unit face
 #pragma unroll
-    for (int ii = 0; ii < NPT; ++ii)
-      if (p * SX + ii < nv) R.bb[p * SX + ii] = v[ii];
+    for (int ii = 0; ii < NPT; ++ii) {
+      const int i = p * SX + ii;
+      if (i >= nv) continue;
+      const bool lo = (SX == 0 && ii == 0), hi = (SX == BX - 1 && ii == p);
+      if (R.row_multi || (lo && xlo_sh) || (hi && xhi_sh))
+        R.bb[i] = v[ii];  // edge line: partial buffer
+      else if (R.row_ess || (lo && xlo_ess) || i == ie)
+        A.y[R.gl + i] = A.x[R.gl + i];
+      else
+        red_add(A.y + R.gl + i, v[ii]);
+    }
     return;
   }
-  const int ie = (int)(iess >= 0 && iess < LX ? iess : -1);
   if (!R.row_ess && nv == LX && ie < 0 && !xlo_ess) {
 #pragma unroll
     for (int ii = 0; ii < NPT; ++ii) {
       const bool lo = (SX == 0 && ii == 0), hi = (SX == BX - 1 && ii == p);
-      if (lo && xlo_sh)
-        R.bxf[0] = v[ii];
-      else if (hi && xhi_sh)
-        R.bxf[FaceLayout<p, LX, C::LY>::FXS] = v[ii];
+      if ((lo && xlo_sh) || (hi && xhi_sh))
+        red_add(A.y + R.gl + p * SX + ii, v[ii]);
       else
         A.y[R.gl + p * SX + ii] = v[ii];
     }
@@ -278,14 +300,13 @@ __device__ __forceinline__ void epi_segment(const ColArgs& A, const double* RA, 
     const int i = p * SX + ii;
     if (i >= nv) continue;
     const bool lo = (SX == 0 && ii == 0), hi = (SX == BX - 1 && ii == p);
-    if (lo && xlo_sh) {
-      R.bxf[0] = v[ii];
-    } else if (hi && xhi_sh) {
-      R.bxf[FaceLayout<p, LX, C::LY>::FXS] = v[ii];
-    } else {
-      const bool ess = R.row_ess || (lo && xlo_ess) || (i == ie);
-      A.y[R.gl + i] = ess ? A.x[R.gl + i] : v[ii];
-    }
+    const bool ess = R.row_ess || (lo && xlo_ess) || (i == ie);
+    if (ess)
+      A.y[R.gl + i] = A.x[R.gl + i];
+    else if ((lo && xlo_sh) || (hi && xhi_sh))
+      red_add(A.y + R.gl + i, v[ii]);
+    else
+      A.y[R.gl + i] = v[ii];
   }
 }
 
@@ -320,7 +341,7 @@ __device__ __forceinline__ void brick_epilogue(const ColArgs& A, const double* R
 #pragma unroll
   for (int q = 0; q < BX; ++q) exok[q] = ex0 + q < A.nx;
   for (int it = threadIdx.x; it < LY * P1 * BX; it += NT) {
-    const int sx = it % BX, r = it / BX, j = r % LY, k = r / LY;
+    const int sx = it / (LY * P1), r = it % (LY * P1), j = r % LY, k = r / LY;
     const long long J = J0 + j, K = K0l + k, Kg = K + A.K0;
     if (J >= A.Ny) continue;
     const int qj = j / p, rj = j - qj * p;
@@ -331,20 +352,16 @@ __device__ __forceinline__ void brick_epilogue(const ColArgs& A, const double* R
     R.base1 = BX * qj * ESTRIDE + (NATURAL ? P1 * (rj + P1 * k) : k + P1 * rj);
     R.to_carry = (k == p) && !last;
     R.from_carry = (k == 0) && !first;
-    R.row_sh = (j == 0 && J > 0) || (j == LY - 1 && J < A.Ny - 1) ||
-               (k == 0 && first && K > 0) || (k == p && last && K < A.Nzl - 1);
+    const bool ysh = (j == 0 && J > 0) || (j == LY - 1 && J < A.Ny - 1);
+    const bool zsh = (k == 0 && first && K > 0) || (k == p && last && K < A.Nzl - 1);
+    R.row_sh = ysh || zsh;
+    R.row_multi = ysh && zsh;
     R.row_ess = A.bc && (J == 0 || J == A.Ny - 1 || Kg == 0 || Kg == A.NzG - 1);
     R.gl = I0 + A.Nx * (J + A.Ny * K);
     {
       using FL = FaceLayout<p, LX, LY>;
       double* fb = A.bbuf + brick * FL::FB;
-      if (k == 0 && first && K > 0)
-        R.bb = fb + FL::zf(0, j);
-      else if (k == p && last && K < A.Nzl - 1)
-        R.bb = fb + FL::zf(1, j);
-      else
-        R.bb = fb + FL::yf(j == 0 ? 0 : 1, k);
-      R.bxf = fb + FL::xf(0, k, j);
+      R.bb = zsh ? fb + FL::zf(k == 0 ? 0 : 1, j) : fb + FL::yf(j == 0 ? 0 : 1, k);
     }
     R.cin = carry_in + LX * j;
     R.cout = carry_out + LX * j;
@@ -1300,6 +1317,14 @@ __device__ __forceinline__ double ld_nc_v(const double* ptr) {
   return v;
 }
 
+template <bool SMEM>
+__device__ __forceinline__ double ld_d(const double* ptr) {
+  if constexpr (SMEM)
+    return *ptr;
+  else
+    return ld_nc_v(ptr);
+}
+
 template <int KIND, int P1, int Q, int BX, int BY>
 struct CfgS {
   static constexpr int p = P1 - 1, P = P1, NE = BX * BY;
@@ -1322,7 +1347,13 @@ struct CfgS {
   static constexpr int PR = P + (P & 1);  // table row stride
   static constexpr int TOFF0 = NE * EB + 2 * LAT + 2 * CARRY;
   static constexpr int TOFF = TOFF0 + (TOFF0 & 1);  // tables 16-byte aligned
-  static constexpr int SMEM_DOUBLES = TOFF + 2 * Q * PR;
+  // D staged in shared memory (one buffer, bulk-copied one brick ahead) or
+  // loaded from L2 into registers inside stage 3.
+  static constexpr bool DSM =
+      HOFEM_SIMT_DSMEM >= 0 ? HOFEM_SIMT_DSMEM != 0 : (P1 == 6 || P1 == 9);  // measured
+  static constexpr int QOFF = TOFF + 2 * Q * PR;  // even => 16-byte aligned
+  static constexpr int QSLOT = ((NC * Q * Q * Q + 2) + 1) / 2 * 2;
+  static constexpr int SMEM_DOUBLES = QOFF + (DSM ? NE * QSLOT : 0);
   static constexpr int SMEM_BYTES = SMEM_DOUBLES * 8;
   static constexpr int NQ1 = Q;
   __device__ static constexpr int lat(int i, int j, int k) { return k + LZ * j + LXS * i; }
@@ -1341,6 +1372,17 @@ __device__ __forceinline__ void ld_row(const double* row, double (&r)[P]) {
   if (P & 1) r[P - 1] = row[P - 1];
 }
 
+template <class C, int NT, int BX, int BY>
+__device__ __forceinline__ void simt_epilogue(const ColArgs& A, double* smem, double* CY,
+                                              const Brick& b) {
+  constexpr int p = C::p;
+  const int ex0 = b.bx * BX, ey0 = b.by * BY, ez = b.ez;
+  const long long brick = b.bx + (long long)A.nbx * (b.by + (long long)A.nby * ez);
+  brick_epilogue<C, NT, BX, BY, false, C::EB, C::T1SZ>(
+      A, smem, CY + ((ez + 1) & 1) * C::CARRY, CY + (ez & 1) * C::CARRY, brick, ex0, ey0,
+      (long long)p * ex0, (long long)p * ey0, (long long)p * ez, ez == b.z0, ez + 1 == b.z1);
+}
+
 template <int KIND, int P1, int Q, int BX, int BY, int NT, int MAXR>
 __global__ void __maxnreg__(MAXR)
     fused_elem_simt(const __grid_constant__ Tab<P1, Q> T, const __grid_constant__ ColArgs A) {
@@ -1355,6 +1397,12 @@ __global__ void __maxnreg__(MAXR)
   double* CY = LB + 2 * C::LAT;
   double* TBs = smem + C::TOFF;  // B[q][c], row stride PR (16-byte aligned)
   double* TGs = TBs + Q * PR;
+  double* QS = smem + C::QOFF;  // staged D of the current brick (DSM)
+  __shared__ __align__(8) unsigned long long qbar;
+  if (C::DSM && threadIdx.x == 0) {
+    mbar_init(&qbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
 
   for (int i = threadIdx.x; i < C::SMEM_DOUBLES; i += NT) smem[i] = 0.0;
   __syncthreads();
@@ -1366,23 +1414,32 @@ __global__ void __maxnreg__(MAXR)
 
   Brick cur = unit_first(A, blockIdx.x);
   if (cur.u >= A.nunits) return;
-  prefetch_qdata_l2<C, BX, BY>(A, cur);
+  if (C::DSM)
+    issue_qdata<C, BX, BY>(A, cur, QS, &qbar);
+  else
+    prefetch_qdata_l2<C, BX, BY>(A, cur);
   issue_lattice<C, NT, BX>(A, LB, (long long)p * cur.bx * BX, (long long)p * cur.by * BY,
                            (long long)p * cur.ez);
   cp_async_wait_all();
   __syncthreads();
+  unsigned qphase = 0;
 
+  // The epilogue of brick k shares a barrier interval with S1 of brick k+1
+  // (disjoint shared memory: y_e/carry vs lattice/T1), one barrier less per
+  // brick and two independent instruction streams for the scheduler.
+  Brick prev;
+  prev.u = A.nunits;  // none yet
   for (int kb = 0; cur.u < A.nunits; ++kb) {
     const int tid = vtid();
     const Brick nxt = brick_next(A, cur);
     const int ex0 = cur.bx * BX, ey0 = cur.by * BY, ez = cur.ez;
-    const long long I0 = (long long)p * ex0, J0 = (long long)p * ey0;
     const double* L = LB + (kb & 1) * C::LAT;
     if (nxt.u < A.nunits) {
       issue_lattice<C, NT, BX>(A, LB + ((kb + 1) & 1) * C::LAT, (long long)p * nxt.bx * BX,
                                (long long)p * nxt.by * BY, (long long)p * nxt.ez);
       prefetch_qdata_l2<C, BX, BY>(A, nxt);
     }
+    if (HOFEM_SIMT_MERGE && prev.u < A.nunits) simt_epilogue<C, NT, BX, BY>(A, smem, CY, prev);
 
     // ---- S1: contract x.  item (el, b, c), c fastest.
     for (int it = tid; it < NE * P * P; it += NT) {
@@ -1448,15 +1505,29 @@ __global__ void __maxnreg__(MAXR)
     // ---- S3: z contraction, pointwise D, z back-contraction; item (el, pt).
     //      Streamed over qz: u(qz) -> w(qz) = D u -> s += B/G(qz) w.  D(qz+1)
     //      is loaded (volatile, in program order) while qz computes.
+    if (C::DSM) {
+      mbar_wait(&qbar, qphase);
+      qphase ^= 1u;
+    }
     for (int it = tid; it < NE * Q2; it += NT) {
       const int el = it / Q2, pt = it % Q2;
       const int ex = ex0 + el % BX, ey = ey0 + el / BX;
       if (ex >= A.nx || ey >= A.ny) continue;
-      const double* qde = A.qd +
-                          (ex + (long long)A.nx * (ey + (long long)A.ny * ez)) *
+      const double* qde =
+          C::DSM ? QS + el * C::QSLOT + stage_off<C>(A, ex, ey, ez) + pt
+                 : A.qd + (ex + (long long)A.nx * (ey + (long long)A.ny * ez)) *
                               (long long)(C::NC * Q3) + pt;
       double* t2 = smem + el * EB + T1SZ + pt * SP;
       if (DIFF) {
+        // D ring: qz .. qz+DPF-1 in flight (volatile loads keep program order)
+        constexpr int DPF0 =
+            C::DSM ? 1 : (HOFEM_SIMT_DPF > 0 ? HOFEM_SIMT_DPF : (P1 >= 7 ? 2 : 1));
+        constexpr int DPF = DPF0 < Q ? DPF0 : Q;
+        double dq[DPF][6];
+#pragma unroll
+        for (int k = 0; k < DPF; ++k)
+#pragma unroll
+          for (int m = 0; m < 6; ++m) dq[k][m] = ld_d<C::DSM>(qde + m * Q3 + k * Q2);
         double g0[P], g1[P], g2[P], s0[P], s1[P], s2[P];
 #pragma unroll
         for (int c = 0; c < P; ++c) {
@@ -1465,17 +1536,14 @@ __global__ void __maxnreg__(MAXR)
           g2[c] = t2[2 * T2M + c];
           s0[c] = s1[c] = s2[c] = 0.0;
         }
-        double dn[6];
-#pragma unroll
-        for (int m = 0; m < 6; ++m) dn[m] = ld_nc_v(qde + m * Q3);
 #pragma unroll
         for (int qz = 0; qz < Q; ++qz) {
           double dc[6];
 #pragma unroll
-          for (int m = 0; m < 6; ++m) dc[m] = dn[m];
-          if (qz + 1 < Q) {
+          for (int m = 0; m < 6; ++m) dc[m] = dq[qz % DPF][m];
+          if (qz + DPF < Q) {
 #pragma unroll
-            for (int m = 0; m < 6; ++m) dn[m] = ld_nc_v(qde + m * Q3 + (qz + 1) * Q2);
+            for (int m = 0; m < 6; ++m) dq[qz % DPF][m] = ld_d<C::DSM>(qde + m * Q3 + (qz + DPF) * Q2);
           }
           double br[P], gr[P];
           ld_row<P, PR>(TBs + qz * PR, br);
@@ -1507,11 +1575,11 @@ __global__ void __maxnreg__(MAXR)
         double g[P], s[P];
 #pragma unroll
         for (int c = 0; c < P; ++c) { g[c] = t2[c]; s[c] = 0.0; }
-        double dn = ld_nc_v(qde);
+        double dn = ld_d<C::DSM>(qde);
 #pragma unroll
         for (int qz = 0; qz < Q; ++qz) {
           const double dc = dn;
-          if (qz + 1 < Q) dn = ld_nc_v(qde + (qz + 1) * Q2);
+          if (qz + 1 < Q) dn = ld_d<C::DSM>(qde + (qz + 1) * Q2);
           double br[P];
           ld_row<P, PR>(TBs + qz * PR, br);
           double u = 0.0;
@@ -1526,6 +1594,7 @@ __global__ void __maxnreg__(MAXR)
       }
     }
     __syncthreads();
+    if (C::DSM) issue_qdata<C, BX, BY>(A, nxt, QS, &qbar);  // D(k) consumed
 
     // ---- S2T: contract qy.  item (el, qx, c), c fastest.
     for (int it = tid; it < NE * Q * P; it += NT) {
@@ -1589,16 +1658,17 @@ __global__ void __maxnreg__(MAXR)
 #pragma unroll
       for (int a = 0; a < P; ++a) yo[C::SA * a] = ye[a];
     }
-    __syncthreads();
 
-    const long long brick = cur.bx + (long long)A.nbx * (cur.by + (long long)A.nby * ez);
-    brick_epilogue<C, NT, BX, BY, false, C::EB, C::T1SZ>(
-        A, smem, CY + ((ez + 1) & 1) * C::CARRY, CY + (ez & 1) * C::CARRY, brick, ex0, ey0, I0,
-        J0, (long long)p * ez, ez == cur.z0, ez + 1 == cur.z1);
+    if (!HOFEM_SIMT_MERGE) {
+      __syncthreads();
+      simt_epilogue<C, NT, BX, BY>(A, smem, CY, cur);
+    }
     cp_async_wait_all();
     __syncthreads();
+    prev = cur;
     cur = nxt;
   }
+  if (HOFEM_SIMT_MERGE && prev.u < A.nunits) simt_epilogue<C, NT, BX, BY>(A, smem, CY, prev);
 }
 
 // SIMT kernel shapes: brick BX x BY elements, NT threads (>= the stage-3 item

@@ -37,19 +37,53 @@ cudaError_t launch_general(const double* B, const double* G, const ColArgs& A, i
 }
 
 template <int KIND, int P1, int Q>
+auto simt_kernel() {
+  using S = ShapeS<P1>;
+  return fused_elem_simt<KIND, P1, Q, S::BX, S::BY, S::NT, S::MAXR>;
+}
+template <int KIND, int P1, int Q>
+constexpr int simt_smem() {
+  using S = ShapeS<P1>;
+  return CfgS<KIND, P1, Q, S::BX, S::BY>::SMEM_BYTES;
+}
+
+template <int KIND, int P1, int Q>
 cudaError_t launch_simt(const double* B, const double* G, const ColArgs& A, int grid,
                         cudaStream_t s) {
   using S = ShapeS<P1>;
-  constexpr int SMEM = CfgS<KIND, P1, Q, S::BX, S::BY>::SMEM_BYTES;
+  constexpr int SMEM = simt_smem<KIND, P1, Q>();
   Tab<P1, Q> T;
   memcpy(T.B, B, sizeof(T.B));
   memcpy(T.G, G, sizeof(T.G));
-  auto kern = fused_elem_simt<KIND, P1, Q, S::BX, S::BY, S::NT, S::MAXR>;
+  auto kern = simt_kernel<KIND, P1, Q>();
   static bool attr_done = false;
   cudaError_t e = set_smem(kern, SMEM, &attr_done);
   if (e != cudaSuccess) return e;
   kern<<<grid, S::NT, SMEM, s>>>(T, A);
   return cudaPeekAtLastError();
+}
+
+// Resident CTAs per SM of a SIMT instantiation (occupancy API; registers and
+// shared memory both count), so the persistent grid never oversubscribes.
+template <int KIND, int P1, int Q>
+int simt_ctas_per_sm() {
+  static int n = 0;
+  if (n == 0) {
+    auto kern = simt_kernel<KIND, P1, Q>();
+    constexpr int SMEM = simt_smem<KIND, P1, Q>();
+    int v = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) ==
+            cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, ShapeS<P1>::NT, SMEM) ==
+            cudaSuccess &&
+        v > 0)
+      n = v;
+    else {
+      cudaGetLastError();
+      n = ShapeS<P1>::CPS;
+    }
+  }
+  return n;
 }
 
 // Default fused variant per P1 (measured): 0 tensor-core, 1 SIMT.
@@ -127,7 +161,9 @@ FusedLaunch fused_shape<HOFEM_P1>(int kind, int variant) {
   }
   if (pick(variant) == 1) {
     using S = ShapeS<HOFEM_P1>;
-    return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB, S::CPS};
+    const int cps = kind == KIND_MASS ? simt_ctas_per_sm<KIND_MASS, HOFEM_P1, HOFEM_P1 + 1>()
+                                      : simt_ctas_per_sm<KIND_DIFF, HOFEM_P1, HOFEM_P1 + 1>();
+    return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB, cps};
   }
   using S = ShapeE<HOFEM_P1>;
   return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB, S::MINB};
