@@ -245,7 +245,8 @@ def run_ours(args):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(f"bp3_p{p}_n{n}")
+            ent = json.load(open(tpath)).get(f"bp3_p{p}_n{n}")
+            traffic = ent["dram_bytes"] if ent else None
         except Exception:
             traffic = None
 

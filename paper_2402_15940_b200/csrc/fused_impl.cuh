@@ -1845,19 +1845,27 @@ constexpr int smem_bytes() {
 // Tensor-core kernel shapes (mass / diffusion): brick = one warp per element,
 // CTAs per SM.
 template <int P1>
-struct ShapeE;
-//                                    BX BY MINB
-template <> struct ShapeE<2> { static constexpr int BX = 4, BY = 2, MINB = 2; };
-template <> struct ShapeE<3> { static constexpr int BX = 4, BY = 2, MINB = 2; };
-template <> struct ShapeE<4> { static constexpr int BX = 4, BY = 2, MINB = 2; };
-template <> struct ShapeE<5> { static constexpr int BX = 2, BY = 2, MINB = 3; };
-#ifndef HOFEM_MINB6
-#define HOFEM_MINB6 3
+struct ShapeED;
+//                                     BX BY MINB
+template <> struct ShapeED<2> { static constexpr int BX = 4, BY = 2, MINB = 2; };
+template <> struct ShapeED<3> { static constexpr int BX = 4, BY = 2, MINB = 2; };
+template <> struct ShapeED<4> { static constexpr int BX = 4, BY = 2, MINB = 2; };
+template <> struct ShapeED<5> { static constexpr int BX = 2, BY = 2, MINB = 3; };
+template <> struct ShapeED<6> { static constexpr int BX = 2, BY = 2, MINB = 3; };
+template <> struct ShapeED<7> { static constexpr int BX = 2, BY = 2, MINB = 2; };
+template <> struct ShapeED<8> { static constexpr int BX = 2, BY = 1, MINB = 3; };
+template <> struct ShapeED<9> { static constexpr int BX = 2, BY = 1, MINB = 2; };
+// Tuning override: -DHOFEM_SE_P1=6 -DHOFEM_SE_BX=1 -DHOFEM_SE_BY=1 -DHOFEM_SE_MINB=12.
+#ifdef HOFEM_SE_P1
+struct ShapeEOverride {
+  static constexpr int BX = HOFEM_SE_BX, BY = HOFEM_SE_BY, MINB = HOFEM_SE_MINB;
+};
+template <int P1>
+struct ShapeE : std::conditional_t<P1 == HOFEM_SE_P1, ShapeEOverride, ShapeED<P1>> {};
+#else
+template <int P1>
+struct ShapeE : ShapeED<P1> {};
 #endif
-template <> struct ShapeE<6> { static constexpr int BX = 2, BY = 2, MINB = HOFEM_MINB6; };
-template <> struct ShapeE<7> { static constexpr int BX = 2, BY = 2, MINB = 2; };
-template <> struct ShapeE<8> { static constexpr int BX = 2, BY = 1, MINB = 3; };
-template <> struct ShapeE<9> { static constexpr int BX = 2, BY = 1, MINB = 2; };
 
 struct FusedLaunch {
   int BX, BY, face_block, ctas_per_sm;  // face_block = FaceLayout<>::FB

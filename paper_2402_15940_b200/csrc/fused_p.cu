@@ -21,6 +21,12 @@ cudaError_t set_smem(K kern, int bytes, bool* done) {
 }
 
 template <int KIND, int P1, int Q>
+auto mma_kernel() {
+  using S = ShapeE<P1>;
+  return fused_elem_mma<KIND, P1, Q, S::BX, S::BY, S::MINB>;
+}
+
+template <int KIND, int P1, int Q>
 cudaError_t launch_general(const double* B, const double* G, const ColArgs& A, int grid,
                            cudaStream_t s) {
   using S = ShapeE<P1>;
@@ -28,7 +34,7 @@ cudaError_t launch_general(const double* B, const double* G, const ColArgs& A, i
   Tab<P1, Q> T;
   memcpy(T.B, B, sizeof(T.B));
   memcpy(T.G, G, sizeof(T.G));
-  auto kern = fused_elem_mma<KIND, P1, Q, S::BX, S::BY, S::MINB>;
+  auto kern = mma_kernel<KIND, P1, Q>();
   static bool attr_done = false;
   cudaError_t e = set_smem(kern, SMEM, &attr_done);
   if (e != cudaSuccess) return e;
@@ -61,6 +67,28 @@ cudaError_t launch_simt(const double* B, const double* G, const ColArgs& A, int 
   if (e != cudaSuccess) return e;
   kern<<<grid, S::NT, SMEM, s>>>(T, A);
   return cudaPeekAtLastError();
+}
+
+// Resident CTAs per SM of a kernel (occupancy API; registers and shared memory
+// both count), so the persistent grid never oversubscribes.
+template <class K>
+int occupancy(K kern, int threads, int smem, int fallback) {
+  int v = 0;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ==
+          cudaSuccess &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, threads, smem) == cudaSuccess &&
+      v > 0)
+    return v;
+  cudaGetLastError();
+  return fallback;
+}
+
+template <int KIND, int P1, int Q>
+int mma_ctas_per_sm() {
+  using S = ShapeE<P1>;
+  static const int n = occupancy(mma_kernel<KIND, P1, Q>(), 32 * S::BX * S::BY,
+                                 smem_bytes_elem<KIND, P1, Q, S::BX, S::BY>(), S::MINB);
+  return n;
 }
 
 // Resident CTAs per SM of a SIMT instantiation (occupancy API; registers and
@@ -166,7 +194,9 @@ FusedLaunch fused_shape<HOFEM_P1>(int kind, int variant) {
     return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB, cps};
   }
   using S = ShapeE<HOFEM_P1>;
-  return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB, S::MINB};
+  const int cps = kind == KIND_MASS ? mma_ctas_per_sm<KIND_MASS, HOFEM_P1, HOFEM_P1 + 1>()
+                                    : mma_ctas_per_sm<KIND_DIFF, HOFEM_P1, HOFEM_P1 + 1>();
+  return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB, cps};
 }
 
 }  // namespace hofem
