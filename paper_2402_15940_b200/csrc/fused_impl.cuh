@@ -50,6 +50,9 @@
 #ifndef HOFEM_SIMT_DSMEM
 #define HOFEM_SIMT_DSMEM -1  // SIMT: D staged in smem (1), from L2 in registers (0), per p (-1)
 #endif
+#ifndef HOFEM_SIMT_CB
+#define HOFEM_SIMT_CB -1  // SIMT tables: 1 constant bank (uniform loads), 0 shared memory, -1 per p
+#endif
 #ifndef HOFEM_SIMT_DPF
 #define HOFEM_SIMT_DPF 0  // SIMT stage 3: qz-steps of D loads in flight (0: per p, measured)
 #endif
@@ -1383,6 +1386,28 @@ __device__ __forceinline__ void simt_epilogue(const ColArgs& A, double* smem, do
       (long long)p * ex0, (long long)p * ey0, (long long)p * ez, ez == b.z0, ez + 1 == b.z1);
 }
 
+// Table row from the kernel-parameter constant bank.  `zo` is a loop-variant
+// uniform zero: it keeps the compiler from hoisting the 2QP table values out of
+// the persistent loop into (spilled) registers, while the loads stay uniform
+// (LDCU into uniform registers, DFMA reads them as operands).
+template <int P>
+__device__ __forceinline__ void cb_row(const double* row, int zo, double (&r)[P]) {
+#pragma unroll
+  for (int c = 0; c < P; ++c) r[c] = row[c + zo];
+}
+// measured: constant-bank tables win at p = 4, 6, 7; shared-memory rows elsewhere
+template <int P1>
+constexpr bool simt_cb() {
+  return HOFEM_SIMT_CB >= 0 ? HOFEM_SIMT_CB != 0 : (P1 == 5 || P1 == 7 || P1 == 8);
+}
+#define TROW(M, q, r)                                 \
+  do {                                                \
+    if constexpr (simt_cb<P1>())                      \
+      cb_row<P>(T.M + (q) * P, zo, r);                \
+    else                                              \
+      ld_row<P, PR>(T##M##s + (q) * PR, r);           \
+  } while (0)
+
 template <int KIND, int P1, int Q, int BX, int BY, int NT, int MAXR>
 __global__ void __maxnreg__(MAXR)
     fused_elem_simt(const __grid_constant__ Tab<P1, Q> T, const __grid_constant__ ColArgs A) {
@@ -1431,6 +1456,8 @@ __global__ void __maxnreg__(MAXR)
   prev.u = A.nunits;  // none yet
   for (int kb = 0; cur.u < A.nunits; ++kb) {
     const int tid = vtid();
+    const int zo = cur.ez >> 30;  // == 0, loop-variant (see cb_row)
+    (void)zo;
     const Brick nxt = brick_next(A, cur);
     const int ex0 = cur.bx * BX, ey0 = cur.by * BY, ez = cur.ez;
     const double* L = LB + (kb & 1) * C::LAT;
@@ -1452,8 +1479,8 @@ __global__ void __maxnreg__(MAXR)
 #pragma unroll
       for (int qx = 0; qx < Q; ++qx) {
         double br[P], gr[P];
-        ld_row<P, PR>(TBs + qx * PR, br);
-        if (DIFF) ld_row<P, PR>(TGs + qx * PR, gr);
+        TROW(B, qx, br);
+        if (DIFF) TROW(G, qx, gr);
         double sb = 0.0, sg = 0.0;
 #pragma unroll
         for (int a = 0; a < P; ++a) {
@@ -1480,8 +1507,8 @@ __global__ void __maxnreg__(MAXR)
 #pragma unroll
       for (int qy = 0; qy < Q; ++qy) {
         double br[P], gr[P];
-        ld_row<P, PR>(TBs + qy * PR, br);
-        if (DIFF) ld_row<P, PR>(TGs + qy * PR, gr);
+        TROW(B, qy, br);
+        if (DIFF) TROW(G, qy, gr);
         double bb = 0.0, gb = 0.0, bg = 0.0;
 #pragma unroll
         for (int b = 0; b < P; ++b) {
@@ -1546,8 +1573,8 @@ __global__ void __maxnreg__(MAXR)
             for (int m = 0; m < 6; ++m) dq[qz % DPF][m] = ld_d<C::DSM>(qde + m * Q3 + (qz + DPF) * Q2);
           }
           double br[P], gr[P];
-          ld_row<P, PR>(TBs + qz * PR, br);
-          ld_row<P, PR>(TGs + qz * PR, gr);
+          TROW(B, qz, br);
+          TROW(G, qz, gr);
           double u0 = 0.0, u1 = 0.0, u2 = 0.0;
 #pragma unroll
           for (int c = 0; c < P; ++c) {
@@ -1581,7 +1608,7 @@ __global__ void __maxnreg__(MAXR)
           const double dc = dn;
           if (qz + 1 < Q) dn = ld_d<C::DSM>(qde + (qz + 1) * Q2);
           double br[P];
-          ld_row<P, PR>(TBs + qz * PR, br);
+          TROW(B, qz, br);
           double u = 0.0;
 #pragma unroll
           for (int c = 0; c < P; ++c) u = fma(br[c], g[c], u);
@@ -1607,9 +1634,9 @@ __global__ void __maxnreg__(MAXR)
 #pragma unroll
       for (int qy = 0; qy < Q; ++qy) {
         double br[P], gr[P];
-        ld_row<P, PR>(TBs + qy * PR, br);
+        TROW(B, qy, br);
         if (DIFF) {
-          ld_row<P, PR>(TGs + qy * PR, gr);
+          TROW(G, qy, gr);
           const double v0 = t2[qy * Q * SP], v1 = t2[T2M + qy * Q * SP],
                        v2 = t2[2 * T2M + qy * Q * SP];
 #pragma unroll
@@ -1642,10 +1669,10 @@ __global__ void __maxnreg__(MAXR)
 #pragma unroll
       for (int qx = 0; qx < Q; ++qx) {
         double br[P], gr[P];
-        ld_row<P, PR>(TBs + qx * PR, br);
+        TROW(B, qx, br);
         const double vb = t1[qx * S1];
         if (DIFF) {
-          ld_row<P, PR>(TGs + qx * PR, gr);
+          TROW(G, qx, gr);
           const double vg = t1[T1M + qx * S1];
 #pragma unroll
           for (int a = 0; a < P; ++a) ye[a] = fma(gr[a], vg, fma(br[a], vb, ye[a]));
@@ -1682,7 +1709,7 @@ template <> struct ShapeSD<3> { static constexpr int BX = 4, BY = 2, NT = 128, M
 template <> struct ShapeSD<4> { static constexpr int BX = 2, BY = 2, NT = 128, MAXR = 144, CPS = 3; };
 template <> struct ShapeSD<5> { static constexpr int BX = 2, BY = 2, NT = 160, MAXR = 128, CPS = 3; };
 template <> struct ShapeSD<6> { static constexpr int BX = 2, BY = 1, NT = 128, MAXR = 168, CPS = 3; };
-template <> struct ShapeSD<7> { static constexpr int BX = 2, BY = 1, NT = 128, MAXR = 168, CPS = 3; };
+template <> struct ShapeSD<7> { static constexpr int BX = 1, BY = 1, NT = 64, MAXR = 168, CPS = 6; };
 template <> struct ShapeSD<8> { static constexpr int BX = 2, BY = 1, NT = 192, MAXR = 168, CPS = 2; };
 template <> struct ShapeSD<9> { static constexpr int BX = 1, BY = 1, NT = 128, MAXR = 232, CPS = 2; };
 
