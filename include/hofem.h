@@ -177,8 +177,9 @@ hofem_status hofem_profile_enable(int enable);
 hofem_status hofem_profile_read(hofem_profile_stats* out);
 
 /* How hofem_op_apply runs this operator (for the bench's roofline figure):
- * fused kernel variant (0 tensor-core DMMA, 1 SIMT, 2 collocated SIMT; -1 the
- * operator has no fused kernel and apply uses the unfused path), brick shape,
+ * fused kernel variant (0 tensor-core DMMA, 1 SIMT thread-per-line incl. the
+ * collocated BP5 form, 2 the older collocated column kernel; -1 the operator
+ * has no fused kernel and apply uses the unfused path), brick shape,
  * work-unit z chunking, and the number of local lattice points the fused
  * kernel completes itself (interior points, and single-face points by two
  * order-independent reductions) vs. through the fix-up kernel (edge lines of
@@ -193,9 +194,10 @@ typedef struct {
 } hofem_fused_info;
 hofem_status hofem_op_fused_info(const void* op, hofem_fused_info* out);
 /* Select the fused kernel of hofem_op_apply for this operator: -1 default
- * (HOFEM_FUSED env or the measured per-p choice), 0 DMMA, 1 SIMT.  Both
- * compute the same operator (parity-tested); only the schedule differs.
- * Ignored for the collocated BP5 kernel.  HOFEM_ERR_ARG if out of range. */
+ * (HOFEM_FUSED env or the measured per-p choice), 0 DMMA, 1 SIMT.  For a
+ * collocated (BP5) operator: 1 (default) the SIMT kernel with B = I, 0 the
+ * older column kernel.  All compute the same operator (parity-tested); only
+ * the schedule differs.  HOFEM_ERR_ARG if out of range. */
 hofem_status hofem_op_set_fused_variant(void* op, int variant);
 
 /* Number of kernel launches the library issued since the last reset (for the

@@ -250,7 +250,12 @@ Plan make_plan(const Op* op) {
   Plan P;
   P.kind = fused_kind(op);
   const int v = op->fused_variant >= 0 ? op->fused_variant : fused_variant();
-  P.variant = P.kind == KIND_COLLOC ? 2 : (v < 0 ? default_variant(m->P1) : v);
+  // variant: 0 DMMA, 1 SIMT (mass / diffusion / collocated), 2 the older
+  // collocated column kernel (requested as 0 for a collocated operator)
+  if (P.kind == KIND_COLLOC)
+    P.variant = (v < 0 || v == 1) ? 1 : 2;
+  else
+    P.variant = v < 0 ? default_variant(m->P1) : v;
   P.L = shape_for(m->P1, P.kind, P.variant == 2 ? 0 : P.variant);
   P.nbx = (m->nx + P.L.BX - 1) / P.L.BX;
   P.nby = (m->ny + P.L.BY - 1) / P.L.BY;

@@ -1414,7 +1414,10 @@ __global__ void __maxnreg__(MAXR)
   using C = CfgS<KIND, P1, Q, BX, BY>;
   constexpr int P = P1, p = P1 - 1, NE = C::NE;
   constexpr int Q2 = Q * Q, Q3 = Q * Q * Q;
-  constexpr bool DIFF = KIND == KIND_DIFF;
+  // COLLOC (BP5): GLL points = nodes, so B = I; every B contraction is the
+  // identity and is skipped (diffusion structure otherwise).
+  constexpr bool COL = KIND == KIND_COLLOC;
+  constexpr bool DIFF = KIND == KIND_DIFF || COL;
   constexpr int EB = C::EB, S1 = C::S1, T1M = C::T1M, T1SZ = C::T1SZ, SP = C::SP,
                 T2M = C::T2M, PR = C::PR;
   extern __shared__ __align__(16) double smem[];
@@ -1479,15 +1482,15 @@ __global__ void __maxnreg__(MAXR)
 #pragma unroll
       for (int qx = 0; qx < Q; ++qx) {
         double br[P], gr[P];
-        TROW(B, qx, br);
+        if (!COL) TROW(B, qx, br);
         if (DIFF) TROW(G, qx, gr);
         double sb = 0.0, sg = 0.0;
 #pragma unroll
         for (int a = 0; a < P; ++a) {
-          sb = fma(br[a], xa[a], sb);
+          if (!COL) sb = fma(br[a], xa[a], sb);
           if (DIFF) sg = fma(gr[a], xa[a], sg);
         }
-        t1[qx * S1] = sb;
+        t1[qx * S1] = COL ? xa[qx] : sb;  // B_x x (= x when collocated)
         if (DIFF) t1[T1M + qx * S1] = sg;
       }
     }
@@ -1507,16 +1510,20 @@ __global__ void __maxnreg__(MAXR)
 #pragma unroll
       for (int qy = 0; qy < Q; ++qy) {
         double br[P], gr[P];
-        TROW(B, qy, br);
+        if (!COL) TROW(B, qy, br);
         if (DIFF) TROW(G, qy, gr);
         double bb = 0.0, gb = 0.0, bg = 0.0;
 #pragma unroll
         for (int b = 0; b < P; ++b) {
-          bb = fma(br[b], vb[b], bb);
+          if (!COL) bb = fma(br[b], vb[b], bb);
           if (DIFF) {
-            gb = fma(br[b], vg[b], gb);
+            if (!COL) gb = fma(br[b], vg[b], gb);
             bg = fma(gr[b], vb[b], bg);
           }
+        }
+        if (COL) {
+          bb = vb[qy];
+          gb = vg[qy];
         }
         if (DIFF) {
           t2[qy * Q * SP] = gb;            // G_x B_y  (-> u_x)
@@ -1573,23 +1580,35 @@ __global__ void __maxnreg__(MAXR)
             for (int m = 0; m < 6; ++m) dq[qz % DPF][m] = ld_d<C::DSM>(qde + m * Q3 + (qz + DPF) * Q2);
           }
           double br[P], gr[P];
-          TROW(B, qz, br);
+          if (!COL) TROW(B, qz, br);
           TROW(G, qz, gr);
           double u0 = 0.0, u1 = 0.0, u2 = 0.0;
 #pragma unroll
           for (int c = 0; c < P; ++c) {
-            u0 = fma(br[c], g0[c], u0);
-            u1 = fma(br[c], g1[c], u1);
+            if (!COL) {
+              u0 = fma(br[c], g0[c], u0);
+              u1 = fma(br[c], g1[c], u1);
+            }
             u2 = fma(gr[c], g2[c], u2);
+          }
+          if (COL) {
+            u0 = g0[qz];
+            u1 = g1[qz];
           }
           const double w0 = dc[0] * u0 + dc[1] * u1 + dc[2] * u2;
           const double w1 = dc[1] * u0 + dc[3] * u1 + dc[4] * u2;
           const double w2 = dc[2] * u0 + dc[4] * u1 + dc[5] * u2;
 #pragma unroll
           for (int c = 0; c < P; ++c) {
-            s0[c] = fma(br[c], w0, s0[c]);
-            s1[c] = fma(br[c], w1, s1[c]);
+            if (!COL) {
+              s0[c] = fma(br[c], w0, s0[c]);
+              s1[c] = fma(br[c], w1, s1[c]);
+            }
             s2[c] = fma(gr[c], w2, s2[c]);
+          }
+          if (COL) {
+            s0[qz] = w0;
+            s1[qz] = w1;
           }
         }
 #pragma unroll
@@ -1634,8 +1653,16 @@ __global__ void __maxnreg__(MAXR)
 #pragma unroll
       for (int qy = 0; qy < Q; ++qy) {
         double br[P], gr[P];
-        TROW(B, qy, br);
-        if (DIFF) {
+        if (!COL) TROW(B, qy, br);
+        if (COL) {
+          TROW(G, qy, gr);
+          const double v0 = t2[qy * Q * SP], v1 = t2[T2M + qy * Q * SP],
+                       v2 = t2[2 * T2M + qy * Q * SP];
+          rg[qy] = v0;
+#pragma unroll
+          for (int b = 0; b < P; ++b) rb[b] = fma(gr[b], v1, rb[b]);
+          rb[qy] += v2;
+        } else if (DIFF) {
           TROW(G, qy, gr);
           const double v0 = t2[qy * Q * SP], v1 = t2[T2M + qy * Q * SP],
                        v2 = t2[2 * T2M + qy * Q * SP];
@@ -1669,9 +1696,15 @@ __global__ void __maxnreg__(MAXR)
 #pragma unroll
       for (int qx = 0; qx < Q; ++qx) {
         double br[P], gr[P];
-        TROW(B, qx, br);
+        if (!COL) TROW(B, qx, br);
         const double vb = t1[qx * S1];
-        if (DIFF) {
+        if (COL) {
+          TROW(G, qx, gr);
+          const double vg = t1[T1M + qx * S1];
+#pragma unroll
+          for (int a = 0; a < P; ++a) ye[a] = fma(gr[a], vg, ye[a]);
+          ye[qx] += vb;
+        } else if (DIFF) {
           TROW(G, qx, gr);
           const double vg = t1[T1M + qx * S1];
 #pragma unroll

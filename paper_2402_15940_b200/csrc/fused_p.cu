@@ -151,7 +151,8 @@ bool fused_launch<HOFEM_P1>(int kind, int variant, int Q, const double* B, const
   constexpr int P1 = HOFEM_P1;
   if (kind == KIND_COLLOC) {
     if (Q != P1) return false;
-    *err = launch_colloc<P1>(G, A, grid, s);
+    *err = variant == 1 ? launch_simt<KIND_COLLOC, P1, P1>(B, G, A, grid, s)
+                        : launch_colloc<P1>(G, A, grid, s);
     return true;
   }
   if (pick(variant) == 1) {
@@ -184,6 +185,11 @@ template <>
 FusedLaunch fused_shape<HOFEM_P1>(int kind, int variant) {
   constexpr int p = HOFEM_P1 - 1;
   if (kind == KIND_COLLOC) {
+    if (variant == 1) {
+      using S = ShapeS<HOFEM_P1>;
+      return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB,
+                         simt_ctas_per_sm<KIND_COLLOC, HOFEM_P1, HOFEM_P1>()};
+    }
     using S = Shape<HOFEM_P1>;
     return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB, 1};
   }

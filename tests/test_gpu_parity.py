@@ -103,7 +103,7 @@ def test_fused_and_unfused_match_oracle(hf, nx, ny, nz, p, bench, bc):
     """Both fused kernels (DMMA and SIMT; BP5 has its own collocated kernel)
     and the unfused path against the oracle."""
     m, op, om, kind, rule = make(hf, nx, ny, nz, p, bench, bc=bc)
-    variants = (0, 1) if bench != "bp5" else (-1,)
+    variants = (0, 1)  # bp5: 0 = older column kernel, 1 = SIMT with B = I
     for seed in (1, 2):
         x = m.random(seed)
         ref = oracle_apply(om, kind, rule, host(x), bc, p)
@@ -140,7 +140,7 @@ def test_fused_bitwise_deterministic(hf, variant):
 
 
 @pytest.mark.parametrize("bench,p,variant", [("bp3", 5, 0), ("bp3", 5, 1), ("bp1", 3, 1),
-                                             ("bp5", 4, -1), ("bp3", 2, 1)])
+                                             ("bp5", 4, -1), ("bp5", 4, 0), ("bp3", 2, 1)])
 def test_fused_info_partition(hf, bench, p, variant):
     """hofem_op_fused_info: the direct / fix-up split covers every lattice point
     once, and the reported variant is the one that ran."""
@@ -148,7 +148,8 @@ def test_fused_info_partition(hf, bench, p, variant):
     op.set_fused_variant(variant)
     info = op.fused_info()
     assert info.direct_points + info.fixup_points == m.n_local
-    assert info.variant == (2 if bench == "bp5" else variant)
+    expect = {-1: 1, 0: 2, 1: 1}[variant] if bench == "bp5" else variant
+    assert info.variant == expect
     assert info.grid >= 1 and info.zc * info.nchunks >= 6
     with pytest.raises(hf.HofemError):
         op.set_fused_variant(7)
