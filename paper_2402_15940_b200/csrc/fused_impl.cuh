@@ -1760,6 +1760,27 @@ template <int P1>
 struct ShapeS : ShapeSD<P1> {};
 #endif
 
+// Collocated (BP5) SIMT shapes: every stage has NE*P1^2 items.
+template <int P1>
+struct ShapeSCD : ShapeS<P1> {};
+//                                      BX BY  NT  MAXR  CTAs/SM  (measured, BP5)
+template <> struct ShapeSCD<6> { static constexpr int BX = 2, BY = 2, NT = 160, MAXR = 128, CPS = 3; };
+template <> struct ShapeSCD<8> { static constexpr int BX = 2, BY = 1, NT = 128, MAXR = 168, CPS = 3; };
+// Tuning override: -DHOFEM_SC_P1=6 -DHOFEM_SC_BX=.. (same fields as HOFEM_SS_*).
+#ifdef HOFEM_SC_P1
+struct ShapeSCOverride {
+  static constexpr int BX = HOFEM_SC_BX, BY = HOFEM_SC_BY, NT = HOFEM_SC_NT,
+                       MAXR = HOFEM_SC_MAXR, CPS = HOFEM_SC_CPS;
+};
+template <int P1>
+struct ShapeSC : std::conditional_t<P1 == HOFEM_SC_P1, ShapeSCOverride, ShapeSCD<P1>> {};
+#else
+template <int P1>
+struct ShapeSC : ShapeSCD<P1> {};
+#endif
+template <int KIND, int P1>
+using ShapeSK = std::conditional_t<KIND == KIND_COLLOC, ShapeSC<P1>, ShapeS<P1>>;
+
 // ---------------------------------------------------------------------------
 // Collocated diffusion kernel (BP5: GLL points = nodes, B1d = I, Q = P1).
 // u_x = G_x x, u_y = G_y x, u_z = G_z x; w = D u; y = G_x^T w_x + G_y^T w_y + G_z^T w_z.

@@ -44,19 +44,19 @@ cudaError_t launch_general(const double* B, const double* G, const ColArgs& A, i
 
 template <int KIND, int P1, int Q>
 auto simt_kernel() {
-  using S = ShapeS<P1>;
+  using S = ShapeSK<KIND, P1>;
   return fused_elem_simt<KIND, P1, Q, S::BX, S::BY, S::NT, S::MAXR>;
 }
 template <int KIND, int P1, int Q>
 constexpr int simt_smem() {
-  using S = ShapeS<P1>;
+  using S = ShapeSK<KIND, P1>;
   return CfgS<KIND, P1, Q, S::BX, S::BY>::SMEM_BYTES;
 }
 
 template <int KIND, int P1, int Q>
 cudaError_t launch_simt(const double* B, const double* G, const ColArgs& A, int grid,
                         cudaStream_t s) {
-  using S = ShapeS<P1>;
+  using S = ShapeSK<KIND, P1>;
   constexpr int SMEM = simt_smem<KIND, P1, Q>();
   Tab<P1, Q> T;
   memcpy(T.B, B, sizeof(T.B));
@@ -102,13 +102,13 @@ int simt_ctas_per_sm() {
     int v = 0;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) ==
             cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, ShapeS<P1>::NT, SMEM) ==
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, ShapeSK<KIND, P1>::NT, SMEM) ==
             cudaSuccess &&
         v > 0)
       n = v;
     else {
       cudaGetLastError();
-      n = ShapeS<P1>::CPS;
+      n = ShapeSK<KIND, P1>::CPS;
     }
   }
   return n;
@@ -186,7 +186,7 @@ FusedLaunch fused_shape<HOFEM_P1>(int kind, int variant) {
   constexpr int p = HOFEM_P1 - 1;
   if (kind == KIND_COLLOC) {
     if (variant == 1) {
-      using S = ShapeS<HOFEM_P1>;
+      using S = ShapeSC<HOFEM_P1>;
       return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB,
                          simt_ctas_per_sm<KIND_COLLOC, HOFEM_P1, HOFEM_P1>()};
     }
