@@ -119,6 +119,14 @@ hofem_status hofem_op_apply(void* op, const double* x, double* y, void* stream);
  * table) -> element kernel -> deterministic scatter through precomputed
  * transposed offsets (R^T, ascending (e, i) order). */
 hofem_status hofem_op_apply_unfused(void* op, const double* x, double* y, void* stream);
+/* SYNC.  y = A x (as hofem_op_apply) and *dot_host = x.y over owned dofs,
+ * allreduced -- the x^T A x energy that CG needs as p^T A p.  On the fused
+ * path the product is accumulated inside the operator kernels from the values
+ * they write (each element contribution times x at its dof, Dirichlet rows
+ * once), in a fixed order: deterministic, and equal to hofem_dot(x, y) up to
+ * rounding (the order of the sum differs). */
+hofem_status hofem_op_apply_dot(void* op, const double* x, double* y, double* dot_host,
+                                void* stream);
 
 /* Device pointer to the stored qdata (owned by op) and its length E*n_c*Q^3. */
 hofem_status hofem_op_qdata(const void* op, const double** qdata, long long* count);

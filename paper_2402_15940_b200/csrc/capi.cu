@@ -224,6 +224,27 @@ hofem_status hofem_op_apply(void* op_, const double* x, double* y, void* stream)
   return apply_any(op, x, y, S(stream));
 }
 
+hofem_status hofem_op_apply_dot(void* op_, const double* x, double* y, double* dot_host,
+                                void* stream) {
+  Op* op = static_cast<Op*>(op_);
+  if (!op || !x || !y || x == y || !dot_host) {
+    set_error("hofem_op_apply_dot: NULL or aliased x/y");
+    return HOFEM_ERR_ARG;
+  }
+  Mesh* m = op->mesh;
+  if (fused_supported(op)) {
+    HOFEM_TRY(apply_fused(op, x, y, S(stream), m->d_scalars));
+  } else {
+    HOFEM_TRY(apply_unfused(op, x, y, S(stream)));
+    HOFEM_TRY(dot_local(m, x, y, m->d_scalars, S(stream)));
+  }
+  HOFEM_TRY(allreduce_sum(m, m->d_scalars, 1, S(stream)));
+  HOFEM_CUDA(cudaMemcpyAsync(dot_host, m->d_scalars, sizeof(double), cudaMemcpyDeviceToHost,
+                             S(stream)));
+  HOFEM_CUDA(cudaStreamSynchronize(S(stream)));
+  return HOFEM_OK;
+}
+
 hofem_status hofem_op_apply_unfused(void* op_, const double* x, double* y, void* stream) {
   Op* op = static_cast<Op*>(op_);
   if (!op || !x || !y || x == y) { set_error("hofem_op_apply_unfused: NULL or aliased x/y"); return HOFEM_ERR_ARG; }

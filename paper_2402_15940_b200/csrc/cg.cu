@@ -203,6 +203,14 @@ __global__ void __launch_bounds__(kDotThreads) pupdate_kernel(
 
 }  // namespace
 
+hofem_status dot_local(Mesh* m, const double* a, const double* b, double* d_out,
+                       cudaStream_t s) {
+  dot_kernel<<<kDotBlocks, kDotThreads, 0, s>>>(m->n_owned, a, b, m->d_partials, m->d_counter,
+                                                d_out);
+  HOFEM_LAUNCHED();
+  return HOFEM_OK;
+}
+
 hofem_status dot_device(Mesh* m, const double* a, const double* b, double* d_out,
                         cudaStream_t s) {
   dot_kernel<<<kDotBlocks, kDotThreads, 0, s>>>(m->n_owned, a, b, m->d_partials, m->d_counter,
@@ -256,10 +264,14 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
   bool done = (rr0 == 0.0 && !fixed_iters);
   if (done) status = HOFEM_OK;
   while (!done && k < max_iter) {
-    HOFEM_TRY(apply_any(op, op->d_p, op->d_Ap, s));
-    dot_kernel<<<kDotBlocks, kDotThreads, 0, s>>>(no, op->d_p, op->d_Ap, m->d_partials,
-                                                  m->d_counter, pAp);
-    HOFEM_LAUNCHED();
+    // Ap = A p and pAp = p.Ap: fused into the operator kernels when possible
+    // (computed from the contributions they write), else a separate dot
+    if (fused_supported(op)) {
+      HOFEM_TRY(apply_fused(op, op->d_p, op->d_Ap, s, pAp));
+    } else {
+      HOFEM_TRY(apply_unfused(op, op->d_p, op->d_Ap, s));
+      HOFEM_TRY(dot_local(m, op->d_p, op->d_Ap, pAp, s));
+    }
     HOFEM_TRY(allreduce_sum(m, pAp, 1, s));
     update_kernel<<<kDotBlocks, kDotThreads, 0, s>>>(n, no, op->d_Ap, op->d_r, rr + k, pAp,
                                                      m->d_partials, m->d_counter, rr + k + 1,

@@ -36,6 +36,8 @@ struct FixArgs {
   int p, PX, PY, PZU, LX, LY, nbx, nby, nzl, bc;
   int FB, OY, OZ, FYS, FZS;  // FaceLayout<> of the launched kernel
   int nplZ, nplY, nplX;      // interior brick-boundary planes per axis
+  double* dotp;              // non-null: one x.y partial per block (flat block index)
+  int kown;                  // local planes K < kown are owned
 };
 
 __device__ __forceinline__ bool on_plane(int I, int P, int N) {
@@ -79,21 +81,32 @@ __device__ __forceinline__ int axis_bricks_z(int K, int p, int nzl, bool split, 
 // skipping y planes), 2 y-z lines (along x, skipping x planes).  Each point sums
 // its partials in ascending brick order (deterministic).  Points on a single
 // plane were completed in the fused kernel by two-term reductions.
+__device__ __forceinline__ double fixup_point(const FixArgs& F);
 __global__ void __launch_bounds__(256) fixup_kernel(FixArgs F) {
+  __shared__ double red[256];
+  double d = fixup_point(F);
+  if (F.dotp) {
+    const unsigned b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    block_sum_store(d, F.dotp + b, red);
+  }
+}
+
+// One edge-line point (see fixup_kernel); returns its x.y term (0 if none).
+__device__ __forceinline__ double fixup_point(const FixArgs& F) {
   const int type = blockIdx.z, line = blockIdx.y;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   int I, J, K;
   if (type == 0) {
-    if (line >= F.nplX * F.nplY || r >= F.Nzl) return;
+    if (line >= F.nplX * F.nplY || r >= F.Nzl) return 0.0;
     I = (line % F.nplX + 1) * F.PX; J = (line / F.nplX + 1) * F.PY; K = r;
   } else if (type == 1) {
-    if (line >= F.nplX * F.nplZ || r >= F.Ny) return;
+    if (line >= F.nplX * F.nplZ || r >= F.Ny) return 0.0;
     I = (line % F.nplX + 1) * F.PX; K = (line / F.nplX + 1) * F.PZU; J = r;
-    if (on_plane(J, F.PY, F.Ny)) return;
+    if (on_plane(J, F.PY, F.Ny)) return 0.0;
   } else {
-    if (line >= F.nplY * F.nplZ || r >= F.Nx) return;
+    if (line >= F.nplY * F.nplZ || r >= F.Nx) return 0.0;
     J = (line % F.nplY + 1) * F.PY; K = (line / F.nplY + 1) * F.PZU; I = r;
-    if (on_plane(I, F.PX, F.Nx)) return;
+    if (on_plane(I, F.PX, F.Nx)) return 0.0;
   }
   const bool zs = on_plane(K, F.PZU, F.Nzl), ys = on_plane(J, F.PY, F.Ny),
              xs = on_plane(I, F.PX, F.Nx);
@@ -111,12 +124,25 @@ __global__ void __launch_bounds__(256) fixup_kernel(FixArgs F) {
         s += F.bbuf[brick * F.FB + off];
       }
   const long long l = I + (long long)F.Nx * (J + (long long)F.Ny * K);
+  const double xl = F.x[l];
   if (F.bc) {
     const long long Kg = K + F.K0;
-    if (I == 0 || I == F.Nx - 1 || J == 0 || J == F.Ny - 1 || Kg == 0 || Kg == F.NzG - 1)
-      s = F.x[l];
+    if (I == 0 || I == F.Nx - 1 || J == 0 || J == F.Ny - 1 || Kg == 0 || Kg == F.NzG - 1) {
+      F.y[l] = xl;
+      return K < F.kown ? xl * xl : 0.0;  // Dirichlet value: counted by the owner
+    }
   }
   F.y[l] = s;
+  return xl * s;
+}
+
+// Sums the x.y partials of the fused kernel and the fix-up in index order.
+__global__ void __launch_bounds__(256) dot_partials_kernel(const double* part, long long n,
+                                                           double* out) {
+  __shared__ double red[256];
+  double v = 0.0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) v += part[i];
+  block_sum_store(v, out, red);
 }
 
 // Tuning knob HOFEM_FUSED = "mma" | "simt" overrides the per-p default kernel.
@@ -289,7 +315,8 @@ hofem_status fused_info(const Op* op, hofem_fused_info* out) {
   return HOFEM_OK;
 }
 
-hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s) {
+hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
+                         double* dot_out) {
   Mesh* m = op->mesh;
   const int P1 = m->P1, p = m->p;
   const Plan PL = make_plan(op);
@@ -322,6 +349,25 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s) {
     return e ? atoi(e) : 1;
   }();
   A.l2pf = l2pf;
+  // fused x.y: per-CTA partials of the brick kernel, then one per fix-up block
+  const bool fdot = dot_out != nullptr && PL.variant != 2;
+  const int gfx = (int)((std::max((int)m->Nzl, std::max((int)m->Ny, (int)m->Nx)) + 255) / 256);
+  const int nlines0 = std::max((nbx - 1) * (nby - 1),
+                               std::max((nbx - 1) * (nchunks - 1), (nby - 1) * (nchunks - 1)));
+  const long long nfixb = nlines0 > 0 ? (long long)gfx * nlines0 * 3 : 0;
+  if (fdot && op->dotp_len < grid + nfixb) {
+    if (op->d_dotp) cudaFree(op->d_dotp);
+    op->d_dotp = nullptr;
+    op->dotp_len = 0;
+    if (cudaMalloc(&op->d_dotp, sizeof(double) * (grid + nfixb)) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("fused apply: out of device memory for the dot partials");
+      return HOFEM_ERR_OOM;
+    }
+    op->dotp_len = grid + nfixb;
+  }
+  A.dotp = fdot ? op->d_dotp : nullptr;
+  A.kown = m->n_owned / (m->Nx * m->Ny);
   cudaError_t err = cudaSuccess;
   bool ok = false;
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
@@ -364,6 +410,8 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s) {
     return HOFEM_ERR_ARG;
   }
   F.nplZ = nchunks - 1; F.nplY = nby - 1; F.nplX = nbx - 1;
+  F.dotp = fdot ? op->d_dotp + grid : nullptr;
+  F.kown = (int)A.kown;
   const int nlines = std::max(F.nplX * F.nplY, std::max(F.nplX * F.nplZ, F.nplY * F.nplZ));
   const int llen = std::max(F.Nzl, std::max(F.Ny, F.Nx));
   if (nlines > 0) {
@@ -371,7 +419,8 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s) {
       ev = {prof_event(), prof_event()};
       cudaEventRecord(ev.first, s);
     }
-    const dim3 fg((unsigned)((llen + 255) / 256), (unsigned)nlines, 3);
+    const dim3 fg((unsigned)gfx, (unsigned)nlines, 3);
+    (void)llen;
     fixup_kernel<<<fg, 256, 0, s>>>(F);
     HOFEM_LAUNCHED();
     if (g_prof.on) {
@@ -379,7 +428,13 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s) {
       g_prof.fixup.push_back(ev);
     }
   }
-  return exchange_planes(op, x, y, s);
+  if (fdot) {
+    dot_partials_kernel<<<1, 256, 0, s>>>(op->d_dotp, grid + (nlines > 0 ? nfixb : 0), dot_out);
+    HOFEM_LAUNCHED();
+  }
+  HOFEM_TRY(exchange_planes(op, x, y, s));
+  if (dot_out && !fdot) return dot_local(m, x, y, dot_out, s);  // owned dofs, after exchange
+  return HOFEM_OK;
 }
 
 }  // namespace hofem

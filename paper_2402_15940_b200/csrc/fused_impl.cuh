@@ -44,9 +44,6 @@
 #ifndef HOFEM_DBG_SKIP
 #define HOFEM_DBG_SKIP 0  // timing ablation only (wrong results): 1 epilogue, 2 D loads, 4 DMMAs
 #endif
-#ifndef HOFEM_SIMT_MERGE
-#define HOFEM_SIMT_MERGE 0  // SIMT kernel: brick k's epilogue in the barrier interval of S1(k+1)
-#endif
 #ifndef HOFEM_SIMT_DSMEM
 #define HOFEM_SIMT_DSMEM -1  // SIMT: D staged in smem (1), from L2 in registers (0), per p (-1)
 #endif
@@ -61,6 +58,25 @@
 #endif
 
 namespace hofem {
+
+// CTA barrier.  __syncthreads() is `bar.sync` (.aligned): every thread of a
+// warp must reach it convergently.  compute-sanitizer synccheck caught warps
+// arriving diverged (lanes of one warp still in a different compile-time
+// epilogue segment), which gave layout-dependent wrong answers; the item
+// loops (FOR_ITEMS) and the warp-uniform epilogue segments below remove the
+// divergence, and the explicit __syncwarp documents the requirement.
+__device__ __forceinline__ void cta_sync() {
+  __syncwarp();
+  __syncthreads();
+}
+
+// Item loop with a warp-uniform trip count: for it = first, first+NT, ... < N.
+// The per-lane bound is an `if` inside each round, so every lane leaves the
+// loop together and divergence stays inside structured if-bodies (a per-lane
+// trip count left warps diverged at the next CTA barrier, see cta_sync).
+#define FOR_ITEMS(it, N, NT, first)                                  \
+  for (int it##_base = 0; it##_base < (N); it##_base += (NT))        \
+    if (const int it = it##_base + (first); it < (N))
 
 template <int P1, int Q>
 struct Tab {
@@ -80,7 +96,30 @@ struct ColArgs {
   long long K0, NzG;      // global index of local plane 0; global plane count
   int bc;
   int l2pf;               // 1: bulk-prefetch the next brick's qdata into L2
+  double* dotp;           // non-null: per-CTA partials of x.y over owned dofs (CG's pAp)
+  long long kown;         // local planes K < kown are owned by this rank
 };
+
+// Fixed-order block sum; thread 0 stores it to *out.  All threads must call.
+// `red` is blockDim.x doubles of free shared scratch.
+__device__ __forceinline__ void block_sum_store(double v, double* out, double* red) {
+  // every thread's value through shared memory, summed in thread order by
+  // warp 0 (lane l adds threads l, l+32, ...), then across lanes in order
+  cta_sync();
+  red[threadIdx.x] = v;
+  cta_sync();
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < (int)blockDim.x; i += 32) s += red[i];
+    red[threadIdx.x] = s;
+  }
+  cta_sync();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < 32 && i < (int)blockDim.x; ++i) s += red[i];
+    *out = s;
+  }
+}
 
 enum { KIND_MASS = 0, KIND_DIFF = 1, KIND_COLLOC = 2 };
 
@@ -162,7 +201,7 @@ __device__ __forceinline__ void issue_lattice(const ColArgs& A, double* L, long 
   const long long Kg0 = K0l + A.K0;
   const bool interior = I0 > 0 && I0 + LX < A.Nx && J0 > 0 && J0 + LY < A.Ny &&
                         (!A.bc || (Kg0 > 0 && Kg0 + LZ < A.NzG));
-  for (int it = vtid(); it < LY * LZ * BX; it += NT) {
+  FOR_ITEMS(it, LY * LZ * BX, NT, vtid()) {
     const int sx = it % BX, r = it / BX, j = r % LY, k = r / LY;
     const long long J = J0 + j, K = K0l + k;
     double* dst = L + C::lat(p * sx, j, k);
@@ -233,14 +272,23 @@ struct EpiRow {
   long long gl;
   int base0, base1;  // y-element offsets of the lower / primary contributions
   bool vy0, vy1, to_carry, from_carry, row_sh, row_multi, row_ess;
+  // fused x.y (CG's pAp): lattice row of x, owned row (Dirichlet terms), lower side of the
+  // row's shared y/z face (a Dirichlet point on one shared face is written by
+  // both bricks and counted by the lower one only)
+  const double* lx;
+  bool dot, own, face_lo;
 };
 
 template <class C, int BX, bool NATURAL, int ESTRIDE, int SX>
 __device__ __forceinline__ void epi_segment(const ColArgs& A, const double* RA, const EpiRow& R,
                                             long long I0, long long nvx, long long iess,
                                             bool exok_lo, bool exok, bool xlo_sh, bool xhi_sh,
-                                            bool xlo_ess) {
+                                            bool xlo_ess, double& dsum) {
   constexpr int p = C::p, LX = C::LX;
+  // x.y by contributions: every contribution this brick writes counts (also on
+  // the non-owned top plane: the neighbour rank counts ITS contributions there);
+  // a Dirichlet value y = x counts once, on the owning rank.
+  const bool acc = R.dot, acc_ess = R.dot && R.own;
   constexpr int NPT = (SX == BX - 1) ? p + 1 : p;  // the last column also owns i = p*BX
   double v[NPT];
 #pragma unroll
@@ -278,12 +326,16 @@ __device__ __forceinline__ void epi_segment(const ColArgs& A, const double* RA, 
       const int i = p * SX + ii;
       if (i >= nv) continue;
       const bool lo = (SX == 0 && ii == 0), hi = (SX == BX - 1 && ii == p);
-      if (R.row_multi || (lo && xlo_sh) || (hi && xhi_sh))
+      if (R.row_multi || (lo && xlo_sh) || (hi && xhi_sh)) {
         R.bb[i] = v[ii];  // edge line: partial buffer
-      else if (R.row_ess || (lo && xlo_ess) || i == ie)
-        A.y[R.gl + i] = A.x[R.gl + i];
-      else
+      } else if (R.row_ess || (lo && xlo_ess) || i == ie) {
+        const double xv = A.x[R.gl + i];
+        A.y[R.gl + i] = xv;
+        if (acc_ess && R.face_lo) dsum = fma(xv, xv, dsum);
+      } else {
         red_add(A.y + R.gl + i, v[ii]);
+        if (acc) dsum = fma(R.lx[C::LXS * i], v[ii], dsum);
+      }
     }
     return;
   }
@@ -295,6 +347,7 @@ __device__ __forceinline__ void epi_segment(const ColArgs& A, const double* RA, 
         red_add(A.y + R.gl + p * SX + ii, v[ii]);
       else
         A.y[R.gl + p * SX + ii] = v[ii];
+      if (acc) dsum = fma(R.lx[C::LXS * (p * SX + ii)], v[ii], dsum);
     }
     return;
   }
@@ -304,12 +357,17 @@ __device__ __forceinline__ void epi_segment(const ColArgs& A, const double* RA, 
     if (i >= nv) continue;
     const bool lo = (SX == 0 && ii == 0), hi = (SX == BX - 1 && ii == p);
     const bool ess = R.row_ess || (lo && xlo_ess) || (i == ie);
-    if (ess)
-      A.y[R.gl + i] = A.x[R.gl + i];
-    else if ((lo && xlo_sh) || (hi && xhi_sh))
-      red_add(A.y + R.gl + i, v[ii]);
-    else
-      A.y[R.gl + i] = v[ii];
+    if (ess) {
+      const double xv = A.x[R.gl + i];
+      A.y[R.gl + i] = xv;
+      if (acc_ess && !(hi && xhi_sh)) dsum = fma(xv, xv, dsum);
+    } else {
+      if ((lo && xlo_sh) || (hi && xhi_sh))
+        red_add(A.y + R.gl + i, v[ii]);
+      else
+        A.y[R.gl + i] = v[ii];
+      if (acc) dsum = fma(R.lx[C::LXS * i], v[ii], dsum);
+    }
   }
 }
 
@@ -317,14 +375,15 @@ template <class C, int BX, bool NATURAL, int ESTRIDE, int SX>
 __device__ __forceinline__ void epi_dispatch(int sx, const ColArgs& A, const double* RA,
                                              const EpiRow& R, long long I0, long long nvx,
                                              long long iess, const bool* exok, bool xlo_sh,
-                                             bool xhi_sh, bool xlo_ess) {
+                                             bool xhi_sh, bool xlo_ess, double& dsum) {
   if constexpr (SX < BX) {
     if (sx == SX)
-      epi_segment<C, BX, NATURAL, ESTRIDE, SX>(A, RA, R, I0, nvx, iess, SX > 0 ? exok[SX > 0 ? SX - 1 : 0] : false,
-                                               exok[SX], xlo_sh, xhi_sh, xlo_ess);
+      epi_segment<C, BX, NATURAL, ESTRIDE, SX>(A, RA, R, I0, nvx, iess,
+                                               SX > 0 ? exok[SX > 0 ? SX - 1 : 0] : false,
+                                               exok[SX], xlo_sh, xhi_sh, xlo_ess, dsum);
     else
       epi_dispatch<C, BX, NATURAL, ESTRIDE, SX + 1>(sx, A, RA, R, I0, nvx, iess, exok, xlo_sh,
-                                                    xhi_sh, xlo_ess);
+                                                    xhi_sh, xlo_ess, dsum);
   }
 }
 
@@ -333,7 +392,7 @@ __device__ __forceinline__ void brick_epilogue(const ColArgs& A, const double* R
                                                const double* carry_in, double* carry_out,
                                                long long brick, int ex0, int ey0, long long I0,
                                                long long J0, long long K0l, bool first,
-                                               bool last) {
+                                               bool last, const double* Lx, double& dsum) {
   constexpr int p = C::p, P1 = p + 1, LX = C::LX, LY = C::LY;
   RA += EOFF;
   const long long nvx = A.Nx - I0;
@@ -343,8 +402,12 @@ __device__ __forceinline__ void brick_epilogue(const ColArgs& A, const double* R
   bool exok[BX];
 #pragma unroll
   for (int q = 0; q < BX; ++q) exok[q] = ex0 + q < A.nx;
-  for (int it = threadIdx.x; it < LY * P1 * BX; it += NT) {
-    const int sx = it / (LY * P1), r = it % (LY * P1), j = r % LY, k = r / LY;
+  // items (element column sx, row r): the rows of one column are padded to a
+  // multiple of 32 so every warp runs a single compile-time segment SX
+  constexpr int ROWS = LY * P1, RPS = (ROWS + 31) / 32 * 32;
+  FOR_ITEMS(it, RPS * BX, NT, threadIdx.x) {
+    const int sx = it / RPS, r = it % RPS, j = r % LY, k = r / LY;
+    if (r >= ROWS) continue;
     const long long J = J0 + j, K = K0l + k, Kg = K + A.K0;
     if (J >= A.Ny) continue;
     const int qj = j / p, rj = j - qj * p;
@@ -368,8 +431,12 @@ __device__ __forceinline__ void brick_epilogue(const ColArgs& A, const double* R
     }
     R.cin = carry_in + LX * j;
     R.cout = carry_out + LX * j;
+    R.dot = A.dotp != nullptr;
+    R.own = K < A.kown;
+    R.face_lo = ysh ? j == 0 : k == 0;
+    R.lx = Lx + C::lat(0, j, k);
     epi_dispatch<C, BX, NATURAL, ESTRIDE, 0>(sx, A, RA, R, I0, nvx, iess, exok, xlo_sh, xhi_sh,
-                                             xlo_ess);
+                                             xlo_ess, dsum);
   }
 }
 
@@ -481,259 +548,6 @@ __device__ __forceinline__ int stage_off(const ColArgs& A, int ex, int ey, int e
 }
 
 // ---------------------------------------------------------------------------
-// General kernel: mass (BP1) and diffusion (BP3) with any (P1, Q) tables.
-// NBUF = qdata staging buffers (2: next brick's copy overlaps the whole current
-// brick; 1: issued right after stage 3 consumed the buffer).
-// ---------------------------------------------------------------------------
-template <int KIND, int P1, int Q, int BX, int BY, int NT, int NBUF, int MAXR>
-__global__ void __maxnreg__(MAXR) fused_column(const __grid_constant__ Tab<P1, Q> T, const __grid_constant__ ColArgs A) {
-  using C = Cfg<KIND, P1, Q, BX, BY>;
-  using SG = Stage<C>;
-  constexpr int p = P1 - 1, NE = C::NE, Qp = C::Qp, S2 = C::S2, NC = C::NC;
-  constexpr int Q2 = Q * Q, Q3 = Q * Q * Q;
-  constexpr bool DIFF = KIND == KIND_DIFF;
-  static_assert(NT >= C::ITEMS3, "one stage-3 item per thread");
-  static_assert(NBUF == 1 || NBUF == 2, "staging buffers");
-  extern __shared__ __align__(16) double smem[];
-  double* QS = smem;                     // NBUF x NE x SLOT (16-byte aligned)
-  double* RA = QS + NBUF * NE * SG::SLOT;
-  double* RB = RA + C::REGA;
-  double* LB = RB + C::REGB;
-  double* CY = LB + 2 * C::LAT;
-  __shared__ __align__(8) unsigned long long bars[2];
-  const int tid = threadIdx.x;
-  const bool has3 = tid < C::ITEMS3;
-  const int el3 = tid / Q2, i3 = tid % Q2;
-  if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  Brick cur = unit_first(A, blockIdx.x);
-  if (cur.u >= A.nunits) return;
-  issue_qdata<C, BX, BY>(A, cur, QS, &bars[0]);
-  issue_lattice<C, NT, BX>(A, LB, (long long)p * cur.bx * BX, (long long)p * cur.by * BY,
-                       (long long)p * cur.ez);
-  cp_async_wait_all();
-  __syncthreads();
-  unsigned phase = 0;  // bit b: parity of the next wait on bars[b]
-
-  for (int k = 0; cur.u < A.nunits; ++k) {
-    const int tid = vtid();
-    const Brick nxt = brick_next(A, cur);
-    const int ex0 = cur.bx * BX, ey0 = cur.by * BY, ez = cur.ez;
-    const long long I0 = (long long)p * ex0, J0 = (long long)p * ey0;
-    const int qb = NBUF == 2 ? (k & 1) : 0;
-    double* L = LB + (k & 1) * C::LAT;
-    if (nxt.u < A.nunits) {
-      issue_lattice<C, NT, BX>(A, LB + ((k + 1) & 1) * C::LAT, (long long)p * nxt.bx * BX,
-                           (long long)p * nxt.by * BY, (long long)p * nxt.ez);
-      if (NBUF == 2) issue_qdata<C, BX, BY>(A, nxt, QS + ((k + 1) & 1) * NE * SG::SLOT,
-                                            &bars[(k + 1) & 1]);
-    }
-
-    // ---- stage 1: contract x.  item (el, b, c), c fastest.
-    for (int it = tid; it < NE * P1 * P1; it += NT) {
-      const int el = it / (P1 * P1), r = it % (P1 * P1), c = r % P1, b = r / P1;
-      const double* xl = L + C::lat(p * (el % BX), p * (el / BX) + b, c);
-      double xa[P1];
-#pragma unroll
-      for (int a = 0; a < P1; ++a) xa[a] = xl[C::LXS * a];
-      double* t1 = RB + el * C::T1N + Qp * c + S2 * b;
-#pragma unroll
-      for (int qx = 0; qx < Q; ++qx) {
-        double sb = 0.0, sg = 0.0;
-#pragma unroll
-        for (int a = 0; a < P1; ++a) {
-          sb = fma(T.B[qx * P1 + a], xa[a], sb);
-          if (DIFF) sg = fma(T.G[qx * P1 + a], xa[a], sg);
-        }
-        t1[qx] = sb;                      // B_x x
-        if (DIFF) t1[S2 * P1 + qx] = sg;  // G_x x
-      }
-    }
-    __syncthreads();
-
-    // ---- stage 2: contract y.  item (el, qx, c), qx fastest.
-    for (int it = tid; it < NE * Q * P1; it += NT) {
-      const int el = it / (Q * P1), r = it % (Q * P1), qx = r % Q, c = r / Q;
-      const double* t1 = RB + el * C::T1N + qx + Qp * c;
-      double vb[P1], vg[P1];
-#pragma unroll
-      for (int b = 0; b < P1; ++b) {
-        vb[b] = t1[S2 * b];
-        if (DIFF) vg[b] = t1[S2 * P1 + S2 * b];
-      }
-      double* t2 = RA + el * C::T2N + qx + Q * c;
-#pragma unroll
-      for (int qy = 0; qy < Q; ++qy) {
-        double bb = 0.0, gb = 0.0, bg = 0.0;
-#pragma unroll
-        for (int b = 0; b < P1; ++b) {
-          bb = fma(T.B[qy * P1 + b], vb[b], bb);
-          if (DIFF) {
-            gb = fma(T.B[qy * P1 + b], vg[b], gb);
-            bg = fma(T.G[qy * P1 + b], vb[b], bg);
-          }
-        }
-        if (DIFF) {
-          t2[C::RS * qy] = gb;               // G_x B_y
-          t2[C::T2C + C::RS * qy] = bg;      // B_x G_y
-          t2[2 * C::T2C + C::RS * qy] = bb;  // B_x B_y
-        } else {
-          t2[C::RS * qy] = bb;
-        }
-      }
-    }
-    __syncthreads();
-
-    // ---- stage 3: contract z in registers, pointwise D (staged in smem by the
-    //      bulk copy), z-transpose.  item (el, qx, qy) = this thread's column.
-    mbar_wait(&bars[qb], (phase >> qb) & 1);
-    phase ^= 1u << qb;
-    if (has3 && ex0 + el3 % BX < A.nx && ey0 + el3 / BX < A.ny) {
-      const int qx3 = i3 % Q, qy3 = i3 / Q;
-      double* t2 = RA + el3 * C::T2N + qx3 + C::RS * qy3;
-      const double* dq = QS + (qb * NE + el3) * SG::SLOT +
-                         stage_off<C>(A, ex0 + el3 % BX, ey0 + el3 / BX, ez) + i3;
-      if (DIFF) {
-        double g0[P1], g1[P1], g2[P1], s0[P1], s1[P1], s2[P1];
-#pragma unroll
-        for (int c = 0; c < P1; ++c) {
-          g0[c] = t2[Q * c];
-          g1[c] = t2[C::T2C + Q * c];
-          g2[c] = t2[2 * C::T2C + Q * c];
-          s0[c] = s1[c] = s2[c] = 0.0;
-        }
-#pragma unroll
-        for (int qz = 0; qz < Q; ++qz) {
-          const double* d = dq + qz * Q2;
-          double u0 = 0.0, u1 = 0.0, u2 = 0.0;
-#pragma unroll
-          for (int c = 0; c < P1; ++c) {
-            u0 = fma(T.B[qz * P1 + c], g0[c], u0);
-            u1 = fma(T.B[qz * P1 + c], g1[c], u1);
-            u2 = fma(T.G[qz * P1 + c], g2[c], u2);
-          }
-          const double d00 = d[0], d01 = d[Q3], d02 = d[2 * Q3], d11 = d[3 * Q3],
-                       d12 = d[4 * Q3], d22 = d[5 * Q3];
-          const double w0 = d00 * u0 + d01 * u1 + d02 * u2;
-          const double w1 = d01 * u0 + d11 * u1 + d12 * u2;
-          const double w2 = d02 * u0 + d12 * u1 + d22 * u2;
-#pragma unroll
-          for (int c = 0; c < P1; ++c) {
-            s0[c] = fma(T.B[qz * P1 + c], w0, s0[c]);
-            s1[c] = fma(T.B[qz * P1 + c], w1, s1[c]);
-            s2[c] = fma(T.G[qz * P1 + c], w2, s2[c]);
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < P1; ++c) {
-          t2[Q * c] = s0[c];
-          t2[C::T2C + Q * c] = s1[c];
-          t2[2 * C::T2C + Q * c] = s2[c];
-        }
-      } else {
-        double g[P1], s[P1];
-#pragma unroll
-        for (int c = 0; c < P1; ++c) { g[c] = t2[Q * c]; s[c] = 0.0; }
-#pragma unroll
-        for (int qz = 0; qz < Q; ++qz) {
-          double uq = 0.0;
-#pragma unroll
-          for (int c = 0; c < P1; ++c) uq = fma(T.B[qz * P1 + c], g[c], uq);
-          const double v = dq[qz * Q2] * uq;
-#pragma unroll
-          for (int c = 0; c < P1; ++c) s[c] = fma(T.B[qz * P1 + c], v, s[c]);
-        }
-#pragma unroll
-        for (int c = 0; c < P1; ++c) t2[Q * c] = s[c];
-      }
-    }
-    __syncthreads();
-    if (NBUF == 1 && nxt.u < A.nunits) issue_qdata<C, BX, BY>(A, nxt, QS, &bars[0]);
-
-    // ---- stage 2^T: contract qy.  item (el, qx, c), qx fastest.
-    for (int it = tid; it < NE * Q * P1; it += NT) {
-      const int el = it / (Q * P1), r = it % (Q * P1), qx = r % Q, c = r / Q;
-      const double* t2 = RA + el * C::T2N + qx + Q * c;
-      double* t1 = RB + el * C::T1N + qx + Qp * c;
-      if (DIFF) {
-        double v0[Q], v1[Q], v2[Q];
-#pragma unroll
-        for (int qy = 0; qy < Q; ++qy) {
-          v0[qy] = t2[C::RS * qy];
-          v1[qy] = t2[C::T2C + C::RS * qy];
-          v2[qy] = t2[2 * C::T2C + C::RS * qy];
-        }
-#pragma unroll
-        for (int b = 0; b < P1; ++b) {
-          double rg = 0.0, rb = 0.0;
-#pragma unroll
-          for (int qy = 0; qy < Q; ++qy) {
-            rg = fma(T.B[qy * P1 + b], v0[qy], rg);
-            rb = fma(T.G[qy * P1 + b], v1[qy], rb);
-            rb = fma(T.B[qy * P1 + b], v2[qy], rb);
-          }
-          t1[S2 * b] = rg;            // -> G_x^T
-          t1[S2 * P1 + S2 * b] = rb;  // -> B_x^T
-        }
-      } else {
-        double v[Q];
-#pragma unroll
-        for (int qy = 0; qy < Q; ++qy) v[qy] = t2[C::RS * qy];
-#pragma unroll
-        for (int b = 0; b < P1; ++b) {
-          double rb = 0.0;
-#pragma unroll
-          for (int qy = 0; qy < Q; ++qy) rb = fma(T.B[qy * P1 + b], v[qy], rb);
-          t1[S2 * b] = rb;
-        }
-      }
-    }
-    __syncthreads();
-
-    // ---- stage 1^T: contract qx.  item (el, b, c), c fastest -> y_e[a][b][c].
-    for (int it = tid; it < NE * P1 * P1; it += NT) {
-      const int el = it / (P1 * P1), r = it % (P1 * P1), c = r % P1, b = r / P1;
-      const double* t1 = RB + el * C::T1N + Qp * c + S2 * b;
-      double rg[Q], rb[Q];
-#pragma unroll
-      for (int qx = 0; qx < Q; ++qx) {
-        if (DIFF) {
-          rg[qx] = t1[qx];
-          rb[qx] = t1[S2 * P1 + qx];
-        } else {
-          rb[qx] = t1[qx];
-        }
-      }
-      double* ye = RA + el * C::YEN + c + P1 * b;
-#pragma unroll
-      for (int a = 0; a < P1; ++a) {
-        double s = 0.0;
-#pragma unroll
-        for (int qx = 0; qx < Q; ++qx) {
-          s = fma(T.B[qx * P1 + a], rb[qx], s);
-          if (DIFF) s = fma(T.G[qx * P1 + a], rg[qx], s);
-        }
-        ye[C::SA * a] = s;
-      }
-    }
-    __syncthreads();
-
-    const long long brick = cur.bx + (long long)A.nbx * (cur.by + (long long)A.nby * ez);
-    brick_epilogue<C, NT, BX, BY, false>(A, RA, CY + ((ez + 1) & 1) * C::CARRY,
-                                         CY + (ez & 1) * C::CARRY, brick, ex0, ey0, I0, J0,
-                                         (long long)p * ez, ez == cur.z0, ez + 1 == cur.z1);
-    cp_async_wait_all();
-    __syncthreads();
-    cur = nxt;
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Tensor-core (DMMA) kernel: mass (BP1) and diffusion (BP3), any (P1, Q).
 //
 // Each 1D contraction of the sum factorization is a small FP64 GEMM on the
@@ -761,32 +575,6 @@ __device__ __forceinline__ void dmma(double (&d)[4], const double (&a)[4], const
 }
 
 constexpr int mod16_4(int n) { return n + (((4 - n) % 16) + 16) % 16; }  // >= n, == 4 (mod 16)
-
-template <int KIND, int P1, int Q, int BX, int BY>
-struct CfgM {
-  static constexpr int p = P1 - 1, P = P1, NE = BX * BY;
-  static constexpr int LX = p * BX + 1, LY = p * BY + 1, LZ = P1;
-  static constexpr int BLAT = LX * LY * LZ;
-  static constexpr int LXS = mod16_4(LY * LZ);  // x-stride of the smem lattice
-  static constexpr int LAT = LXS * LX;
-  static constexpr int NR1 = NE * P * P, NR2 = NE * Q * P, NR3 = NE * Q * Q;  // GEMM rows
-  static constexpr int MT1 = (NR1 + 15) / 16, MT2 = (NR2 + 15) / 16, MT3 = (NR3 + 15) / 16;
-  static constexpr int KS1 = mod16_4(NR1), KS2 = mod16_4(NR2), KS3 = mod16_4(NR3);
-  static constexpr int NA = (KIND == KIND_MASS) ? 1 : 2;  // stage-1 outputs / stage-2T outputs
-  static constexpr int NB = (KIND == KIND_MASS) ? 1 : 3;  // stage-2 outputs / stage-3 outputs
-  static constexpr int cmax(int a, int b) { return a > b ? a : b; }
-  static constexpr int T1A = cmax(P * KS2, Q * KS1);      // one array of the T1 region
-  static constexpr int T2A = P * KS3;                      // one array of the T2 region
-  static constexpr int SA = ((P * P) % 2 == 0) ? P * P + 1 : P * P;
-  static constexpr int YEN = SA * P;
-  static constexpr int REG1 = NA * T1A;
-  static constexpr int REG2 = cmax(NB * T2A, NE * YEN);
-  static constexpr int CARRY = LX * LY;
-  static constexpr int SMEM_BYTES = (REG1 + REG2 + 2 * LAT + 2 * CARRY) * 8;
-  static constexpr int NC = (KIND == KIND_MASS) ? 1 : 6;
-  static constexpr int NQ1 = Q;
-  __device__ static constexpr int lat(int i, int j, int k) { return k + LZ * j + LXS * i; }
-};
 
 // B-operand fragment of a 1D table M (rows x cols, row-major) for GEMM n index
 // `n` and k index `k`: value M[n][k] if TRANS == false (k runs over the table's
@@ -901,17 +689,21 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB)
   const int exl = warp % BX, eyl = warp / BX;
   const unsigned long long pol = evict_first_policy();
 
-  for (int i = tid; i < C::SMEM_DOUBLES; i += NT) smem[i] = 0.0;
-  __syncthreads();
+  FOR_ITEMS(i, C::SMEM_DOUBLES, NT, tid) smem[i] = 0.0;
+  cta_sync();
 
   Brick cur = unit_first(A, blockIdx.x);
-  if (cur.u >= A.nunits) return;
+  if (cur.u >= A.nunits) {
+    if (A.dotp && threadIdx.x == 0) A.dotp[blockIdx.x] = 0.0;
+    return;
+  }
   prefetch_qdata_l2<C, BX, BY>(A, cur);
   issue_lattice<C, NT, BX>(A, LB, (long long)p * cur.bx * BX, (long long)p * cur.by * BY,
                            (long long)p * cur.ez);
   cp_async_wait_all();
-  __syncthreads();
+  cta_sync();
 
+  double dsum = 0.0;  // this thread's share of x.y (A.dotp)
   for (int kb = 0; cur.u < A.nunits; ++kb) {
     const Brick nxt = brick_next(A, cur);
     const int ex0 = cur.bx * BX, ey0 = cur.by * BY, ez = cur.ez;
@@ -1275,16 +1067,17 @@ __global__ void __launch_bounds__(32 * BX * BY, MINB)
         }
       }
     }
-    __syncthreads();
+    cta_sync();
 
     const long long brick = cur.bx + (long long)A.nbx * (cur.by + (long long)A.nby * ez);
     if (!(HOFEM_DBG_SKIP & 1)) brick_epilogue<C, NT, BX, BY, false, C::WS, C::W1>(
         A, smem, CY + ((ez + 1) & 1) * C::CARRY, CY + (ez & 1) * C::CARRY, brick, ex0, ey0, I0,
-        J0, (long long)p * ez, ez == cur.z0, ez + 1 == cur.z1);
+        J0, (long long)p * ez, ez == cur.z0, ez + 1 == cur.z1, L, dsum);
     cp_async_wait_all();
-    __syncthreads();
+    cta_sync();
     cur = nxt;
   }
+  if (A.dotp) block_sum_store(dsum, A.dotp + blockIdx.x, smem);
 }
 
 template <int KIND, int P1, int Q, int BX, int BY>
@@ -1377,13 +1170,13 @@ __device__ __forceinline__ void ld_row(const double* row, double (&r)[P]) {
 
 template <class C, int NT, int BX, int BY>
 __device__ __forceinline__ void simt_epilogue(const ColArgs& A, double* smem, double* CY,
-                                              const Brick& b) {
+                                              const Brick& b, const double* L, double& dsum) {
   constexpr int p = C::p;
   const int ex0 = b.bx * BX, ey0 = b.by * BY, ez = b.ez;
   const long long brick = b.bx + (long long)A.nbx * (b.by + (long long)A.nby * ez);
   brick_epilogue<C, NT, BX, BY, false, C::EB, C::T1SZ>(
       A, smem, CY + ((ez + 1) & 1) * C::CARRY, CY + (ez & 1) * C::CARRY, brick, ex0, ey0,
-      (long long)p * ex0, (long long)p * ey0, (long long)p * ez, ez == b.z0, ez + 1 == b.z1);
+      (long long)p * ex0, (long long)p * ey0, (long long)p * ez, ez == b.z0, ez + 1 == b.z1, L, dsum);
 }
 
 // Table row from the kernel-parameter constant bank.  `zo` is a loop-variant
@@ -1432,16 +1225,19 @@ __global__ void __maxnreg__(MAXR)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
 
-  for (int i = threadIdx.x; i < C::SMEM_DOUBLES; i += NT) smem[i] = 0.0;
-  __syncthreads();
-  for (int i = threadIdx.x; i < Q * P; i += NT) {
+  FOR_ITEMS(i, C::SMEM_DOUBLES, NT, threadIdx.x) smem[i] = 0.0;
+  cta_sync();
+  FOR_ITEMS(i, Q * P, NT, threadIdx.x) {
     TBs[(i / P) * PR + i % P] = T.B[i];
     TGs[(i / P) * PR + i % P] = T.G[i];
   }
-  __syncthreads();
+  cta_sync();
 
   Brick cur = unit_first(A, blockIdx.x);
-  if (cur.u >= A.nunits) return;
+  if (cur.u >= A.nunits) {
+    if (A.dotp && threadIdx.x == 0) A.dotp[blockIdx.x] = 0.0;
+    return;
+  }
   if (C::DSM)
     issue_qdata<C, BX, BY>(A, cur, QS, &qbar);
   else
@@ -1449,14 +1245,10 @@ __global__ void __maxnreg__(MAXR)
   issue_lattice<C, NT, BX>(A, LB, (long long)p * cur.bx * BX, (long long)p * cur.by * BY,
                            (long long)p * cur.ez);
   cp_async_wait_all();
-  __syncthreads();
+  cta_sync();
   unsigned qphase = 0;
 
-  // The epilogue of brick k shares a barrier interval with S1 of brick k+1
-  // (disjoint shared memory: y_e/carry vs lattice/T1), one barrier less per
-  // brick and two independent instruction streams for the scheduler.
-  Brick prev;
-  prev.u = A.nunits;  // none yet
+  double dsum = 0.0;  // this thread's share of x.y (A.dotp)
   for (int kb = 0; cur.u < A.nunits; ++kb) {
     const int tid = vtid();
     const int zo = cur.ez >> 30;  // == 0, loop-variant (see cb_row)
@@ -1469,10 +1261,9 @@ __global__ void __maxnreg__(MAXR)
                                (long long)p * nxt.by * BY, (long long)p * nxt.ez);
       prefetch_qdata_l2<C, BX, BY>(A, nxt);
     }
-    if (HOFEM_SIMT_MERGE && prev.u < A.nunits) simt_epilogue<C, NT, BX, BY>(A, smem, CY, prev);
 
     // ---- S1: contract x.  item (el, b, c), c fastest.
-    for (int it = tid; it < NE * P * P; it += NT) {
+    FOR_ITEMS(it, NE * P * P, NT, tid) {
       const int el = it / (P * P), r = it % (P * P), b = r / P, c = r % P;
       const double* xl = L + C::lat(p * (el % BX), p * (el / BX) + b, c);
       double xa[P];
@@ -1494,10 +1285,10 @@ __global__ void __maxnreg__(MAXR)
         if (DIFF) t1[T1M + qx * S1] = sg;
       }
     }
-    __syncthreads();
+    cta_sync();
 
     // ---- S2: contract y.  item (el, qx, c), c fastest.
-    for (int it = tid; it < NE * Q * P; it += NT) {
+    FOR_ITEMS(it, NE * Q * P, NT, tid) {
       const int el = it / (Q * P), r = it % (Q * P), qx = r / P, c = r % P;
       const double* t1 = smem + el * EB + qx * S1 + c;
       double vb[P], vg[P];
@@ -1534,7 +1325,7 @@ __global__ void __maxnreg__(MAXR)
         }
       }
     }
-    __syncthreads();
+    cta_sync();
 
     // ---- S3: z contraction, pointwise D, z back-contraction; item (el, pt).
     //      Streamed over qz: u(qz) -> w(qz) = D u -> s += B/G(qz) w.  D(qz+1)
@@ -1543,7 +1334,7 @@ __global__ void __maxnreg__(MAXR)
       mbar_wait(&qbar, qphase);
       qphase ^= 1u;
     }
-    for (int it = tid; it < NE * Q2; it += NT) {
+    FOR_ITEMS(it, NE * Q2, NT, tid) {
       const int el = it / Q2, pt = it % Q2;
       const int ex = ex0 + el % BX, ey = ey0 + el / BX;
       if (ex >= A.nx || ey >= A.ny) continue;
@@ -1639,11 +1430,11 @@ __global__ void __maxnreg__(MAXR)
         for (int c = 0; c < P; ++c) t2[c] = s[c];
       }
     }
-    __syncthreads();
+    cta_sync();
     if (C::DSM) issue_qdata<C, BX, BY>(A, nxt, QS, &qbar);  // D(k) consumed
 
     // ---- S2T: contract qy.  item (el, qx, c), c fastest.
-    for (int it = tid; it < NE * Q * P; it += NT) {
+    FOR_ITEMS(it, NE * Q * P, NT, tid) {
       const int el = it / (Q * P), r = it % (Q * P), qx = r / P, c = r % P;
       const double* t2 = smem + el * EB + T1SZ + qx * SP + c;
       double* t1 = smem + el * EB + qx * S1 + c;
@@ -1684,10 +1475,10 @@ __global__ void __maxnreg__(MAXR)
         if (DIFF) t1[T1M + b * P] = rg[b];  // -> G_x^T
       }
     }
-    __syncthreads();
+    cta_sync();
 
     // ---- S1T: contract qx.  item (el, b, c) -> y_e[a][b][c] (aliases T2).
-    for (int it = tid; it < NE * P * P; it += NT) {
+    FOR_ITEMS(it, NE * P * P, NT, tid) {
       const int el = it / (P * P), r = it % (P * P);
       const double* t1 = smem + el * EB + r;
       double ye[P];
@@ -1719,16 +1510,13 @@ __global__ void __maxnreg__(MAXR)
       for (int a = 0; a < P; ++a) yo[C::SA * a] = ye[a];
     }
 
-    if (!HOFEM_SIMT_MERGE) {
-      __syncthreads();
-      simt_epilogue<C, NT, BX, BY>(A, smem, CY, cur);
-    }
+    cta_sync();
+    simt_epilogue<C, NT, BX, BY>(A, smem, CY, cur, L, dsum);
     cp_async_wait_all();
-    __syncthreads();
-    prev = cur;
+    cta_sync();
     cur = nxt;
   }
-  if (HOFEM_SIMT_MERGE && prev.u < A.nunits) simt_epilogue<C, NT, BX, BY>(A, smem, CY, prev);
+  if (A.dotp) block_sum_store(dsum, A.dotp + blockIdx.x, smem);
 }
 
 // SIMT kernel shapes: brick BX x BY elements, NT threads (>= the stage-3 item
@@ -1806,15 +1594,18 @@ __global__ void __maxnreg__(MAXR) fused_column_colloc(const __grid_constant__ Ta
     mbar_init(&bars[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
+  cta_sync();
 
   Brick cur = unit_first(A, blockIdx.x);
-  if (cur.u >= A.nunits) return;
+  if (cur.u >= A.nunits) {
+    if (A.dotp && threadIdx.x == 0) A.dotp[blockIdx.x] = 0.0;
+    return;
+  }
   issue_qdata<C, BX, BY>(A, cur, QS, &bars[0]);
   issue_lattice<C, NT, BX>(A, LB, (long long)p * cur.bx * BX, (long long)p * cur.by * BY,
                        (long long)p * cur.ez);
   cp_async_wait_all();
-  __syncthreads();
+  cta_sync();
   unsigned phase = 0;
 
   for (int k = 0; cur.u < A.nunits; ++k) {
@@ -1862,11 +1653,11 @@ __global__ void __maxnreg__(MAXR) fused_column_colloc(const __grid_constant__ Ta
         w[2 * N3 + N2 * kz] = d02 * ux + d12 * uy + d22 * uz;
       }
     }
-    __syncthreads();
+    cta_sync();
     if (NBUF == 1 && nxt.u < A.nunits) issue_qdata<C, BX, BY>(A, nxt, QS, &bars[0]);
 
     // ---- transpose: item (el, a, b) -> y_e[a + P1 b + P1^2 c] for all c.
-    for (int it = tid; it < NE * N2; it += NT) {
+    FOR_ITEMS(it, NE * N2, NT, tid) {
       const int el = it / N2, itm = it % N2, a = itm % P1, b = itm / P1;
       const double* w = RB + el * C::WN;
       double Ga[P1], Gb[P1], wz[P1];
@@ -1889,14 +1680,16 @@ __global__ void __maxnreg__(MAXR) fused_column_colloc(const __grid_constant__ Ta
         ye[N2 * c] = s;
       }
     }
-    __syncthreads();
+    cta_sync();
 
     const long long brick = cur.bx + (long long)A.nbx * (cur.by + (long long)A.nby * ez);
+    double dsum_unused = 0.0;  // no fused dot for this kernel (A.dotp == nullptr)
     brick_epilogue<C, NT, BX, BY, true>(A, RA, CY + ((ez + 1) & 1) * C::CARRY,
                                         CY + (ez & 1) * C::CARRY, brick, ex0, ey0, I0, J0,
-                                        (long long)p * ez, ez == cur.z0, ez + 1 == cur.z1);
+                                        (long long)p * ez, ez == cur.z0, ez + 1 == cur.z1, L,
+                                        dsum_unused);
     cp_async_wait_all();
-    __syncthreads();
+    cta_sync();
     cur = nxt;
   }
 }

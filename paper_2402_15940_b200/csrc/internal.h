@@ -91,6 +91,8 @@ struct Op {
   double* d_bbuf = nullptr;
   long long bbuf_len = 0;
   int fused_variant = -1;   // -1: HOFEM_FUSED env / per-p default; 0 DMMA; 1 SIMT
+  double* d_dotp = nullptr; // per-CTA partials of the fused x.y (CG)
+  long long dotp_len = 0;
   // CG scratch
   double *d_r = nullptr, *d_p = nullptr, *d_Ap = nullptr;
   double* d_cg = nullptr;   // device CG scalars / history
@@ -108,7 +110,13 @@ hofem_status build_rhs(Op* op, double* b, cudaStream_t s);
 
 // ---- operator apply paths
 hofem_status apply_unfused(Op* op, const double* x, double* y, cudaStream_t s);
-hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s);
+// dot_out (device scalar, optional): the rank-local owned x.y, computed inside
+// the fused kernels from the contributions they write (deterministic); the
+// caller allreduces it.
+hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
+                         double* dot_out = nullptr);
+// Rank-local a.b over owned dofs into *d_out (device), deterministic; no allreduce.
+hofem_status dot_local(Mesh* m, const double* a, const double* b, double* d_out, cudaStream_t s);
 hofem_status fused_info(const Op* op, hofem_fused_info* out);
 bool fused_supported(const Op* op);
 

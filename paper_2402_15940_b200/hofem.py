@@ -81,6 +81,7 @@ SIGNATURES = {
     "hofem_op_destroy": (None, [_V]),
     "hofem_cg": (_I, [_V, _V, _V, _D, _I, _I, _I, _V, ctypes.POINTER(CGStats), _V]),
     "hofem_dot": (_I, [_V, _V, _V, ctypes.POINTER(_D), _V]),
+    "hofem_op_apply_dot": (_I, [_V, _V, _V, ctypes.POINTER(_D), _V]),
     "hofem_op_fused_info": (_I, [_V, ctypes.POINTER(FusedInfo)]),
     "hofem_op_set_fused_variant": (_I, [_V, _I]),
     "hofem_profile_enable": (_I, [_I]),
@@ -240,6 +241,14 @@ class Operator:
     def set_fused_variant(self, variant: int):
         """-1 default, 0 DMMA tensor-core kernel, 1 SIMT kernel."""
         _check(lib().hofem_op_set_fused_variant(self.handle, int(variant)))
+
+    def apply_dot(self, x: torch.Tensor, y: torch.Tensor | None = None, stream=None):
+        """y = A x and x.y over owned dofs (fused into the operator kernels)."""
+        y = torch.empty_like(x) if y is None else y
+        v = ctypes.c_double()
+        _check(lib().hofem_op_apply_dot(self.handle, _ptr(x), _ptr(y), ctypes.byref(v),
+                                        _stream(stream)))
+        return y, v.value
 
     def apply_unfused(self, x: torch.Tensor, y: torch.Tensor | None = None, stream=None):
         y = torch.empty_like(x) if y is None else y

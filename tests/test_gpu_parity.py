@@ -128,6 +128,29 @@ def test_q_override(hf, p, q, bench):
     assert rel(host(op.apply_unfused(x)), ref) <= APPLY_TOL
 
 
+@pytest.mark.parametrize("nx,ny,nz,p,bench,bc,variant", [
+    (5, 3, 4, 2, "bp3", 1, 1), (7, 5, 6, 5, "bp3", 1, 0), (7, 5, 6, 5, "bp3", 1, 1),
+    (5, 3, 3, 3, "bp1", 0, 1), (3, 3, 2, 6, "bp3", 0, 1), (5, 4, 3, 4, "bp5", 1, -1),
+    (5, 4, 3, 4, "bp5", 1, 0), (9, 5, 3, 1, "bp3", 1, 1), (3, 2, 2, 8, "bp3", 1, 1)])
+def test_fused_dot_matches_separate_dot(hf, nx, ny, nz, p, bench, bc, variant):
+    """hofem_op_apply_dot: the x.y accumulated inside the fused kernels equals
+    the plain owned-dof dot of the same x and y (and the oracle's x.Ax) up to
+    summation order, and y is the ordinary apply."""
+    m, op, om, kind, rule = make(hf, nx, ny, nz, p, bench, bc=bc)
+    op.set_fused_variant(variant)
+    x = m.random(11)
+    y, d = op.apply_dot(x)
+    y2 = host(op.apply(x))
+    assert np.array_equal(host(y).view(np.uint64), y2.view(np.uint64))
+    d2 = m.dot(x, y)
+    ref = float(np.dot(host(x), oracle_apply(om, kind, rule, host(x), bc, p)))
+    scale = float(np.dot(np.abs(host(x)), np.abs(host(y))))
+    assert abs(d - d2) <= 1e-13 * scale, (d, d2)
+    assert abs(d - ref) <= 1e-12 * scale, (d, ref)
+    _, d3 = op.apply_dot(x)
+    assert d3 == d  # deterministic
+
+
 @pytest.mark.parametrize("variant", [0, 1])
 def test_fused_bitwise_deterministic(hf, variant):
     m, op, _, _, _ = make(hf, 7, 5, 6, 5, "bp3", bc=1)
