@@ -21,7 +21,7 @@ namespace hofem {
   template <>                                                                              \
   FusedLaunch fused_shape<P1>(int, int);                                                   \
   template <>                                                                              \
-  int fused_default_variant<P1>();
+  int fused_default_variant<P1>(int);
 HOFEM_FOR_P1(HOFEM_DECL)
 #undef HOFEM_DECL
 
@@ -157,11 +157,11 @@ int fused_variant() {
   return v;
 }
 
-int default_variant(int P1) {
+int default_variant(int P1, int kind) {
   switch (P1) {
 #define HOFEM_CASE(P) \
   case P:             \
-    return fused_default_variant<P>();
+    return fused_default_variant<P>(kind);
     HOFEM_FOR_P1(HOFEM_CASE)
 #undef HOFEM_CASE
   }
@@ -281,7 +281,7 @@ Plan make_plan(const Op* op) {
   if (P.kind == KIND_COLLOC)
     P.variant = (v < 0 || v == 1) ? 1 : 2;
   else
-    P.variant = v < 0 ? default_variant(m->P1) : v;
+    P.variant = v < 0 ? default_variant(m->P1, P.kind) : v;
   P.L = shape_for(m->P1, P.kind, P.variant == 2 ? 0 : P.variant);
   P.nbx = (m->nx + P.L.BX - 1) / P.L.BX;
   P.nby = (m->ny + P.L.BY - 1) / P.L.BY;

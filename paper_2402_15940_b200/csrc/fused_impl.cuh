@@ -1756,6 +1756,6 @@ bool fused_launch(int kind, int variant, int Q, const double* B, const double* G
 template <int P1>
 FusedLaunch fused_shape(int kind, int variant);
 template <int P1>
-int fused_default_variant();
+int fused_default_variant(int kind);
 
 }  // namespace hofem

@@ -115,15 +115,18 @@ int simt_ctas_per_sm() {
 }
 
 // Default fused variant per P1 (measured): 0 tensor-core, 1 SIMT.
-constexpr int kDefaultVariant = (HOFEM_P1 == 6) ? 0 : 1;
+// Diffusion: tensor cores at p = 5 only; mass (BP1, small problems): p >= 5.
+constexpr int default_for(int kind) {
+  return kind == KIND_MASS ? (HOFEM_P1 >= 6 ? 0 : 1) : (HOFEM_P1 == 6 ? 0 : 1);
+}
 
-int pick(int variant) { return variant < 0 ? kDefaultVariant : variant; }
+int pick(int variant, int kind) { return variant < 0 ? default_for(kind) : variant; }
 
 }  // namespace
 
 template <>
-int fused_default_variant<HOFEM_P1>() {
-  return kDefaultVariant;
+int fused_default_variant<HOFEM_P1>(int kind) {
+  return default_for(kind);
 }
 
 namespace {
@@ -155,7 +158,7 @@ bool fused_launch<HOFEM_P1>(int kind, int variant, int Q, const double* B, const
                         : launch_colloc<P1>(G, A, grid, s);
     return true;
   }
-  if (pick(variant) == 1) {
+  if (pick(variant, kind) == 1) {
     if (Q == P1 + 1) {
       *err = kind == KIND_MASS ? launch_simt<KIND_MASS, P1, P1 + 1>(B, G, A, grid, s)
                                : launch_simt<KIND_DIFF, P1, P1 + 1>(B, G, A, grid, s);
@@ -193,7 +196,7 @@ FusedLaunch fused_shape<HOFEM_P1>(int kind, int variant) {
     using S = Shape<HOFEM_P1>;
     return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB, 1};
   }
-  if (pick(variant) == 1) {
+  if (pick(variant, kind) == 1) {
     using S = ShapeS<HOFEM_P1>;
     const int cps = kind == KIND_MASS ? simt_ctas_per_sm<KIND_MASS, HOFEM_P1, HOFEM_P1 + 1>()
                                       : simt_ctas_per_sm<KIND_DIFF, HOFEM_P1, HOFEM_P1 + 1>();
