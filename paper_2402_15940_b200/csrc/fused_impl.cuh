@@ -53,6 +53,9 @@
 #ifndef HOFEM_SIMT_DPF
 #define HOFEM_SIMT_DPF 0  // SIMT stage 3: qz-steps of D loads in flight (0: per p, measured)
 #endif
+#ifndef HOFEM_SIMT_EO
+#define HOFEM_SIMT_EO 1  // SIMT: even-odd (symmetry-halved) 1D contractions
+#endif
 #ifndef HOFEM_APF
 #define HOFEM_APF 0  // 1: stage 3 loads the next tile's A fragments before this tile's MMAs
 #endif
@@ -78,11 +81,42 @@ __device__ __forceinline__ void cta_sync() {
   for (int it##_base = 0; it##_base < (N); it##_base += (NT))        \
     if (const int it = it##_base + (first); it < (N))
 
+// 1D tables.  B/G [q][i] row-major; BE/BO/GE/GO are their even-odd halves
+// (fill_tab): the GLL nodes and the Gauss/GLL points are symmetric about 1/2,
+// so B[Q-1-q][P-1-i] = B[q][i] and G[Q-1-q][P-1-i] = -G[q][i], and
+//   ME[t][i] = (M[t][i] + M[t][P-1-i]) / 2   (i < P/2;  ME[t][P/2] = M[t][P/2] for odd P)
+//   MO[t][i] = (M[t][i] - M[t][P-1-i]) / 2   (i < P/2)
+// for rows t < ceil(Q/2).  A contraction of length P -> Q then costs about
+// half the multiply-adds (even-odd decomposition of symmetric 1D operators).
 template <int P1, int Q>
 struct Tab {
+  static constexpr int H = (P1 + 1) / 2, PH = P1 / 2, HQ = (Q + 1) / 2;
   double B[Q * P1];
   double G[Q * P1];
+  double BE[HQ * H], BO[HQ * PH], GE[HQ * H], GO[HQ * PH];
 };
+
+template <int P1, int Q>
+inline void fill_tab(Tab<P1, Q>& T, const double* B, const double* G) {
+  using TT = Tab<P1, Q>;
+  for (int i = 0; i < Q * P1; ++i) {
+    T.B[i] = B ? B[i] : 0.0;
+    T.G[i] = G[i];
+  }
+  for (int t = 0; t < TT::HQ; ++t) {
+    for (int i = 0; i < TT::PH; ++i) {
+      const int j = P1 - 1 - i;
+      T.BE[t * TT::H + i] = 0.5 * (T.B[t * P1 + i] + T.B[t * P1 + j]);
+      T.BO[t * TT::PH + i] = 0.5 * (T.B[t * P1 + i] - T.B[t * P1 + j]);
+      T.GE[t * TT::H + i] = 0.5 * (T.G[t * P1 + i] + T.G[t * P1 + j]);
+      T.GO[t * TT::PH + i] = 0.5 * (T.G[t * P1 + i] - T.G[t * P1 + j]);
+    }
+    if (P1 & 1) {
+      T.BE[t * TT::H + TT::PH] = T.B[t * P1 + TT::PH];
+      T.GE[t * TT::H + TT::PH] = T.G[t * P1 + TT::PH];
+    }
+  }
+}
 
 struct ColArgs {
   const double* x;
@@ -1188,6 +1222,92 @@ __device__ __forceinline__ void cb_row(const double* row, int zo, double (&r)[P]
 #pragma unroll
   for (int c = 0; c < P; ++c) r[c] = row[c + zo];
 }
+// ---- even-odd contractions (tables BE/BO/GE/GO of Tab, constant bank).  S is
+// the symmetry sign of the 1D matrix: +1 for B, -1 for G.
+template <int P>
+struct EOn {
+  static constexpr int H = (P + 1) / 2, PH = P / 2;
+};
+// v[P] -> e[i] = v[i] + v[P-1-i], o[i] = v[i] - v[P-1-i] (i < P/2); e[P/2] = v[P/2] (odd P)
+template <int P>
+__device__ __forceinline__ void eo_split(const double (&v)[P], double (&e)[EOn<P>::H],
+                                         double (&o)[EOn<P>::PH]) {
+#pragma unroll
+  for (int i = 0; i < P / 2; ++i) {
+    e[i] = v[i] + v[P - 1 - i];
+    o[i] = v[i] - v[P - 1 - i];
+  }
+  if (P & 1) e[P / 2] = v[P / 2];
+}
+// row . v over N entries (table row from the constant bank, zo = loop-variant 0)
+template <int N>
+__device__ __forceinline__ double cdot(const double* row, int zo, const double (&v)[N]) {
+  double s = row[zo] * v[0];
+#pragma unroll
+  for (int i = 1; i < N; ++i) s = fma(row[i + zo], v[i], s);
+  return s;
+}
+// forward pair t < Q/2: outputs at q = t (lo) and q = Q-1-t (hi)
+template <int S, int P>
+__device__ __forceinline__ void eo_fwd(const double* ME, const double* MO, int t, int zo,
+                                       const double (&e)[EOn<P>::H],
+                                       const double (&o)[EOn<P>::PH], double& lo, double& hi) {
+  constexpr int H = EOn<P>::H, PH = EOn<P>::PH;
+  const double E = cdot<H>(ME + t * H, zo, e), O = cdot<PH>(MO + t * PH, zo, o);
+  lo = E + O;
+  hi = S > 0 ? E - O : O - E;
+}
+// forward middle row (odd Q): B rows are even (O = 0), G rows odd (E = 0)
+template <int S, int P>
+__device__ __forceinline__ double eo_fwd_mid(const double* ME, const double* MO, int t, int zo,
+                                             const double (&e)[EOn<P>::H],
+                                             const double (&o)[EOn<P>::PH]) {
+  constexpr int H = EOn<P>::H, PH = EOn<P>::PH;
+  return S > 0 ? cdot<H>(ME + t * H, zo, e) : cdot<PH>(MO + t * PH, zo, o);
+}
+// transposed accumulate of the pair (w at q = t, w at q = Q-1-t) into SE/SO
+template <int S, int P>
+__device__ __forceinline__ void eo_acc(const double* ME, const double* MO, int t, int zo,
+                                       double wlo, double whi, double (&SE)[EOn<P>::H],
+                                       double (&SO)[EOn<P>::PH]) {
+  constexpr int H = EOn<P>::H, PH = EOn<P>::PH;
+  const double we = S > 0 ? wlo + whi : wlo - whi;
+  const double wo = S > 0 ? wlo - whi : wlo + whi;
+#pragma unroll
+  for (int i = 0; i < H; ++i) SE[i] = fma(ME[t * H + i + zo], we, SE[i]);
+#pragma unroll
+  for (int i = 0; i < PH; ++i) SO[i] = fma(MO[t * PH + i + zo], wo, SO[i]);
+}
+template <int S, int P>
+__device__ __forceinline__ void eo_acc_mid(const double* ME, const double* MO, int t, int zo,
+                                           double w, double (&SE)[EOn<P>::H],
+                                           double (&SO)[EOn<P>::PH]) {
+  constexpr int H = EOn<P>::H, PH = EOn<P>::PH;
+  if (S > 0) {
+#pragma unroll
+    for (int i = 0; i < H; ++i) SE[i] = fma(ME[t * H + i + zo], w, SE[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < PH; ++i) SO[i] = fma(MO[t * PH + i + zo], w, SO[i]);
+  }
+}
+// r[i] = SE[i] + SO[i], r[P-1-i] = SE[i] - SO[i]; r[P/2] = SE[P/2] (odd P)
+template <int P>
+__device__ __forceinline__ void eo_join(const double (&SE)[EOn<P>::H],
+                                        const double (&SO)[EOn<P>::PH], double (&r)[P]) {
+#pragma unroll
+  for (int i = 0; i < P / 2; ++i) {
+    r[i] = SE[i] + SO[i];
+    r[P - 1 - i] = SE[i] - SO[i];
+  }
+  if (P & 1) r[P / 2] = SE[P / 2];
+}
+template <int N>
+__device__ __forceinline__ void zero(double (&v)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = 0.0;
+}
+
 // measured: constant-bank tables win at p = 4, 6, 7; shared-memory rows elsewhere
 template <int P1>
 constexpr bool simt_cb() {
@@ -1201,12 +1321,14 @@ constexpr bool simt_cb() {
       ld_row<P, PR>(T##M##s + (q) * PR, r);           \
   } while (0)
 
-template <int KIND, int P1, int Q, int BX, int BY, int NT, int MAXR>
+template <int KIND, int P1, int Q, int BX, int BY, int NT, int MAXR, bool EO>
 __global__ void __maxnreg__(MAXR)
     fused_elem_simt(const __grid_constant__ Tab<P1, Q> T, const __grid_constant__ ColArgs A) {
   using C = CfgS<KIND, P1, Q, BX, BY>;
   constexpr int P = P1, p = P1 - 1, NE = C::NE;
   constexpr int Q2 = Q * Q, Q3 = Q * Q * Q;
+  constexpr int H = (P + 1) / 2, PH = P / 2, QH = Q / 2;  // even-odd sizes (EO)
+  (void)H; (void)PH; (void)QH;
   // COLLOC (BP5): GLL points = nodes, so B = I; every B contraction is the
   // identity and is skipped (diffusion structure otherwise).
   constexpr bool COL = KIND == KIND_COLLOC;
@@ -1270,6 +1392,31 @@ __global__ void __maxnreg__(MAXR)
 #pragma unroll
       for (int a = 0; a < P; ++a) xa[a] = xl[C::LXS * a];
       double* t1 = smem + el * EB + r;
+      if constexpr (EO) {
+        double e[H], o[PH];
+        eo_split<P>(xa, e, o);
+#pragma unroll
+        for (int t = 0; t < QH; ++t) {
+          double lo, hi;
+          if (COL) {
+            lo = xa[t];
+            hi = xa[Q - 1 - t];
+          } else {
+            eo_fwd<1, P>(T.BE, T.BO, t, zo, e, o, lo, hi);
+          }
+          t1[t * S1] = lo;
+          t1[(Q - 1 - t) * S1] = hi;
+          if (DIFF) {
+            eo_fwd<-1, P>(T.GE, T.GO, t, zo, e, o, lo, hi);
+            t1[T1M + t * S1] = lo;
+            t1[T1M + (Q - 1 - t) * S1] = hi;
+          }
+        }
+        if (Q & 1) {
+          t1[QH * S1] = COL ? xa[QH] : eo_fwd_mid<1, P>(T.BE, T.BO, QH, zo, e, o);
+          if (DIFF) t1[T1M + QH * S1] = eo_fwd_mid<-1, P>(T.GE, T.GO, QH, zo, e, o);
+        }
+      } else {
 #pragma unroll
       for (int qx = 0; qx < Q; ++qx) {
         double br[P], gr[P];
@@ -1283,6 +1430,7 @@ __global__ void __maxnreg__(MAXR)
         }
         t1[qx * S1] = COL ? xa[qx] : sb;  // B_x x (= x when collocated)
         if (DIFF) t1[T1M + qx * S1] = sg;
+      }
       }
     }
     cta_sync();
@@ -1298,6 +1446,45 @@ __global__ void __maxnreg__(MAXR)
         vg[b] = DIFF ? t1[T1M + b * P] : 0.0;
       }
       double* t2 = smem + el * EB + T1SZ + qx * SP + c;
+      if constexpr (EO) {
+        double eb[H], ob[PH], eg[H], og[PH];
+        eo_split<P>(vb, eb, ob);
+        if (DIFF && !COL) eo_split<P>(vg, eg, og);
+        auto put = [&](int qy, double bb, double gb, double bg) {
+          if (DIFF) {
+            t2[qy * Q * SP] = gb;            // G_x B_y  (-> u_x)
+            t2[T2M + qy * Q * SP] = bg;      // B_x G_y  (-> u_y)
+            t2[2 * T2M + qy * Q * SP] = bb;  // B_x B_y  (-> u_z)
+          } else {
+            t2[qy * Q * SP] = bb;
+          }
+        };
+#pragma unroll
+        for (int t = 0; t < QH; ++t) {
+          double bbl, bbh, gbl = 0.0, gbh = 0.0, bgl = 0.0, bgh = 0.0;
+          if (COL) {
+            bbl = vb[t]; bbh = vb[Q - 1 - t];
+            gbl = vg[t]; gbh = vg[Q - 1 - t];
+          } else {
+            eo_fwd<1, P>(T.BE, T.BO, t, zo, eb, ob, bbl, bbh);
+            if (DIFF) eo_fwd<1, P>(T.BE, T.BO, t, zo, eg, og, gbl, gbh);
+          }
+          if (DIFF) eo_fwd<-1, P>(T.GE, T.GO, t, zo, eb, ob, bgl, bgh);
+          put(t, bbl, gbl, bgl);
+          put(Q - 1 - t, bbh, gbh, bgh);
+        }
+        if (Q & 1) {
+          double bb, gb = 0.0, bg = 0.0;
+          if (COL) {
+            bb = vb[QH]; gb = vg[QH];
+          } else {
+            bb = eo_fwd_mid<1, P>(T.BE, T.BO, QH, zo, eb, ob);
+            if (DIFF) gb = eo_fwd_mid<1, P>(T.BE, T.BO, QH, zo, eg, og);
+          }
+          if (DIFF) bg = eo_fwd_mid<-1, P>(T.GE, T.GO, QH, zo, eb, ob);
+          put(QH, bb, gb, bg);
+        }
+      } else {
 #pragma unroll
       for (int qy = 0; qy < Q; ++qy) {
         double br[P], gr[P];
@@ -1324,6 +1511,7 @@ __global__ void __maxnreg__(MAXR)
           t2[qy * Q * SP] = bb;
         }
       }
+      }
     }
     cta_sync();
 
@@ -1343,6 +1531,134 @@ __global__ void __maxnreg__(MAXR)
                  : A.qd + (ex + (long long)A.nx * (ey + (long long)A.ny * ez)) *
                               (long long)(C::NC * Q3) + pt;
       double* t2 = smem + el * EB + T1SZ + pt * SP;
+      if constexpr (EO) {
+        // pairs (qz = t, Q-1-t), then the middle point (odd Q); the next pair's
+        // D values are loaded while this pair computes
+        constexpr int HQ = (Q + 1) / 2;
+        constexpr int NCD = DIFF ? 6 : 1;
+        double dl[NCD], dh[NCD];
+#pragma unroll
+        for (int m = 0; m < NCD; ++m) {
+          dl[m] = ld_d<C::DSM>(qde + m * Q3);
+          dh[m] = (HQ > 1 || !(Q & 1)) ? ld_d<C::DSM>(qde + m * Q3 + (Q - 1) * Q2) : 0.0;
+        }
+        if (DIFF) {
+          double g0[P], g1[P], g2[P];
+#pragma unroll
+          for (int c = 0; c < P; ++c) {
+            g0[c] = t2[c];
+            g1[c] = t2[T2M + c];
+            g2[c] = t2[2 * T2M + c];
+          }
+          double e0[H], o0[PH], e1[H], o1[PH], e2[H], o2[PH];
+          if (!COL) {
+            eo_split<P>(g0, e0, o0);
+            eo_split<P>(g1, e1, o1);
+          }
+          eo_split<P>(g2, e2, o2);
+          double SE0[H], SO0[PH], SE1[H], SO1[PH], SE2[H], SO2[PH];
+          zero(SE0); zero(SO0); zero(SE1); zero(SO1); zero(SE2); zero(SO2);
+#pragma unroll
+          for (int t = 0; t < HQ; ++t) {
+            const bool mid = (Q & 1) && t == QH;
+            double nl[6], nh[6];
+            if (t + 1 < HQ) {
+              const bool nmid = (Q & 1) && t + 1 == QH;
+#pragma unroll
+              for (int m = 0; m < 6; ++m) {
+                nl[m] = ld_d<C::DSM>(qde + m * Q3 + (t + 1) * Q2);
+                nh[m] = nmid ? 0.0 : ld_d<C::DSM>(qde + m * Q3 + (Q - 2 - t) * Q2);
+              }
+            }
+            double u0l, u0h = 0.0, u1l, u1h = 0.0, u2l, u2h = 0.0;
+            if (mid) {
+              u0l = COL ? g0[t] : eo_fwd_mid<1, P>(T.BE, T.BO, t, zo, e0, o0);
+              u1l = COL ? g1[t] : eo_fwd_mid<1, P>(T.BE, T.BO, t, zo, e1, o1);
+              u2l = eo_fwd_mid<-1, P>(T.GE, T.GO, t, zo, e2, o2);
+            } else {
+              if (COL) {
+                u0l = g0[t]; u0h = g0[Q - 1 - t];
+                u1l = g1[t]; u1h = g1[Q - 1 - t];
+              } else {
+                eo_fwd<1, P>(T.BE, T.BO, t, zo, e0, o0, u0l, u0h);
+                eo_fwd<1, P>(T.BE, T.BO, t, zo, e1, o1, u1l, u1h);
+              }
+              eo_fwd<-1, P>(T.GE, T.GO, t, zo, e2, o2, u2l, u2h);
+            }
+            const double w0l = dl[0] * u0l + dl[1] * u1l + dl[2] * u2l;
+            const double w1l = dl[1] * u0l + dl[3] * u1l + dl[4] * u2l;
+            const double w2l = dl[2] * u0l + dl[4] * u1l + dl[5] * u2l;
+            if (mid) {
+              if (COL) {
+                t2[t] = w0l;  // written after all loads of g0 (registers)
+                t2[T2M + t] = w1l;
+              } else {
+                eo_acc_mid<1, P>(T.BE, T.BO, t, zo, w0l, SE0, SO0);
+                eo_acc_mid<1, P>(T.BE, T.BO, t, zo, w1l, SE1, SO1);
+              }
+              eo_acc_mid<-1, P>(T.GE, T.GO, t, zo, w2l, SE2, SO2);
+            } else {
+              const double w0h = dh[0] * u0h + dh[1] * u1h + dh[2] * u2h;
+              const double w1h = dh[1] * u0h + dh[3] * u1h + dh[4] * u2h;
+              const double w2h = dh[2] * u0h + dh[4] * u1h + dh[5] * u2h;
+              if (COL) {
+                t2[t] = w0l; t2[Q - 1 - t] = w0h;
+                t2[T2M + t] = w1l; t2[T2M + Q - 1 - t] = w1h;
+              } else {
+                eo_acc<1, P>(T.BE, T.BO, t, zo, w0l, w0h, SE0, SO0);
+                eo_acc<1, P>(T.BE, T.BO, t, zo, w1l, w1h, SE1, SO1);
+              }
+              eo_acc<-1, P>(T.GE, T.GO, t, zo, w2l, w2h, SE2, SO2);
+            }
+            if (t + 1 < HQ) {
+#pragma unroll
+              for (int m = 0; m < 6; ++m) { dl[m] = nl[m]; dh[m] = nh[m]; }
+            }
+          }
+          double s[P];
+          if (!COL) {
+            eo_join<P>(SE0, SO0, s);
+#pragma unroll
+            for (int c = 0; c < P; ++c) t2[c] = s[c];
+            eo_join<P>(SE1, SO1, s);
+#pragma unroll
+            for (int c = 0; c < P; ++c) t2[T2M + c] = s[c];
+          }
+          eo_join<P>(SE2, SO2, s);
+#pragma unroll
+          for (int c = 0; c < P; ++c) t2[2 * T2M + c] = s[c];
+        } else {
+          double g[P];
+#pragma unroll
+          for (int c = 0; c < P; ++c) g[c] = t2[c];
+          double e[H], o[PH], SE[H], SO[PH];
+          eo_split<P>(g, e, o);
+          zero(SE); zero(SO);
+#pragma unroll
+          for (int t = 0; t < HQ; ++t) {
+            const bool mid = (Q & 1) && t == QH;
+            double nl = 0.0, nh = 0.0;
+            if (t + 1 < HQ) {
+              nl = ld_d<C::DSM>(qde + (t + 1) * Q2);
+              nh = ((Q & 1) && t + 1 == QH) ? 0.0 : ld_d<C::DSM>(qde + (Q - 2 - t) * Q2);
+            }
+            if (mid) {
+              const double u = eo_fwd_mid<1, P>(T.BE, T.BO, t, zo, e, o);
+              eo_acc_mid<1, P>(T.BE, T.BO, t, zo, dl[0] * u, SE, SO);
+            } else {
+              double ul, uh;
+              eo_fwd<1, P>(T.BE, T.BO, t, zo, e, o, ul, uh);
+              eo_acc<1, P>(T.BE, T.BO, t, zo, dl[0] * ul, dh[0] * uh, SE, SO);
+            }
+            dl[0] = nl;
+            dh[0] = nh;
+          }
+          double s[P];
+          eo_join<P>(SE, SO, s);
+#pragma unroll
+          for (int c = 0; c < P; ++c) t2[c] = s[c];
+        }
+      } else {
       if (DIFF) {
         // D ring: qz .. qz+DPF-1 in flight (volatile loads keep program order)
         constexpr int DPF0 =
@@ -1429,6 +1745,7 @@ __global__ void __maxnreg__(MAXR)
 #pragma unroll
         for (int c = 0; c < P; ++c) t2[c] = s[c];
       }
+      }
     }
     cta_sync();
     if (C::DSM) issue_qdata<C, BX, BY>(A, nxt, QS, &qbar);  // D(k) consumed
@@ -1438,6 +1755,60 @@ __global__ void __maxnreg__(MAXR)
       const int el = it / (Q * P), r = it % (Q * P), qx = r / P, c = r % P;
       const double* t2 = smem + el * EB + T1SZ + qx * SP + c;
       double* t1 = smem + el * EB + qx * S1 + c;
+      if constexpr (EO) {
+        // rg = B_y^T v0 (x part), rb = G_y^T v1 + B_y^T v2 (y, z parts); mass: rb = B_y^T v0
+        double SEg[H], SOg[PH], SEb[H], SOb[PH];
+        zero(SEg); zero(SOg); zero(SEb); zero(SOb);
+        double rg[P] = {}, rb[P];
+        constexpr int QS = Q * SP;
+#pragma unroll
+        for (int t = 0; t < (Q + 1) / 2; ++t) {
+          const int th = Q - 1 - t;
+          if ((Q & 1) && t == QH) {
+            const double v0 = t2[t * QS];
+            if (!DIFF) {
+              eo_acc_mid<1, P>(T.BE, T.BO, t, zo, v0, SEb, SOb);
+              continue;
+            }
+            const double v1 = t2[T2M + t * QS], v2 = t2[2 * T2M + t * QS];
+            if (COL) {
+              rg[t] = v0;
+            } else {
+              eo_acc_mid<1, P>(T.BE, T.BO, t, zo, v0, SEg, SOg);
+              eo_acc_mid<1, P>(T.BE, T.BO, t, zo, v2, SEb, SOb);
+            }
+            eo_acc_mid<-1, P>(T.GE, T.GO, t, zo, v1, SEb, SOb);
+            continue;
+          }
+          const double v0l = t2[t * QS], v0h = t2[th * QS];
+          if (!DIFF) {
+            eo_acc<1, P>(T.BE, T.BO, t, zo, v0l, v0h, SEb, SOb);
+            continue;
+          }
+          const double v1l = t2[T2M + t * QS], v1h = t2[T2M + th * QS];
+          const double v2l = t2[2 * T2M + t * QS], v2h = t2[2 * T2M + th * QS];
+          if (COL) {
+            rg[t] = v0l;
+            rg[th] = v0h;
+          } else {
+            eo_acc<1, P>(T.BE, T.BO, t, zo, v0l, v0h, SEg, SOg);
+            eo_acc<1, P>(T.BE, T.BO, t, zo, v2l, v2h, SEb, SOb);
+          }
+          eo_acc<-1, P>(T.GE, T.GO, t, zo, v1l, v1h, SEb, SOb);
+        }
+        eo_join<P>(SEb, SOb, rb);
+        if (DIFF && !COL) eo_join<P>(SEg, SOg, rg);
+        if (COL) {
+          // collocated: the z part is B_y^T v2 = v2 (identity), added after G_y^T v1
+#pragma unroll
+          for (int b = 0; b < P; ++b) rb[b] += t2[2 * T2M + b * QS];
+        }
+#pragma unroll
+        for (int b = 0; b < P; ++b) {
+          t1[b * P] = rb[b];
+          if (DIFF) t1[T1M + b * P] = rg[b];
+        }
+      } else {
       double rb[P], rg[P];
 #pragma unroll
       for (int b = 0; b < P; ++b) rb[b] = rg[b] = 0.0;
@@ -1474,6 +1845,7 @@ __global__ void __maxnreg__(MAXR)
         t1[b * P] = rb[b];                  // -> B_x^T
         if (DIFF) t1[T1M + b * P] = rg[b];  // -> G_x^T
       }
+      }
     }
     cta_sync();
 
@@ -1482,6 +1854,27 @@ __global__ void __maxnreg__(MAXR)
       const int el = it / (P * P), r = it % (P * P);
       const double* t1 = smem + el * EB + r;
       double ye[P];
+      if constexpr (EO) {
+        // ye = B_x^T vb + G_x^T vg (collocated: vb + G_x^T vg; mass: B_x^T vb)
+        double SE[H], SO[PH];
+        zero(SE); zero(SO);
+#pragma unroll
+        for (int t = 0; t < (Q + 1) / 2; ++t) {
+          const int th = Q - 1 - t;
+          if ((Q & 1) && t == QH) {
+            if (!COL) eo_acc_mid<1, P>(T.BE, T.BO, t, zo, t1[t * S1], SE, SO);
+            if (DIFF) eo_acc_mid<-1, P>(T.GE, T.GO, t, zo, t1[T1M + t * S1], SE, SO);
+            continue;
+          }
+          if (!COL) eo_acc<1, P>(T.BE, T.BO, t, zo, t1[t * S1], t1[th * S1], SE, SO);
+          if (DIFF) eo_acc<-1, P>(T.GE, T.GO, t, zo, t1[T1M + t * S1], t1[T1M + th * S1], SE, SO);
+        }
+        eo_join<P>(SE, SO, ye);
+        if (COL) {
+#pragma unroll
+          for (int a = 0; a < P; ++a) ye[a] += t1[a * S1];
+        }
+      } else {
 #pragma unroll
       for (int a = 0; a < P; ++a) ye[a] = 0.0;
 #pragma unroll
@@ -1504,6 +1897,7 @@ __global__ void __maxnreg__(MAXR)
 #pragma unroll
           for (int a = 0; a < P; ++a) ye[a] = fma(br[a], vb, ye[a]);
         }
+      }
       }
       double* yo = smem + el * EB + T1SZ + r;
 #pragma unroll

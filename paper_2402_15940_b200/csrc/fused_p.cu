@@ -32,8 +32,7 @@ cudaError_t launch_general(const double* B, const double* G, const ColArgs& A, i
   using S = ShapeE<P1>;
   constexpr int SMEM = smem_bytes_elem<KIND, P1, Q, S::BX, S::BY>();
   Tab<P1, Q> T;
-  memcpy(T.B, B, sizeof(T.B));
-  memcpy(T.G, G, sizeof(T.G));
+  fill_tab(T, B, G);
   auto kern = mma_kernel<KIND, P1, Q>();
   static bool attr_done = false;
   cudaError_t e = set_smem(kern, SMEM, &attr_done);
@@ -45,7 +44,7 @@ cudaError_t launch_general(const double* B, const double* G, const ColArgs& A, i
 template <int KIND, int P1, int Q>
 auto simt_kernel() {
   using S = ShapeSK<KIND, P1>;
-  return fused_elem_simt<KIND, P1, Q, S::BX, S::BY, S::NT, S::MAXR>;
+  return fused_elem_simt<KIND, P1, Q, S::BX, S::BY, S::NT, S::MAXR, HOFEM_SIMT_EO != 0>;
 }
 template <int KIND, int P1, int Q>
 constexpr int simt_smem() {
@@ -59,8 +58,7 @@ cudaError_t launch_simt(const double* B, const double* G, const ColArgs& A, int 
   using S = ShapeSK<KIND, P1>;
   constexpr int SMEM = simt_smem<KIND, P1, Q>();
   Tab<P1, Q> T;
-  memcpy(T.B, B, sizeof(T.B));
-  memcpy(T.G, G, sizeof(T.G));
+  fill_tab(T, B, G);
   auto kern = simt_kernel<KIND, P1, Q>();
   static bool attr_done = false;
   cudaError_t e = set_smem(kern, SMEM, &attr_done);
@@ -115,10 +113,9 @@ int simt_ctas_per_sm() {
 }
 
 // Default fused variant per P1 (measured): 0 tensor-core, 1 SIMT.
-// Diffusion: tensor cores at p = 5 only; mass (BP1, small problems): p >= 5.
-constexpr int default_for(int kind) {
-  return kind == KIND_MASS ? (HOFEM_P1 >= 6 ? 0 : 1) : (HOFEM_P1 == 6 ? 0 : 1);
-}
+// With even-odd contractions the SIMT kernel is faster at every p and kind
+// (gpurun_out/e1: BP3 p=5 1.37 ms vs 1.62 ms DMMA; BP1 p=8 31.5 us vs 45 us).
+constexpr int default_for(int) { return 1; }
 
 int pick(int variant, int kind) { return variant < 0 ? default_for(kind) : variant; }
 
@@ -136,8 +133,7 @@ cudaError_t launch_colloc(const double* G, const ColArgs& A, int grid, cudaStrea
   using S = Shape<P1>;
   constexpr int SMEM = smem_bytes<KIND_COLLOC, P1, P1, S::BX, S::BY, S::NBUF>();
   Tab<P1, P1> T;
-  memset(T.B, 0, sizeof(T.B));
-  memcpy(T.G, G, sizeof(T.G));
+  fill_tab(T, nullptr, G);
   auto kern = fused_column_colloc<P1, S::BX, S::BY, S::NT, S::NBUF, S::MAXR>;
   static bool attr_done = false;
   cudaError_t e = set_smem(kern, SMEM, &attr_done);
