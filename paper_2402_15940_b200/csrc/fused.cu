@@ -120,7 +120,7 @@ __device__ __forceinline__ double fixup_point(const FixArgs& F) {
       for (int a = 0; a < nbxl; ++a) {
         const long long brick = bx[a] + (long long)F.nbx * (by[b] + (long long)F.nby * bz[c]);
         const int off = zs ? F.OZ + (c == 0) * F.FZS + iy[b] * F.LX + ix[a]
-                           : F.OY + (b == 0) * F.FYS + iz[c] * F.LX + ix[a];
+                           : F.OY + (b == 0) * F.FYS + (ix[a] == 0 ? 0 : F.p + 1) + iz[c];
         s += F.bbuf[brick * F.FB + off];
       }
   const long long l = I + (long long)F.Nx * (J + (long long)F.Ny * K);
@@ -403,7 +403,7 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
   F.p = p; F.PX = p * L.BX; F.PY = p * L.BY; F.PZU = p * zc;
   F.LX = F.PX + 1; F.LY = F.PY + 1;
   F.nbx = nbx; F.nby = nby; F.nzl = m->nzl; F.bc = op->bc;
-  F.FYS = (p + 1) * F.LX; F.OY = 0; F.OZ = 2 * F.FYS;
+  F.FYS = 2 * (p + 1); F.OY = 0; F.OZ = 2 * F.FYS;  // FaceLayout<>
   F.FZS = F.LX * F.LY; F.FB = F.OZ + 2 * F.FZS;
   if (F.FB != L.face_block) {
     set_error("fused apply: face-block layout mismatch (%d vs %d)", F.FB, L.face_block);

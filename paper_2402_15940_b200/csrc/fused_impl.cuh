@@ -56,6 +56,25 @@
 #ifndef HOFEM_SIMT_EO
 #define HOFEM_SIMT_EO 1  // SIMT: even-odd (symmetry-halved) 1D contractions
 #endif
+#ifndef HOFEM_EO_DLA
+#define HOFEM_EO_DLA 0  // SIMT-EO stage 3: point pairs of D loads in flight (0: per p)
+#endif
+#ifndef HOFEM_EO_PRE
+#define HOFEM_EO_PRE -1  // SIMT-EO: stage-3 D loads of the first round issued before stage 2
+                          // (1: into registers, 2: L1 prefetch, 0: no, -1: per p)
+#endif
+#ifndef HOFEM_EO_ZO
+#define HOFEM_EO_ZO 1  // table offsets through a loop-variant zero (no hoisting)
+#endif
+#ifndef HOFEM_L2PF_AHEAD
+#define HOFEM_L2PF_AHEAD 1  // SIMT: qdata L2 bulk prefetch this many bricks ahead
+#endif
+#ifndef HOFEM_EO_DPOL
+#define HOFEM_EO_DPOL -1  // SIMT-EO: L2 policy of the stage-3 D loads (see ld_dp; -1 per p)
+#endif
+#ifndef HOFEM_L2PF_POL
+#define HOFEM_L2PF_POL 0  // 1: the qdata L2 prefetch marks its lines evict_last
+#endif
 #ifndef HOFEM_APF
 #define HOFEM_APF 0  // 1: stage 3 loads the next tile's A fragments before this tile's MMAs
 #endif
@@ -287,11 +306,13 @@ template <int p, int LX, int LY>
 struct FaceLayout {
   static constexpr int P1 = p + 1;
   static constexpr int OY = 0;                  // y faces
-  static constexpr int FYS = P1 * LX;
+  // a y face only ever holds its two x-end columns (the z lines of the brick
+  // grid): [ys][x end][k], k fastest, so the fix-up reads a z line contiguously
+  static constexpr int FYS = 2 * P1;
   static constexpr int OZ = OY + 2 * FYS;       // z faces
   static constexpr int FZS = LX * LY;
   static constexpr int FB = OZ + 2 * FZS;       // doubles per brick
-  __device__ __forceinline__ static int yf(int ys, int k) { return OY + ys * FYS + k * LX; }
+  __device__ __forceinline__ static int yf(int ys, int k) { return OY + ys * FYS + k; }
   __device__ __forceinline__ static int zf(int zs, int j) { return OZ + zs * FZS + j * LX; }
 };
 
@@ -305,7 +326,7 @@ struct EpiRow {
   double* bb;   // shared-face row (z-unit or y face) in the brick's face block
   long long gl;
   int base0, base1;  // y-element offsets of the lower / primary contributions
-  bool vy0, vy1, to_carry, from_carry, row_sh, row_multi, row_ess;
+  bool vy0, vy1, to_carry, from_carry, row_sh, row_multi, row_ess, yface;
   // fused x.y (CG's pAp): lattice row of x, owned row (Dirichlet terms), lower side of the
   // row's shared y/z face (a Dirichlet point on one shared face is written by
   // both bricks and counted by the lower one only)
@@ -361,7 +382,7 @@ __device__ __forceinline__ void epi_segment(const ColArgs& A, const double* RA, 
       if (i >= nv) continue;
       const bool lo = (SX == 0 && ii == 0), hi = (SX == BX - 1 && ii == p);
       if (R.row_multi || (lo && xlo_sh) || (hi && xhi_sh)) {
-        R.bb[i] = v[ii];  // edge line: partial buffer
+        R.bb[R.yface ? (i == 0 ? 0 : p + 1) : i] = v[ii];  // edge line: partial buffer
       } else if (R.row_ess || (lo && xlo_ess) || i == ie) {
         const double xv = A.x[R.gl + i];
         A.y[R.gl + i] = xv;
@@ -462,6 +483,7 @@ __device__ __forceinline__ void brick_epilogue(const ColArgs& A, const double* R
       using FL = FaceLayout<p, LX, LY>;
       double* fb = A.bbuf + brick * FL::FB;
       R.bb = zsh ? fb + FL::zf(k == 0 ? 0 : 1, j) : fb + FL::yf(j == 0 ? 0 : 1, k);
+      R.yface = !zsh;
     }
     R.cin = carry_in + LX * j;
     R.cout = carry_out + LX * j;
@@ -631,9 +653,17 @@ __device__ __forceinline__ void prefetch_qdata_l2(const ColArgs& A, const Brick&
     if (ex < A.nx && ey < A.ny) {
       const long long e = ex + (long long)A.nx * (ey + (long long)A.ny * b.ez);
       const long long lo = (e * per) & ~15LL, hi = ((e + 1) * per + 15) & ~15LL;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + lo),
-                   "r"((unsigned)(hi - lo))
-                   : "memory");
+      if (HOFEM_L2PF_POL) {
+        unsigned long long pol;
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(base + lo),
+                     "r"((unsigned)(hi - lo)), "l"(pol)
+                     : "memory");
+      } else {
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + lo),
+                     "r"((unsigned)(hi - lo))
+                     : "memory");
+      }
     }
   }
 }
@@ -1154,6 +1184,30 @@ __device__ __forceinline__ double ld_d(const double* ptr) {
   else
     return ld_nc_v(ptr);
 }
+// stage-3 D load with an L2 policy (HOFEM_EO_DPOL: 1 = evict_first hint,
+// 2 = evict_first + no L1 allocation; 0 = plain ld_d)
+// measured (gpurun_out/e7): evict_first + no L1 allocation is 6 % faster at p = 6,
+// slower at p = 4, 5
+template <int P1>
+constexpr int eo_dpol() {
+  return HOFEM_EO_DPOL >= 0 ? HOFEM_EO_DPOL : (P1 == 7 ? 2 : 0);
+}
+template <bool SMEM, int DPOL>
+__device__ __forceinline__ double ld_dp(const double* ptr, unsigned long long pol) {
+  if constexpr (SMEM || DPOL == 0) {
+    (void)pol;
+    return ld_d<SMEM>(ptr);
+  } else {
+    double v;
+    if (DPOL == 1)
+      asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(ptr), "l"(pol));
+    else
+      asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                   : "=d"(v)
+                   : "l"(ptr), "l"(pol));
+    return v;
+  }
+}
 
 template <int KIND, int P1, int Q, int BX, int BY>
 struct CfgS {
@@ -1180,7 +1234,7 @@ struct CfgS {
   // D staged in shared memory (one buffer, bulk-copied one brick ahead) or
   // loaded from L2 into registers inside stage 3.
   static constexpr bool DSM =
-      HOFEM_SIMT_DSMEM >= 0 ? HOFEM_SIMT_DSMEM != 0 : (P1 == 6 || P1 == 9);  // measured
+      HOFEM_SIMT_DSMEM >= 0 ? HOFEM_SIMT_DSMEM != 0 : (P1 == 9);  // measured
   static constexpr int QOFF = TOFF + 2 * Q * PR;  // even => 16-byte aligned
   static constexpr int QSLOT = ((NC * Q * Q * Q + 2) + 1) / 2 * 2;
   static constexpr int SMEM_DOUBLES = QOFF + (DSM ? NE * QSLOT : 0);
@@ -1308,6 +1362,19 @@ __device__ __forceinline__ void zero(double (&v)[N]) {
   for (int i = 0; i < N; ++i) v[i] = 0.0;
 }
 
+// D of the point pair t of a z line (qz = t and Q-1-t; the middle point alone)
+template <bool SMEM, int NCD, int Q, int DPOL>
+__device__ __forceinline__ void eo_ldpair(const double* qde, int t, double (&d)[2][NCD],
+                                          unsigned long long pol) {
+  constexpr int Q2 = Q * Q, Q3 = Q * Q * Q;
+  const bool mid = (Q & 1) && t == Q / 2;
+#pragma unroll
+  for (int m = 0; m < NCD; ++m) {
+    d[0][m] = ld_dp<SMEM, DPOL>(qde + m * Q3 + t * Q2, pol);
+    d[1][m] = mid ? 0.0 : ld_dp<SMEM, DPOL>(qde + m * Q3 + (Q - 1 - t) * Q2, pol);
+  }
+}
+
 // measured: constant-bank tables win at p = 4, 6, 7; shared-memory rows elsewhere
 template <int P1>
 constexpr bool simt_cb() {
@@ -1329,6 +1396,16 @@ __global__ void __maxnreg__(MAXR)
   constexpr int Q2 = Q * Q, Q3 = Q * Q * Q;
   constexpr int H = (P + 1) / 2, PH = P / 2, QH = Q / 2;  // even-odd sizes (EO)
   (void)H; (void)PH; (void)QH;
+  // EO stage 3: D of LA point pairs in flight; EOPRE: the first round's are
+  // issued before stage 2 (registers live across S2 and the barrier)
+  constexpr int HQ = (Q + 1) / 2, NCD = KIND == KIND_MASS ? 1 : 6;
+  // measured (gpurun_out/e4, e5, e8): register hoist helps at p = 6, 7 (3-4 %), costs
+  // at p = 4, 5 (register cap 128); deeper rings and L1 prefetch do not help
+  constexpr int LA0 = HOFEM_EO_DLA > 0 ? HOFEM_EO_DLA : 1;
+  constexpr int LA = LA0 < HQ ? LA0 : HQ;
+  constexpr int PRE = HOFEM_EO_PRE >= 0 ? HOFEM_EO_PRE : (P1 == 7 || P1 == 8 ? 1 : 0);
+  constexpr bool EOPRE = EO && !C::DSM && PRE == 1;
+  constexpr bool EOPF1 = EO && !C::DSM && PRE == 2;  // L1 prefetch instead
   // COLLOC (BP5): GLL points = nodes, so B = I; every B contraction is the
   // identity and is skipped (diffusion structure otherwise).
   constexpr bool COL = KIND == KIND_COLLOC;
@@ -1360,10 +1437,12 @@ __global__ void __maxnreg__(MAXR)
     if (A.dotp && threadIdx.x == 0) A.dotp[blockIdx.x] = 0.0;
     return;
   }
-  if (C::DSM)
+  if (C::DSM) {
     issue_qdata<C, BX, BY>(A, cur, QS, &qbar);
-  else
+  } else {
     prefetch_qdata_l2<C, BX, BY>(A, cur);
+    if (HOFEM_L2PF_AHEAD > 1) prefetch_qdata_l2<C, BX, BY>(A, brick_next(A, cur));
+  }
   issue_lattice<C, NT, BX>(A, LB, (long long)p * cur.bx * BX, (long long)p * cur.by * BY,
                            (long long)p * cur.ez);
   cp_async_wait_all();
@@ -1371,9 +1450,16 @@ __global__ void __maxnreg__(MAXR)
   unsigned qphase = 0;
 
   double dsum = 0.0;  // this thread's share of x.y (A.dotp)
+  constexpr int DPOL = eo_dpol<P1>();
+  unsigned long long dpol = 0;
+  if (DPOL) dpol = evict_first_policy();
   for (int kb = 0; cur.u < A.nunits; ++kb) {
     const int tid = vtid();
+#if HOFEM_EO_ZO
     const int zo = cur.ez >> 30;  // == 0, loop-variant (see cb_row)
+#else
+    constexpr int zo = 0;  // EO tables: direct constant-bank operands
+#endif
     (void)zo;
     const Brick nxt = brick_next(A, cur);
     const int ex0 = cur.bx * BX, ey0 = cur.by * BY, ez = cur.ez;
@@ -1381,7 +1467,10 @@ __global__ void __maxnreg__(MAXR)
     if (nxt.u < A.nunits) {
       issue_lattice<C, NT, BX>(A, LB + ((kb + 1) & 1) * C::LAT, (long long)p * nxt.bx * BX,
                                (long long)p * nxt.by * BY, (long long)p * nxt.ez);
-      prefetch_qdata_l2<C, BX, BY>(A, nxt);
+      if (HOFEM_L2PF_AHEAD > 1)
+        prefetch_qdata_l2<C, BX, BY>(A, brick_next(A, nxt));
+      else
+        prefetch_qdata_l2<C, BX, BY>(A, nxt);
     }
 
     // ---- S1: contract x.  item (el, b, c), c fastest.
@@ -1435,6 +1524,38 @@ __global__ void __maxnreg__(MAXR)
     }
     cta_sync();
 
+    double dpre[LA][2][NCD];
+    if constexpr (EOPF1) {
+      // the first LA point pairs of this thread's stage-3 item into L1
+      if (tid < NE * Q2) {
+        const int el = tid / Q2, pt = tid % Q2;
+        const int ex = ex0 + el % BX, ey = ey0 + el / BX;
+        if (ex < A.nx && ey < A.ny) {
+          const double* qde = A.qd + (ex + (long long)A.nx * (ey + (long long)A.ny * ez)) *
+                                         (long long)(C::NC * Q3) + pt;
+#pragma unroll
+          for (int k = 0; k < LA; ++k)
+#pragma unroll
+            for (int m = 0; m < NCD; ++m) {
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(qde + m * Q3 + k * Q2));
+              if (!((Q & 1) && k == QH))
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(qde + m * Q3 + (Q - 1 - k) * Q2));
+            }
+        }
+      }
+    }
+    if constexpr (EOPRE) {
+      if (tid < NE * Q2) {
+        const int el = tid / Q2, pt = tid % Q2;
+        const int ex = ex0 + el % BX, ey = ey0 + el / BX;
+        if (ex < A.nx && ey < A.ny) {
+          const double* qde = A.qd + (ex + (long long)A.nx * (ey + (long long)A.ny * ez)) *
+                                         (long long)(C::NC * Q3) + pt;
+#pragma unroll
+          for (int k = 0; k < LA; ++k) eo_ldpair<false, NCD, Q, DPOL>(qde, k, dpre[k], dpol);
+        }
+      }
+    }
     // ---- S2: contract y.  item (el, qx, c), c fastest.
     FOR_ITEMS(it, NE * Q * P, NT, tid) {
       const int el = it / (Q * P), r = it % (Q * P), qx = r / P, c = r % P;
@@ -1534,13 +1655,18 @@ __global__ void __maxnreg__(MAXR)
       if constexpr (EO) {
         // pairs (qz = t, Q-1-t), then the middle point (odd Q); the next pair's
         // D values are loaded while this pair computes
-        constexpr int HQ = (Q + 1) / 2;
-        constexpr int NCD = DIFF ? 6 : 1;
-        double dl[NCD], dh[NCD];
+        double dr[LA][2][NCD];
+        if (EOPRE && it_base == 0) {
 #pragma unroll
-        for (int m = 0; m < NCD; ++m) {
-          dl[m] = ld_d<C::DSM>(qde + m * Q3);
-          dh[m] = (HQ > 1 || !(Q & 1)) ? ld_d<C::DSM>(qde + m * Q3 + (Q - 1) * Q2) : 0.0;
+          for (int k = 0; k < LA; ++k)
+#pragma unroll
+            for (int m = 0; m < NCD; ++m) {
+              dr[k][0][m] = dpre[k][0][m];
+              dr[k][1][m] = dpre[k][1][m];
+            }
+        } else {
+#pragma unroll
+          for (int k = 0; k < LA; ++k) eo_ldpair<C::DSM, NCD, Q, DPOL>(qde, k, dr[k], dpol);
         }
         if (DIFF) {
           double g0[P], g1[P], g2[P];
@@ -1561,15 +1687,13 @@ __global__ void __maxnreg__(MAXR)
 #pragma unroll
           for (int t = 0; t < HQ; ++t) {
             const bool mid = (Q & 1) && t == QH;
-            double nl[6], nh[6];
-            if (t + 1 < HQ) {
-              const bool nmid = (Q & 1) && t + 1 == QH;
+            double dl[NCD], dh[NCD];
 #pragma unroll
-              for (int m = 0; m < 6; ++m) {
-                nl[m] = ld_d<C::DSM>(qde + m * Q3 + (t + 1) * Q2);
-                nh[m] = nmid ? 0.0 : ld_d<C::DSM>(qde + m * Q3 + (Q - 2 - t) * Q2);
-              }
+            for (int m = 0; m < NCD; ++m) {
+              dl[m] = dr[t % LA][0][m];
+              dh[m] = dr[t % LA][1][m];
             }
+            if (t + LA < HQ) eo_ldpair<C::DSM, NCD, Q, DPOL>(qde, t + LA, dr[t % LA], dpol);
             double u0l, u0h = 0.0, u1l, u1h = 0.0, u2l, u2h = 0.0;
             if (mid) {
               u0l = COL ? g0[t] : eo_fwd_mid<1, P>(T.BE, T.BO, t, zo, e0, o0);
@@ -1610,10 +1734,6 @@ __global__ void __maxnreg__(MAXR)
               }
               eo_acc<-1, P>(T.GE, T.GO, t, zo, w2l, w2h, SE2, SO2);
             }
-            if (t + 1 < HQ) {
-#pragma unroll
-              for (int m = 0; m < 6; ++m) { dl[m] = nl[m]; dh[m] = nh[m]; }
-            }
           }
           double s[P];
           if (!COL) {
@@ -1637,11 +1757,8 @@ __global__ void __maxnreg__(MAXR)
 #pragma unroll
           for (int t = 0; t < HQ; ++t) {
             const bool mid = (Q & 1) && t == QH;
-            double nl = 0.0, nh = 0.0;
-            if (t + 1 < HQ) {
-              nl = ld_d<C::DSM>(qde + (t + 1) * Q2);
-              nh = ((Q & 1) && t + 1 == QH) ? 0.0 : ld_d<C::DSM>(qde + (Q - 2 - t) * Q2);
-            }
+            double dl[1] = {dr[t % LA][0][0]}, dh[1] = {dr[t % LA][1][0]};
+            if (t + LA < HQ) eo_ldpair<C::DSM, NCD, Q, DPOL>(qde, t + LA, dr[t % LA], dpol);
             if (mid) {
               const double u = eo_fwd_mid<1, P>(T.BE, T.BO, t, zo, e, o);
               eo_acc_mid<1, P>(T.BE, T.BO, t, zo, dl[0] * u, SE, SO);
@@ -1650,8 +1767,6 @@ __global__ void __maxnreg__(MAXR)
               eo_fwd<1, P>(T.BE, T.BO, t, zo, e, o, ul, uh);
               eo_acc<1, P>(T.BE, T.BO, t, zo, dl[0] * ul, dh[0] * uh, SE, SO);
             }
-            dl[0] = nl;
-            dh[0] = nh;
           }
           double s[P];
           eo_join<P>(SE, SO, s);
@@ -1921,11 +2036,11 @@ struct ShapeSD;
 //                                     BX BY  NT  MAXR  CTAs/SM
 template <> struct ShapeSD<2> { static constexpr int BX = 4, BY = 4, NT = 160, MAXR = 96, CPS = 4; };
 template <> struct ShapeSD<3> { static constexpr int BX = 4, BY = 2, NT = 128, MAXR = 128, CPS = 4; };
-template <> struct ShapeSD<4> { static constexpr int BX = 2, BY = 2, NT = 128, MAXR = 144, CPS = 3; };
+template <> struct ShapeSD<4> { static constexpr int BX = 3, BY = 2, NT = 160, MAXR = 102, CPS = 4; };
 template <> struct ShapeSD<5> { static constexpr int BX = 2, BY = 2, NT = 160, MAXR = 128, CPS = 3; };
-template <> struct ShapeSD<6> { static constexpr int BX = 2, BY = 1, NT = 128, MAXR = 168, CPS = 3; };
+template <> struct ShapeSD<6> { static constexpr int BX = 1, BY = 2, NT = 128, MAXR = 128, CPS = 4; };
 template <> struct ShapeSD<7> { static constexpr int BX = 1, BY = 1, NT = 64, MAXR = 168, CPS = 6; };
-template <> struct ShapeSD<8> { static constexpr int BX = 2, BY = 1, NT = 192, MAXR = 168, CPS = 2; };
+template <> struct ShapeSD<8> { static constexpr int BX = 1, BY = 1, NT = 96, MAXR = 168, CPS = 4; };
 template <> struct ShapeSD<9> { static constexpr int BX = 1, BY = 1, NT = 128, MAXR = 232, CPS = 2; };
 
 // Tuning override (scripts/build_variant.py): -DHOFEM_SS_P1=6 -DHOFEM_SS_BX=2
@@ -1946,6 +2061,7 @@ struct ShapeS : ShapeSD<P1> {};
 template <int P1>
 struct ShapeSCD : ShapeS<P1> {};
 //                                      BX BY  NT  MAXR  CTAs/SM  (measured, BP5)
+template <> struct ShapeSCD<4> { static constexpr int BX = 2, BY = 2, NT = 128, MAXR = 144, CPS = 3; };
 template <> struct ShapeSCD<6> { static constexpr int BX = 2, BY = 2, NT = 160, MAXR = 128, CPS = 3; };
 template <> struct ShapeSCD<8> { static constexpr int BX = 2, BY = 1, NT = 128, MAXR = 168, CPS = 3; };
 // Tuning override: -DHOFEM_SC_P1=6 -DHOFEM_SC_BX=.. (same fields as HOFEM_SS_*).

@@ -48,8 +48,10 @@ def main(tag):
                 v = float(r[i].replace(",", ""))
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units[i], 1)
             b = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
-            if name.startswith("fused_bp3p"):
-                p = int(name[len("fused_bp3p"):])
+            import re
+            m = re.match(r"(?:fused_bp3p|simt_p|mma_p)(\d+)$", name)
+            if m:
+                p = int(m.group(1))
                 n = int(round(311.0 / p))
                 traffic[f"bp3_p{p}_n{n}"] = {"dram_bytes": b, "kernel": kn[:80],
                                              "source": f"profiles/{tag}_{name}_raw.csv"}
