@@ -81,20 +81,26 @@ __device__ __forceinline__ int axis_bricks_z(int K, int p, int nzl, bool split, 
 // skipping y planes), 2 y-z lines (along x, skipping x planes).  Each point sums
 // its partials in ascending brick order (deterministic).  Points on a single
 // plane were completed in the fused kernel by two-term reductions.
-__device__ __forceinline__ double fixup_point(const FixArgs& F);
+__device__ __forceinline__ double fixup_point(const FixArgs& F, int type, int line, int r);
+// Flat launch: thread g enumerates the edge points type by type (n0 x-y line
+// points, then n1 x-z, then n2 y-z), so no thread idles on a short line type.
 __global__ void __launch_bounds__(256) fixup_kernel(FixArgs F) {
   __shared__ double red[256];
-  double d = fixup_point(F);
-  if (F.dotp) {
-    const unsigned b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    block_sum_store(d, F.dotp + b, red);
-  }
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long n0 = (long long)F.nplX * F.nplY * F.Nzl, n1 = (long long)F.nplX * F.nplZ * F.Ny,
+                  n2 = (long long)F.nplY * F.nplZ * F.Nx;
+  double d = 0.0;
+  if (g < n0)
+    d = fixup_point(F, 0, (int)(g / F.Nzl), (int)(g % F.Nzl));
+  else if (g < n0 + n1)
+    d = fixup_point(F, 1, (int)((g - n0) / F.Ny), (int)((g - n0) % F.Ny));
+  else if (g < n0 + n1 + n2)
+    d = fixup_point(F, 2, (int)((g - n0 - n1) / F.Nx), (int)((g - n0 - n1) % F.Nx));
+  if (F.dotp) block_sum_store(d, F.dotp + blockIdx.x, red);
 }
 
 // One edge-line point (see fixup_kernel); returns its x.y term (0 if none).
-__device__ __forceinline__ double fixup_point(const FixArgs& F) {
-  const int type = blockIdx.z, line = blockIdx.y;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ double fixup_point(const FixArgs& F, int type, int line, int r) {
   int I, J, K;
   if (type == 0) {
     if (line >= F.nplX * F.nplY || r >= F.Nzl) return 0.0;
@@ -351,10 +357,12 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
   A.l2pf = l2pf;
   // fused x.y: per-CTA partials of the brick kernel, then one per fix-up block
   const bool fdot = dot_out != nullptr && PL.variant != 2;
-  const int gfx = (int)((std::max((int)m->Nzl, std::max((int)m->Ny, (int)m->Nx)) + 255) / 256);
+  const long long nfixp = (long long)(nbx - 1) * (nby - 1) * m->Nzl +
+                          (long long)(nbx - 1) * (nchunks - 1) * m->Ny +
+                          (long long)(nby - 1) * (nchunks - 1) * m->Nx;
   const int nlines0 = std::max((nbx - 1) * (nby - 1),
                                std::max((nbx - 1) * (nchunks - 1), (nby - 1) * (nchunks - 1)));
-  const long long nfixb = nlines0 > 0 ? (long long)gfx * nlines0 * 3 : 0;
+  const long long nfixb = nlines0 > 0 ? (nfixp + 255) / 256 : 0;
   if (fdot && op->dotp_len < grid + nfixb) {
     if (op->d_dotp) cudaFree(op->d_dotp);
     op->d_dotp = nullptr;
@@ -413,15 +421,12 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
   F.dotp = fdot ? op->d_dotp + grid : nullptr;
   F.kown = (int)A.kown;
   const int nlines = std::max(F.nplX * F.nplY, std::max(F.nplX * F.nplZ, F.nplY * F.nplZ));
-  const int llen = std::max(F.Nzl, std::max(F.Ny, F.Nx));
   if (nlines > 0) {
     if (g_prof.on) {
       ev = {prof_event(), prof_event()};
       cudaEventRecord(ev.first, s);
     }
-    const dim3 fg((unsigned)gfx, (unsigned)nlines, 3);
-    (void)llen;
-    fixup_kernel<<<fg, 256, 0, s>>>(F);
+    fixup_kernel<<<(unsigned)nfixb, 256, 0, s>>>(F);
     HOFEM_LAUNCHED();
     if (g_prof.on) {
       cudaEventRecord(ev.second, s);

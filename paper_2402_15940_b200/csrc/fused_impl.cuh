@@ -2061,9 +2061,13 @@ struct ShapeS : ShapeSD<P1> {};
 template <int P1>
 struct ShapeSCD : ShapeS<P1> {};
 //                                      BX BY  NT  MAXR  CTAs/SM  (measured, BP5)
+// collocated (BP5) shapes, measured (gpurun_out/e10)
 template <> struct ShapeSCD<4> { static constexpr int BX = 2, BY = 2, NT = 128, MAXR = 144, CPS = 3; };
+template <> struct ShapeSCD<5> { static constexpr int BX = 3, BY = 2, NT = 160, MAXR = 102, CPS = 4; };
 template <> struct ShapeSCD<6> { static constexpr int BX = 2, BY = 2, NT = 160, MAXR = 128, CPS = 3; };
-template <> struct ShapeSCD<8> { static constexpr int BX = 2, BY = 1, NT = 128, MAXR = 168, CPS = 3; };
+template <> struct ShapeSCD<7> { static constexpr int BX = 2, BY = 1, NT = 128, MAXR = 128, CPS = 4; };
+template <> struct ShapeSCD<8> { static constexpr int BX = 2, BY = 1, NT = 128, MAXR = 128, CPS = 4; };
+template <> struct ShapeSCD<9> { static constexpr int BX = 1, BY = 1, NT = 96, MAXR = 128, CPS = 5; };
 // Tuning override: -DHOFEM_SC_P1=6 -DHOFEM_SC_BX=.. (same fields as HOFEM_SS_*).
 #ifdef HOFEM_SC_P1
 struct ShapeSCOverride {
