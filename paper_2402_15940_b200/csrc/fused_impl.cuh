@@ -42,7 +42,7 @@
 #define HOFEM_DEARLY 0  // 1: tile-0 D values loaded at brick start; 0: at stage-3 start
 #endif
 #ifndef HOFEM_DBG_SKIP
-#define HOFEM_DBG_SKIP 0  // timing ablation only (wrong results): 1 epilogue, 2 D loads, 4 DMMAs
+#define HOFEM_DBG_SKIP 0  // timing ablation only (wrong results): 1 epilogue, 2 D loads, 4 DMMAs, 8 face reductions
 #endif
 #ifndef HOFEM_SIMT_DSMEM
 #define HOFEM_SIMT_DSMEM -1  // SIMT: D staged in smem (1), from L2 in registers (0), per p (-1)
@@ -317,7 +317,10 @@ struct FaceLayout {
 };
 
 __device__ __forceinline__ void red_add(double* p, double v) {
-  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+  if (HOFEM_DBG_SKIP & 8)
+    *p = v;  // timing ablation only (wrong results): face points stored, not reduced
+  else
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
 struct EpiRow {
@@ -2080,8 +2083,26 @@ struct ShapeSC : std::conditional_t<P1 == HOFEM_SC_P1, ShapeSCOverride, ShapeSCD
 template <int P1>
 struct ShapeSC : ShapeSCD<P1> {};
 #endif
+// mass (BP1) shapes: the diffusion ones unless measured otherwise
+template <int P1>
+struct ShapeSMD : ShapeS<P1> {};
+// measured (BP1 at ~1M dofs, whole apply incl. memset and fix-up; gpurun_out/e12,
+// f5): single-element bricks pay off at p = 8 only (more edge lines elsewhere)
+template <> struct ShapeSMD<9> { static constexpr int BX = 1, BY = 1, NT = 128, MAXR = 96, CPS = 5; };
+#ifdef HOFEM_SM_P1
+struct ShapeSMOverride {
+  static constexpr int BX = HOFEM_SM_BX, BY = HOFEM_SM_BY, NT = HOFEM_SM_NT,
+                       MAXR = HOFEM_SM_MAXR, CPS = HOFEM_SM_CPS;
+};
+template <int P1>
+struct ShapeSM : std::conditional_t<P1 == HOFEM_SM_P1, ShapeSMOverride, ShapeSMD<P1>> {};
+#else
+template <int P1>
+struct ShapeSM : ShapeSMD<P1> {};
+#endif
 template <int KIND, int P1>
-using ShapeSK = std::conditional_t<KIND == KIND_COLLOC, ShapeSC<P1>, ShapeS<P1>>;
+using ShapeSK = std::conditional_t<KIND == KIND_COLLOC, ShapeSC<P1>,
+                                   std::conditional_t<KIND == KIND_MASS, ShapeSM<P1>, ShapeS<P1>>>;
 
 // ---------------------------------------------------------------------------
 // Collocated diffusion kernel (BP5: GLL points = nodes, B1d = I, Q = P1).

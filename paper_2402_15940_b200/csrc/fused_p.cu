@@ -193,10 +193,14 @@ FusedLaunch fused_shape<HOFEM_P1>(int kind, int variant) {
     return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB, 1};
   }
   if (pick(variant, kind) == 1) {
+    if (kind == KIND_MASS) {
+      using S = ShapeSK<KIND_MASS, HOFEM_P1>;
+      return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB,
+                         simt_ctas_per_sm<KIND_MASS, HOFEM_P1, HOFEM_P1 + 1>()};
+    }
     using S = ShapeS<HOFEM_P1>;
-    const int cps = kind == KIND_MASS ? simt_ctas_per_sm<KIND_MASS, HOFEM_P1, HOFEM_P1 + 1>()
-                                      : simt_ctas_per_sm<KIND_DIFF, HOFEM_P1, HOFEM_P1 + 1>();
-    return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB, cps};
+    return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB,
+                       simt_ctas_per_sm<KIND_DIFF, HOFEM_P1, HOFEM_P1 + 1>()};
   }
   using S = ShapeE<HOFEM_P1>;
   const int cps = kind == KIND_MASS ? mma_ctas_per_sm<KIND_MASS, HOFEM_P1, HOFEM_P1 + 1>()

@@ -83,9 +83,11 @@ CASES = [
     # (nx, ny, nz, p, bench) -- several bricks, ragged tails (nx not a brick multiple)
     (2, 2, 2, 2, "bp3"),   # config 1
     (5, 3, 4, 1, "bp1"), (3, 5, 3, 2, "bp1"), (5, 3, 2, 3, "bp1"), (3, 3, 3, 5, "bp1"),
+    (3, 2, 2, 6, "bp1"), (2, 3, 2, 7, "bp1"), (2, 2, 3, 8, "bp1"),  # mass shapes (ShapeSMD)
     (9, 5, 3, 1, "bp3"), (5, 5, 3, 2, "bp3"), (5, 3, 3, 3, "bp3"), (3, 3, 3, 4, "bp3"),
     (3, 3, 3, 5, "bp3"), (3, 3, 2, 6, "bp3"), (3, 2, 2, 7, "bp3"), (3, 2, 2, 8, "bp3"),
     (5, 3, 3, 2, "bp5"), (3, 3, 3, 4, "bp5"), (3, 3, 2, 5, "bp5"), (3, 2, 2, 8, "bp5"),
+    (4, 3, 2, 3, "bp5"), (3, 2, 2, 6, "bp5"), (2, 3, 2, 7, "bp5"),  # collocated shapes
     (1, 1, 1, 1, "bp3"), (1, 1, 1, 5, "bp3"), (1, 1, 1, 4, "bp5"),
 ]
 
