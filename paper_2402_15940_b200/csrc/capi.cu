@@ -69,6 +69,7 @@ void free_op(Op* op) {
   cudaFree(op->d_B); cudaFree(op->d_G); cudaFree(op->d_qdata);
   cudaFree(op->d_ein); cudaFree(op->d_eout); cudaFree(op->d_bbuf);
   cudaFree(op->d_r); cudaFree(op->d_p); cudaFree(op->d_Ap); cudaFree(op->d_cg);
+  cudaFree(op->d_dotp); cudaFree(op->d_bar);
   delete op;
 }
 

@@ -27,119 +27,13 @@ HOFEM_FOR_P1(HOFEM_DECL)
 
 namespace {
 
-struct FixArgs {
-  const double* x;
-  double* y;
-  const double* bbuf;
-  long long K0, NzG;
-  int Nx, Ny, Nzl;
-  int p, PX, PY, PZU, LX, LY, nbx, nby, nzl, bc;
-  int FB, OY, OZ, FYS, FZS;  // FaceLayout<> of the launched kernel
-  int nplZ, nplY, nplX;      // interior brick-boundary planes per axis
-  double* dotp;              // non-null: one x.y partial per block (flat block index)
-  int kown;                  // local planes K < kown are owned
-};
-
-__device__ __forceinline__ bool on_plane(int I, int P, int N) {
-  return I % P == 0 && I > 0 && I < N - 1;
-}
-
-__device__ __forceinline__ int axis_bricks(int I, int P, int nb, int L, bool split, int* br,
-                                           int* loc) {
-  if (split) {
-    br[0] = I / P - 1; loc[0] = L - 1;
-    br[1] = I / P;     loc[1] = 0;
-    return 2;
-  }
-  int b = I / P;
-  if (b > nb - 1) b = nb - 1;
-  br[0] = b;
-  loc[0] = I - P * b;
-  return 1;
-}
-
-// z: bricks are single element layers; only work-unit boundary planes (every
-// PZU = p*zc lattice planes) are split between two bricks -- element faces
-// inside a unit were summed through the in-kernel carry into the upper brick.
-__device__ __forceinline__ int axis_bricks_z(int K, int p, int nzl, bool split, int* br,
-                                             int* loc) {
-  if (split) {
-    br[0] = K / p - 1; loc[0] = p;
-    br[1] = K / p;     loc[1] = 0;
-    return 2;
-  }
-  int b = K / p;
-  if (b > nzl - 1) b = nzl - 1;
-  br[0] = b;
-  loc[0] = K - p * b;
-  return 1;
-}
-
-// The edge lines of the brick grid: lattice points on two or three interior
-// brick-boundary planes (4 or 8 contributions).  grid (ceil(line length/256),
-// line count, 3): blockIdx.z = 0 x-y lines (along z), 1 x-z lines (along y,
-// skipping y planes), 2 y-z lines (along x, skipping x planes).  Each point sums
-// its partials in ascending brick order (deterministic).  Points on a single
-// plane were completed in the fused kernel by two-term reductions.
-__device__ __forceinline__ double fixup_point(const FixArgs& F, int type, int line, int r);
-// Flat launch: thread g enumerates the edge points type by type (n0 x-y line
-// points, then n1 x-z, then n2 y-z), so no thread idles on a short line type.
+// Edge-line fix-up as its own kernel (one thread per edge point, flat
+// enumeration: fixup_flat in fused_impl.cuh).
 __global__ void __launch_bounds__(256) fixup_kernel(FixArgs F) {
   __shared__ double red[256];
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long n0 = (long long)F.nplX * F.nplY * F.Nzl, n1 = (long long)F.nplX * F.nplZ * F.Ny,
-                  n2 = (long long)F.nplY * F.nplZ * F.Nx;
-  double d = 0.0;
-  if (g < n0)
-    d = fixup_point(F, 0, (int)(g / F.Nzl), (int)(g % F.Nzl));
-  else if (g < n0 + n1)
-    d = fixup_point(F, 1, (int)((g - n0) / F.Ny), (int)((g - n0) % F.Ny));
-  else if (g < n0 + n1 + n2)
-    d = fixup_point(F, 2, (int)((g - n0 - n1) / F.Nx), (int)((g - n0 - n1) % F.Nx));
+  const double d = g < fixup_count(F) ? fixup_flat(F, g) : 0.0;
   if (F.dotp) block_sum_store(d, F.dotp + blockIdx.x, red);
-}
-
-// One edge-line point (see fixup_kernel); returns its x.y term (0 if none).
-__device__ __forceinline__ double fixup_point(const FixArgs& F, int type, int line, int r) {
-  int I, J, K;
-  if (type == 0) {
-    if (line >= F.nplX * F.nplY || r >= F.Nzl) return 0.0;
-    I = (line % F.nplX + 1) * F.PX; J = (line / F.nplX + 1) * F.PY; K = r;
-  } else if (type == 1) {
-    if (line >= F.nplX * F.nplZ || r >= F.Ny) return 0.0;
-    I = (line % F.nplX + 1) * F.PX; K = (line / F.nplX + 1) * F.PZU; J = r;
-    if (on_plane(J, F.PY, F.Ny)) return 0.0;
-  } else {
-    if (line >= F.nplY * F.nplZ || r >= F.Nx) return 0.0;
-    J = (line % F.nplY + 1) * F.PY; K = (line / F.nplY + 1) * F.PZU; I = r;
-    if (on_plane(I, F.PX, F.Nx)) return 0.0;
-  }
-  const bool zs = on_plane(K, F.PZU, F.Nzl), ys = on_plane(J, F.PY, F.Ny),
-             xs = on_plane(I, F.PX, F.Nx);
-  int bx[2], ix[2], by[2], iy[2], bz[2], iz[2];
-  const int nbxl = axis_bricks(I, F.PX, F.nbx, F.LX, xs, bx, ix);
-  const int nbyl = axis_bricks(J, F.PY, F.nby, F.LY, ys, by, iy);
-  const int nbzl = axis_bricks_z(K, F.p, F.nzl, zs, bz, iz);
-  double s = 0.0;
-  for (int c = 0; c < nbzl; ++c)
-    for (int b = 0; b < nbyl; ++b)
-      for (int a = 0; a < nbxl; ++a) {
-        const long long brick = bx[a] + (long long)F.nbx * (by[b] + (long long)F.nby * bz[c]);
-        const int off = zs ? F.OZ + (c == 0) * F.FZS + iy[b] * F.LX + ix[a]
-                           : F.OY + (b == 0) * F.FYS + (ix[a] == 0 ? 0 : F.p + 1) + iz[c];
-        s += F.bbuf[brick * F.FB + off];
-      }
-  const long long l = I + (long long)F.Nx * (J + (long long)F.Ny * K);
-  const double xl = F.x[l];
-  if (F.bc) {
-    const long long Kg = K + F.K0;
-    if (I == 0 || I == F.Nx - 1 || J == 0 || J == F.Ny - 1 || Kg == 0 || Kg == F.NzG - 1) {
-      F.y[l] = xl;
-      return K < F.kown ? xl * xl : 0.0;  // Dirichlet value: counted by the owner
-    }
-  }
-  F.y[l] = s;
-  return xl * s;
 }
 
 // Sums the x.y partials of the fused kernel and the fix-up in index order.
@@ -376,6 +270,47 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
   }
   A.dotp = fdot ? op->d_dotp : nullptr;
   A.kown = m->n_owned / (m->Nx * m->Ny);
+  FixArgs F;
+  F.x = x; F.y = y; F.bbuf = op->d_bbuf;
+  F.Nx = (int)m->Nx; F.Ny = (int)m->Ny; F.Nzl = (int)m->Nzl; F.K0 = A.K0; F.NzG = m->NzG;
+  F.p = p; F.PX = p * L.BX; F.PY = p * L.BY; F.PZU = p * zc;
+  F.LX = F.PX + 1; F.LY = F.PY + 1;
+  F.nbx = nbx; F.nby = nby; F.nzl = m->nzl; F.bc = op->bc;
+  F.FYS = 2 * (p + 1); F.OY = 0; F.OZ = 2 * F.FYS;  // FaceLayout<>
+  F.FZS = F.LX * F.LY; F.FB = F.OZ + 2 * F.FZS;
+  if (F.FB != L.face_block) {
+    set_error("fused apply: face-block layout mismatch (%d vs %d)", F.FB, L.face_block);
+    return HOFEM_ERR_ARG;
+  }
+  F.nplZ = nchunks - 1; F.nplY = nby - 1; F.nplX = nbx - 1;
+  F.dotp = fdot ? op->d_dotp + grid : nullptr;
+  F.kown = (int)A.kown;
+  const int nlines = std::max(F.nplX * F.nplY, std::max(F.nplX * F.nplZ, F.nplY * F.nplZ));
+  // in-kernel fix-up (SIMT kernel; cooperative launch with a grid barrier)
+  static const int infix_env = [] {
+    // tuning knob: 0 = always the separate fixup_kernel, 2 = always in-kernel,
+    // 1 (default) = in-kernel for local meshes up to 8 Mi lattice points
+    const char* e = getenv("HOFEM_INFIX");
+    return e ? atoi(e) : 1;
+  }();
+  // measured (gpurun_out/e15, e16): pays for small (launch/latency-bound)
+  // problems, neutral or slower at ~30M dofs
+  const long long npts = m->Nx * m->Ny * m->Nzl;
+  const bool infix = (infix_env == 1 ? npts <= (8LL << 20) : infix_env == 2) &&
+                     PL.variant == 1 && nlines > 0 && grid <= nunits;
+  if (infix && !op->d_bar) {
+    if (cudaMalloc(&op->d_bar, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(op->d_bar, 0, sizeof(unsigned long long)) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("fused apply: out of device memory for the grid barrier");
+      return HOFEM_ERR_OOM;
+    }
+    op->bar_count = 0;
+  }
+  A.infix = infix ? 1 : 0;
+  A.bar = op->d_bar;
+  A.bar_target = infix ? op->bar_count + (unsigned long long)grid : 0;
+  A.fx = F;
   cudaError_t err = cudaSuccess;
   bool ok = false;
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
@@ -401,27 +336,12 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
   }
   count_launch();
   if (err != cudaSuccess) return cuda_status(err, "fused column kernel launch");
+  if (infix) op->bar_count += (unsigned long long)grid;  // every CTA arrives once
   if (g_prof.on) {
     cudaEventRecord(ev.second, s);
     g_prof.brick.push_back(ev);
   }
-  FixArgs F;
-  F.x = x; F.y = y; F.bbuf = op->d_bbuf;
-  F.Nx = (int)m->Nx; F.Ny = (int)m->Ny; F.Nzl = (int)m->Nzl; F.K0 = A.K0; F.NzG = m->NzG;
-  F.p = p; F.PX = p * L.BX; F.PY = p * L.BY; F.PZU = p * zc;
-  F.LX = F.PX + 1; F.LY = F.PY + 1;
-  F.nbx = nbx; F.nby = nby; F.nzl = m->nzl; F.bc = op->bc;
-  F.FYS = 2 * (p + 1); F.OY = 0; F.OZ = 2 * F.FYS;  // FaceLayout<>
-  F.FZS = F.LX * F.LY; F.FB = F.OZ + 2 * F.FZS;
-  if (F.FB != L.face_block) {
-    set_error("fused apply: face-block layout mismatch (%d vs %d)", F.FB, L.face_block);
-    return HOFEM_ERR_ARG;
-  }
-  F.nplZ = nchunks - 1; F.nplY = nby - 1; F.nplX = nbx - 1;
-  F.dotp = fdot ? op->d_dotp + grid : nullptr;
-  F.kown = (int)A.kown;
-  const int nlines = std::max(F.nplX * F.nplY, std::max(F.nplX * F.nplZ, F.nplY * F.nplZ));
-  if (nlines > 0) {
+  if (nlines > 0 && !infix) {
     if (g_prof.on) {
       ev = {prof_event(), prof_event()};
       cudaEventRecord(ev.first, s);
@@ -434,7 +354,8 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
     }
   }
   if (fdot) {
-    dot_partials_kernel<<<1, 256, 0, s>>>(op->d_dotp, grid + (nlines > 0 ? nfixb : 0), dot_out);
+    dot_partials_kernel<<<1, 256, 0, s>>>(op->d_dotp, grid + (nlines > 0 && !infix ? nfixb : 0),
+                                          dot_out);
     HOFEM_LAUNCHED();
   }
   HOFEM_TRY(exchange_planes(op, x, y, s));

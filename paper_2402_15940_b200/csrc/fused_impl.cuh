@@ -137,6 +137,118 @@ inline void fill_tab(Tab<P1, Q>& T, const double* B, const double* G) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Edge-line fix-up (a8): lattice points on two or three interior brick-boundary
+// planes (4 or 8 contributions) sum their partials in ascending brick order
+// (deterministic).  Points on a single plane were completed in the fused kernel
+// by two-term reductions.  Run either as fixup_kernel (fused.cu) after the
+// brick kernel or inside the SIMT kernel after a grid barrier (ColArgs::infix).
+// ---------------------------------------------------------------------------
+struct FixArgs {
+  const double* x;
+  double* y;
+  const double* bbuf;
+  long long K0, NzG;
+  int Nx, Ny, Nzl;
+  int p, PX, PY, PZU, LX, LY, nbx, nby, nzl, bc;
+  int FB, OY, OZ, FYS, FZS;  // FaceLayout<> of the launched kernel
+  int nplZ, nplY, nplX;      // interior brick-boundary planes per axis
+  double* dotp;              // non-null: one x.y partial per block (flat block index)
+  int kown;                  // local planes K < kown are owned
+};
+
+__device__ __forceinline__ bool on_plane(int I, int P, int N) {
+  return I % P == 0 && I > 0 && I < N - 1;
+}
+
+__device__ __forceinline__ int axis_bricks(int I, int P, int nb, int L, bool split, int* br,
+                                           int* loc) {
+  if (split) {
+    br[0] = I / P - 1; loc[0] = L - 1;
+    br[1] = I / P;     loc[1] = 0;
+    return 2;
+  }
+  int b = I / P;
+  if (b > nb - 1) b = nb - 1;
+  br[0] = b;
+  loc[0] = I - P * b;
+  return 1;
+}
+
+// z: bricks are single element layers; only work-unit boundary planes (every
+// PZU = p*zc lattice planes) are split between two bricks -- element faces
+// inside a unit were summed through the in-kernel carry into the upper brick.
+__device__ __forceinline__ int axis_bricks_z(int K, int p, int nzl, bool split, int* br,
+                                             int* loc) {
+  if (split) {
+    br[0] = K / p - 1; loc[0] = p;
+    br[1] = K / p;     loc[1] = 0;
+    return 2;
+  }
+  int b = K / p;
+  if (b > nzl - 1) b = nzl - 1;
+  br[0] = b;
+  loc[0] = K - p * b;
+  return 1;
+}
+
+// One edge-line point (see fixup_kernel); returns its x.y term (0 if none).
+__device__ __forceinline__ double fixup_point(const FixArgs& F, int type, int line, int r) {
+  int I, J, K;
+  if (type == 0) {
+    if (line >= F.nplX * F.nplY || r >= F.Nzl) return 0.0;
+    I = (line % F.nplX + 1) * F.PX; J = (line / F.nplX + 1) * F.PY; K = r;
+  } else if (type == 1) {
+    if (line >= F.nplX * F.nplZ || r >= F.Ny) return 0.0;
+    I = (line % F.nplX + 1) * F.PX; K = (line / F.nplX + 1) * F.PZU; J = r;
+    if (on_plane(J, F.PY, F.Ny)) return 0.0;
+  } else {
+    if (line >= F.nplY * F.nplZ || r >= F.Nx) return 0.0;
+    J = (line % F.nplY + 1) * F.PY; K = (line / F.nplY + 1) * F.PZU; I = r;
+    if (on_plane(I, F.PX, F.Nx)) return 0.0;
+  }
+  const bool zs = on_plane(K, F.PZU, F.Nzl), ys = on_plane(J, F.PY, F.Ny),
+             xs = on_plane(I, F.PX, F.Nx);
+  int bx[2], ix[2], by[2], iy[2], bz[2], iz[2];
+  const int nbxl = axis_bricks(I, F.PX, F.nbx, F.LX, xs, bx, ix);
+  const int nbyl = axis_bricks(J, F.PY, F.nby, F.LY, ys, by, iy);
+  const int nbzl = axis_bricks_z(K, F.p, F.nzl, zs, bz, iz);
+  double s = 0.0;
+  for (int c = 0; c < nbzl; ++c)
+    for (int b = 0; b < nbyl; ++b)
+      for (int a = 0; a < nbxl; ++a) {
+        const long long brick = bx[a] + (long long)F.nbx * (by[b] + (long long)F.nby * bz[c]);
+        const int off = zs ? F.OZ + (c == 0) * F.FZS + iy[b] * F.LX + ix[a]
+                           : F.OY + (b == 0) * F.FYS + (ix[a] == 0 ? 0 : F.p + 1) + iz[c];
+        s += __ldcg(F.bbuf + brick * F.FB + off);  // written by other CTAs
+      }
+  const long long l = I + (long long)F.Nx * (J + (long long)F.Ny * K);
+  const double xl = F.x[l];
+  if (F.bc) {
+    const long long Kg = K + F.K0;
+    if (I == 0 || I == F.Nx - 1 || J == 0 || J == F.Ny - 1 || Kg == 0 || Kg == F.NzG - 1) {
+      F.y[l] = xl;
+      return K < F.kown ? xl * xl : 0.0;  // Dirichlet value: counted by the owner
+    }
+  }
+  F.y[l] = s;
+  return xl * s;
+}
+
+
+// Flat enumeration of the edge points, type by type: n0 x-y line points (along
+// z), then n1 x-z (along y, skipping y planes), then n2 y-z (along x).
+__device__ __forceinline__ long long fixup_count(const FixArgs& F) {
+  return (long long)F.nplX * F.nplY * F.Nzl + (long long)F.nplX * F.nplZ * F.Ny +
+         (long long)F.nplY * F.nplZ * F.Nx;
+}
+__device__ __forceinline__ double fixup_flat(const FixArgs& F, long long g) {
+  const long long n0 = (long long)F.nplX * F.nplY * F.Nzl, n1 = (long long)F.nplX * F.nplZ * F.Ny;
+  if (g < n0) return fixup_point(F, 0, (int)(g / F.Nzl), (int)(g % F.Nzl));
+  if (g < n0 + n1) return fixup_point(F, 1, (int)((g - n0) / F.Ny), (int)((g - n0) % F.Ny));
+  return fixup_point(F, 2, (int)((g - n0 - n1) / F.Nx), (int)((g - n0 - n1) % F.Nx));
+}
+
 struct ColArgs {
   const double* x;
   double* y;
@@ -151,6 +263,12 @@ struct ColArgs {
   int l2pf;               // 1: bulk-prefetch the next brick's qdata into L2
   double* dotp;           // non-null: per-CTA partials of x.y over owned dofs (CG's pAp)
   long long kown;         // local planes K < kown are owned by this rank
+  // in-kernel fix-up (SIMT kernel, cooperative launch): after all bricks, a grid
+  // barrier, then the edge points of fx
+  int infix;
+  unsigned long long* bar;       // grid-barrier counter (monotonic)
+  unsigned long long bar_target; // its value once every CTA of this launch arrived
+  FixArgs fx;
 };
 
 // Fixed-order block sum; thread 0 stores it to *out.  All threads must call.
@@ -172,6 +290,29 @@ __device__ __forceinline__ void block_sum_store(double v, double* out, double* r
     for (int i = 0; i < 32 && i < (int)blockDim.x; ++i) s += red[i];
     *out = s;
   }
+}
+
+// Grid-wide barrier of a cooperative (co-resident) launch on a monotonic
+// 64-bit counter: every CTA adds 1 and waits for `target` (the host keeps the
+// running total of launched CTAs, so the counter is never reset).  Bounded
+// spin: a barrier that cannot complete traps (launch error) instead of
+// hanging the GPU.
+__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1ull);
+    unsigned long long v;
+    unsigned spins = 0;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
+      if (v >= target) break;
+      __nanosleep(100);
+    } while (++spins < (1u << 25));
+    if (v < target) __trap();
+    __threadfence();
+  }
+  __syncthreads();
 }
 
 enum { KIND_MASS = 0, KIND_DIFF = 1, KIND_COLLOC = 2 };
@@ -1436,7 +1577,7 @@ __global__ void __maxnreg__(MAXR)
   cta_sync();
 
   Brick cur = unit_first(A, blockIdx.x);
-  if (cur.u >= A.nunits) {
+  if (cur.u >= A.nunits) {  // never with infix: the host launches grid <= units
     if (A.dotp && threadIdx.x == 0) A.dotp[blockIdx.x] = 0.0;
     return;
   }
@@ -2027,6 +2168,14 @@ __global__ void __maxnreg__(MAXR)
     cp_async_wait_all();
     cta_sync();
     cur = nxt;
+  }
+  if (A.infix) {
+    // all bricks' partials and face reductions are in memory: the edge points
+    grid_barrier(A.bar, A.bar_target);
+    const long long nfx = fixup_count(A.fx);
+    for (long long g = (long long)blockIdx.x * NT + threadIdx.x; g < nfx;
+         g += (long long)gridDim.x * NT)
+      dsum += fixup_flat(A.fx, g);
   }
   if (A.dotp) block_sum_store(dsum, A.dotp + blockIdx.x, smem);
 }

@@ -63,8 +63,23 @@ cudaError_t launch_simt(const double* B, const double* G, const ColArgs& A, int 
   static bool attr_done = false;
   cudaError_t e = set_smem(kern, SMEM, &attr_done);
   if (e != cudaSuccess) return e;
-  kern<<<grid, S::NT, SMEM, s>>>(T, A);
-  return cudaPeekAtLastError();
+  if (!A.infix) {
+    kern<<<grid, S::NT, SMEM, s>>>(T, A);
+    return cudaPeekAtLastError();
+  }
+  // in-kernel fix-up behind a grid barrier: cooperative launch, so all CTAs
+  // are guaranteed co-resident (or the launch fails instead of deadlocking)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(S::NT);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, T, A);
 }
 
 // Resident CTAs per SM of a kernel (occupancy API; registers and shared memory

@@ -93,6 +93,8 @@ struct Op {
   int fused_variant = -1;   // -1: HOFEM_FUSED env / per-p default; 0 DMMA; 1 SIMT
   double* d_dotp = nullptr; // per-CTA partials of the fused x.y (CG)
   long long dotp_len = 0;
+  unsigned long long* d_bar = nullptr;  // grid-barrier counter of the in-kernel fix-up
+  unsigned long long bar_count = 0;     // CTAs launched against it so far
   // CG scratch
   double *d_r = nullptr, *d_p = nullptr, *d_Ap = nullptr;
   double* d_cg = nullptr;   // device CG scalars / history
