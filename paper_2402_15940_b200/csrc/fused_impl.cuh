@@ -75,6 +75,10 @@
 #ifndef HOFEM_L2PF_POL
 #define HOFEM_L2PF_POL 0  // 1: the qdata L2 prefetch marks its lines evict_last
 #endif
+#ifndef HOFEM_SIMT_ENDBAR
+#define HOFEM_SIMT_ENDBAR -1  // SIMT: 1 = barrier at the end of every brick, 0 = folded (see
+                               // kernel), -1 = per kind (measured, gpurun_out/e17)
+#endif
 #ifndef HOFEM_APF
 #define HOFEM_APF 0  // 1: stage 3 loads the next tile's A fragments before this tile's MMAs
 #endif
@@ -1554,6 +1558,8 @@ __global__ void __maxnreg__(MAXR)
   // identity and is skipped (diffusion structure otherwise).
   constexpr bool COL = KIND == KIND_COLLOC;
   constexpr bool DIFF = KIND == KIND_DIFF || COL;
+  // folded end-of-brick barrier: +1-2 % for BP1/BP3, -1.5 % for BP5
+  constexpr bool ENDBAR = HOFEM_SIMT_ENDBAR >= 0 ? HOFEM_SIMT_ENDBAR != 0 : COL;
   constexpr int EB = C::EB, S1 = C::S1, T1M = C::T1M, T1SZ = C::T1SZ, SP = C::SP,
                 T2M = C::T2M, PR = C::PR;
   extern __shared__ __align__(16) double smem[];
@@ -1609,8 +1615,9 @@ __global__ void __maxnreg__(MAXR)
     const int ex0 = cur.bx * BX, ey0 = cur.by * BY, ez = cur.ez;
     const double* L = LB + (kb & 1) * C::LAT;
     if (nxt.u < A.nunits) {
-      issue_lattice<C, NT, BX>(A, LB + ((kb + 1) & 1) * C::LAT, (long long)p * nxt.bx * BX,
-                               (long long)p * nxt.by * BY, (long long)p * nxt.ez);
+      if (ENDBAR)
+        issue_lattice<C, NT, BX>(A, LB + ((kb + 1) & 1) * C::LAT, (long long)p * nxt.bx * BX,
+                                 (long long)p * nxt.by * BY, (long long)p * nxt.ez);
       if (HOFEM_L2PF_AHEAD > 1)
         prefetch_qdata_l2<C, BX, BY>(A, brick_next(A, nxt));
       else
@@ -1667,6 +1674,11 @@ __global__ void __maxnreg__(MAXR)
       }
     }
     cta_sync();
+    // (no end-of-brick barrier) the previous brick's epilogue read the lattice
+    // buffer the next brick's copies target; every thread is past it here
+    if (!ENDBAR && nxt.u < A.nunits)
+      issue_lattice<C, NT, BX>(A, LB + ((kb + 1) & 1) * C::LAT, (long long)p * nxt.bx * BX,
+                               (long long)p * nxt.by * BY, (long long)p * nxt.ez);
 
     double dpre[LA][2][NCD];
     if constexpr (EOPF1) {
@@ -2163,10 +2175,19 @@ __global__ void __maxnreg__(MAXR)
       for (int a = 0; a < P; ++a) yo[C::SA * a] = ye[a];
     }
 
-    cta_sync();
-    simt_epilogue<C, NT, BX, BY>(A, smem, CY, cur, L, dsum);
-    cp_async_wait_all();
-    cta_sync();
+    if (ENDBAR) {
+      cta_sync();
+      simt_epilogue<C, NT, BX, BY>(A, smem, CY, cur, L, dsum);
+      cp_async_wait_all();
+      cta_sync();
+    } else {
+      // the next brick's lattice (issued after S1) lands before this barrier,
+      // which also publishes y_e to the epilogue; the next brick's first
+      // shared-memory writes (T1 in S1) do not touch what the epilogue reads
+      cp_async_wait_all();
+      cta_sync();
+      simt_epilogue<C, NT, BX, BY>(A, smem, CY, cur, L, dsum);
+    }
     cur = nxt;
   }
   if (A.infix) {
