@@ -130,6 +130,17 @@ def oracle_cg_sample(p, n, iters, warmup=0):
     return om.n_dofs * iters / (t3 - t2), t1 - t0, t3 - t2, om.n_dofs, O.num_threads()
 
 
+def arm_config(p, n, world):
+    """The workload both arms report (BASELINE configs[2] size, one n^3 slab per GPU)."""
+    Q = p + 2
+    n_global = (p * n + 1) ** 2 * (p * n * world + 1)
+    return {"workload": f"bp3_p{p}_{n}x{n}x{n}_per_gpu", "p": p, "q": Q,
+            "elements_per_gpu": n ** 3, "dofs_global": n_global,
+            "dofs_per_gpu": (p * n + 1) ** 3, "bc": "dirichlet", "mesh": "curvilinear alpha=0.1",
+            "parallelism": f"z-slab x{world} (NCCL plane exchange + allreduce)",
+            "l2": "inputs larger than L2 (qdata 3.9 GB/GPU, vectors 240 MB)"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -143,8 +154,9 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * cg_s / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": f"bp3_p{p}_oracle_sample_{n}^3",
-                                        "p": p, "elements": n ** 3, "dofs": dofs},
+        "data": "synthetic",
+        # the arm's workload; each step is the bounded oracle sample named in cpu_baseline
+        "config": arm_config(p, args.n or int(round(311.0 / p)), args.gpus),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -294,11 +306,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_cg / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"bp3_p{p}_{nx}x{ny}x{n}_per_gpu", "p": p, "q": Q,
-                       "elements_per_gpu": nx * ny * n, "dofs_global": n_global,
-                       "dofs_per_gpu": N_l, "bc": "dirichlet", "mesh": "curvilinear alpha=0.1",
-                       "parallelism": f"z-slab x{world} (NCCL plane exchange + allreduce)",
-                       "l2": "inputs larger than L2 (qdata 3.9 GB/GPU, vectors 240 MB)"},
+            "config": arm_config(p, n, world),
             "apply_gdof_s_per_gpu": N_l / t_apply / 1e9,
             "apply_ms": 1e3 * t_apply,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
