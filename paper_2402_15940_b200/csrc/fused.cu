@@ -164,6 +164,16 @@ void choose_chunks(long long ncol, int nzl, int G, int* zc_out, int* nchunks_out
   *nchunks_out = bn;
 }
 
+// Dirichlet points of the local slab (the fix-up's boundary pass; same count
+// as bnd_count in fused_impl.cuh)
+long long boundary_points(const Mesh* m) {
+  const long long K0 = (long long)m->p * m->z0;
+  const bool bot = K0 == 0, top = K0 + m->Nzl - 1 == m->NzG - 1;
+  const long long kz0 = bot ? 1 : 0, kz1 = m->Nzl - (top ? 1 : 0);
+  const long long nk = kz1 > kz0 ? kz1 - kz0 : 0;
+  return m->Nx * m->Ny * ((bot ? 1 : 0) + (top ? 1 : 0)) + 2 * m->Nx * nk + 2 * (m->Ny - 2) * nk;
+}
+
 namespace {
 struct Plan {
   int variant, kind;
@@ -211,7 +221,7 @@ hofem_status fused_info(const Op* op, hofem_fused_info* out) {
   const long long N = m->Nx * m->Ny * m->Nzl;
   const long long ax = P.nbx - 1, ay = P.nby - 1, az = P.nchunks - 1;
   out->fixup_points = ax * ay * m->Nzl + ax * az * m->Ny + ay * az * m->Nx - 2 * ax * ay * az;
-  out->direct_points = N - out->fixup_points;
+  out->direct_points = N - out->fixup_points;  // (Dirichlet points: boundary pass)
   return HOFEM_OK;
 }
 
@@ -251,12 +261,14 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
   A.l2pf = l2pf;
   // fused x.y: per-CTA partials of the brick kernel, then one per fix-up block
   const bool fdot = dot_out != nullptr && PL.variant != 2;
-  const long long nfixp = (long long)(nbx - 1) * (nby - 1) * m->Nzl +
-                          (long long)(nbx - 1) * (nchunks - 1) * m->Ny +
-                          (long long)(nby - 1) * (nchunks - 1) * m->Nx;
-  const int nlines0 = std::max((nbx - 1) * (nby - 1),
-                               std::max((nbx - 1) * (nchunks - 1), (nby - 1) * (nchunks - 1)));
-  const long long nfixb = nlines0 > 0 ? (nfixp + 255) / 256 : 0;
+  // fix-up work: edge-line points, plus the Dirichlet boundary points
+  // (fixup_bnd; same count as bnd_count in fused_impl.cuh)
+  long long nfixp = (long long)(nbx - 1) * (nby - 1) * m->Nzl +
+                    (long long)(nbx - 1) * (nchunks - 1) * m->Ny +
+                    (long long)(nby - 1) * (nchunks - 1) * m->Nx;
+  if (op->bc) nfixp += boundary_points(m);
+  const bool need_fix = nfixp > 0;
+  const long long nfixb = need_fix ? (nfixp + 255) / 256 : 0;
   if (fdot && op->dotp_len < grid + nfixb) {
     if (op->d_dotp) cudaFree(op->d_dotp);
     op->d_dotp = nullptr;
@@ -285,7 +297,6 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
   F.nplZ = nchunks - 1; F.nplY = nby - 1; F.nplX = nbx - 1;
   F.dotp = fdot ? op->d_dotp + grid : nullptr;
   F.kown = (int)A.kown;
-  const int nlines = std::max(F.nplX * F.nplY, std::max(F.nplX * F.nplZ, F.nplY * F.nplZ));
   // in-kernel fix-up (SIMT kernel; cooperative launch with a grid barrier)
   static const int infix_env = [] {
     // tuning knob: 0 = always the separate fixup_kernel, 2 = always in-kernel,
@@ -297,7 +308,7 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
   // problems, neutral or slower at ~30M dofs
   const long long npts = m->Nx * m->Ny * m->Nzl;
   const bool infix = (infix_env == 1 ? npts <= (8LL << 20) : infix_env == 2) &&
-                     PL.variant == 1 && nlines > 0 && grid <= nunits;
+                     PL.variant == 1 && need_fix && grid <= nunits;
   if (infix && !op->d_bar) {
     if (cudaMalloc(&op->d_bar, sizeof(unsigned long long)) != cudaSuccess ||
         cudaMemset(op->d_bar, 0, sizeof(unsigned long long)) != cudaSuccess) {
@@ -341,7 +352,7 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
     cudaEventRecord(ev.second, s);
     g_prof.brick.push_back(ev);
   }
-  if (nlines > 0 && !infix) {
+  if (need_fix && !infix) {
     if (g_prof.on) {
       ev = {prof_event(), prof_event()};
       cudaEventRecord(ev.first, s);
@@ -354,7 +365,7 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
     }
   }
   if (fdot) {
-    dot_partials_kernel<<<1, 256, 0, s>>>(op->d_dotp, grid + (nlines > 0 && !infix ? nfixb : 0),
+    dot_partials_kernel<<<1, 256, 0, s>>>(op->d_dotp, grid + (need_fix && !infix ? nfixb : 0),
                                           dot_out);
     HOFEM_LAUNCHED();
   }

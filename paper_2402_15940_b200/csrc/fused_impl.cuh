@@ -227,27 +227,80 @@ __device__ __forceinline__ double fixup_point(const FixArgs& F, int type, int li
         s += __ldcg(F.bbuf + brick * F.FB + off);  // written by other CTAs
       }
   const long long l = I + (long long)F.Nx * (J + (long long)F.Ny * K);
-  const double xl = F.x[l];
   if (F.bc) {
     const long long Kg = K + F.K0;
-    if (I == 0 || I == F.Nx - 1 || J == 0 || J == F.Ny - 1 || Kg == 0 || Kg == F.NzG - 1) {
-      F.y[l] = xl;
-      return K < F.kown ? xl * xl : 0.0;  // Dirichlet value: counted by the owner
-    }
+    if (I == 0 || I == F.Nx - 1 || J == 0 || J == F.Ny - 1 || Kg == 0 || Kg == F.NzG - 1)
+      return 0.0;  // Dirichlet point: written by the boundary pass (fixup_bnd)
   }
   F.y[l] = s;
-  return xl * s;
+  return F.x[l] * s;
+}
+
+// a9 boundary pass: y = x at every Dirichlet point of the local slab (global
+// boundary I, J or Kg in {0, max}), x.x counted by the owning rank.  The brick
+// kernels skip these points, so their x loads leave the brick epilogue.
+// Enumeration: global-bottom / global-top planes, then the two y faces, then
+// the two x faces (without the rows already covered).
+struct BndCount {
+  long long nz, ny, nx;
+  int kz0, nk;
+  bool bot, top;
+};
+__device__ __forceinline__ BndCount bnd_count(const FixArgs& F) {
+  BndCount b;
+  b.bot = F.K0 == 0;
+  b.top = F.K0 + F.Nzl - 1 == F.NzG - 1;
+  const long long plane = (long long)F.Nx * F.Ny;
+  b.kz0 = b.bot ? 1 : 0;
+  const int kz1 = F.Nzl - (b.top ? 1 : 0);
+  b.nk = kz1 > b.kz0 ? kz1 - b.kz0 : 0;
+  b.nz = F.bc ? plane * ((b.bot ? 1 : 0) + (b.top ? 1 : 0)) : 0;
+  b.ny = F.bc ? 2LL * F.Nx * b.nk : 0;
+  b.nx = F.bc ? 2LL * (F.Ny - 2) * b.nk : 0;
+  return b;
+}
+__device__ __forceinline__ double fixup_bnd(const FixArgs& F, const BndCount& b, long long g) {
+  int I, J, K;
+  const long long plane = (long long)F.Nx * F.Ny;
+  if (g < b.nz) {
+    K = (b.bot && g < plane) ? 0 : F.Nzl - 1;
+    const long long r = g % plane;
+    I = (int)(r % F.Nx);
+    J = (int)(r / F.Nx);
+  } else if ((g -= b.nz) < b.ny) {
+    const long long face = (long long)F.Nx * b.nk, r = g % face;
+    J = g < face ? 0 : F.Ny - 1;
+    I = (int)(r % F.Nx);
+    K = b.kz0 + (int)(r / F.Nx);
+  } else {
+    g -= b.ny;
+    const long long face = (long long)(F.Ny - 2) * b.nk, r = g % face;
+    I = g < face ? 0 : F.Nx - 1;
+    J = 1 + (int)(r % (F.Ny - 2));
+    K = b.kz0 + (int)(r / (F.Ny - 2));
+  }
+  const long long l = I + (long long)F.Nx * (J + (long long)F.Ny * K);
+  const double xl = F.x[l];
+  F.y[l] = xl;
+  return K < F.kown ? xl * xl : 0.0;
 }
 
 
 // Flat enumeration of the edge points, type by type: n0 x-y line points (along
 // z), then n1 x-z (along y, skipping y planes), then n2 y-z (along x).
-__device__ __forceinline__ long long fixup_count(const FixArgs& F) {
+// (then, with Dirichlet conditions, the boundary points: fixup_bnd)
+__device__ __forceinline__ long long fixup_edges(const FixArgs& F) {
   return (long long)F.nplX * F.nplY * F.Nzl + (long long)F.nplX * F.nplZ * F.Ny +
          (long long)F.nplY * F.nplZ * F.Nx;
 }
+__device__ __forceinline__ long long fixup_count(const FixArgs& F) {
+  const BndCount b = bnd_count(F);
+  return fixup_edges(F) + b.nz + b.ny + b.nx;
+}
 __device__ __forceinline__ double fixup_flat(const FixArgs& F, long long g) {
   const long long n0 = (long long)F.nplX * F.nplY * F.Nzl, n1 = (long long)F.nplX * F.nplZ * F.Ny;
+  const long long ne = fixup_edges(F);
+  if (g >= ne) return fixup_bnd(F, bnd_count(F), g - ne);
   if (g < n0) return fixup_point(F, 0, (int)(g / F.Nzl), (int)(g % F.Nzl));
   if (g < n0 + n1) return fixup_point(F, 1, (int)((g - n0) / F.Ny), (int)((g - n0) % F.Ny));
   return fixup_point(F, 2, (int)((g - n0 - n1) / F.Nx), (int)((g - n0 - n1) % F.Nx));
@@ -491,7 +544,7 @@ __device__ __forceinline__ void epi_segment(const ColArgs& A, const double* RA, 
   // x.y by contributions: every contribution this brick writes counts (also on
   // the non-owned top plane: the neighbour rank counts ITS contributions there);
   // a Dirichlet value y = x counts once, on the owning rank.
-  const bool acc = R.dot, acc_ess = R.dot && R.own;
+  const bool acc = R.dot;
   constexpr int NPT = (SX == BX - 1) ? p + 1 : p;  // the last column also owns i = p*BX
   double v[NPT];
 #pragma unroll
@@ -532,9 +585,7 @@ __device__ __forceinline__ void epi_segment(const ColArgs& A, const double* RA, 
       if (R.row_multi || (lo && xlo_sh) || (hi && xhi_sh)) {
         R.bb[R.yface ? (i == 0 ? 0 : p + 1) : i] = v[ii];  // edge line: partial buffer
       } else if (R.row_ess || (lo && xlo_ess) || i == ie) {
-        const double xv = A.x[R.gl + i];
-        A.y[R.gl + i] = xv;
-        if (acc_ess && R.face_lo) dsum = fma(xv, xv, dsum);
+        // Dirichlet point: y = x and its x.y term come from the fix-up pass
       } else {
         red_add(A.y + R.gl + i, v[ii]);
         if (acc) dsum = fma(R.lx[C::LXS * i], v[ii], dsum);
@@ -560,11 +611,7 @@ __device__ __forceinline__ void epi_segment(const ColArgs& A, const double* RA, 
     if (i >= nv) continue;
     const bool lo = (SX == 0 && ii == 0), hi = (SX == BX - 1 && ii == p);
     const bool ess = R.row_ess || (lo && xlo_ess) || (i == ie);
-    if (ess) {
-      const double xv = A.x[R.gl + i];
-      A.y[R.gl + i] = xv;
-      if (acc_ess && !(hi && xhi_sh)) dsum = fma(xv, xv, dsum);
-    } else {
+    if (!ess) {  // Dirichlet points: y = x and x.y in the fix-up pass
       if ((lo && xlo_sh) || (hi && xhi_sh))
         red_add(A.y + R.gl + i, v[ii]);
       else
