@@ -2257,7 +2257,7 @@ struct ShapeSD;
 template <> struct ShapeSD<2> { static constexpr int BX = 4, BY = 4, NT = 160, MAXR = 96, CPS = 4; };
 template <> struct ShapeSD<3> { static constexpr int BX = 4, BY = 2, NT = 128, MAXR = 128, CPS = 4; };
 template <> struct ShapeSD<4> { static constexpr int BX = 3, BY = 2, NT = 160, MAXR = 102, CPS = 4; };
-template <> struct ShapeSD<5> { static constexpr int BX = 2, BY = 2, NT = 160, MAXR = 128, CPS = 3; };
+template <> struct ShapeSD<5> { static constexpr int BX = 3, BY = 1, NT = 128, MAXR = 102, CPS = 5; };
 template <> struct ShapeSD<6> { static constexpr int BX = 1, BY = 2, NT = 128, MAXR = 128, CPS = 4; };
 template <> struct ShapeSD<7> { static constexpr int BX = 1, BY = 1, NT = 64, MAXR = 168, CPS = 6; };
 template <> struct ShapeSD<8> { static constexpr int BX = 1, BY = 1, NT = 96, MAXR = 168, CPS = 4; };
@@ -2305,6 +2305,7 @@ template <int P1>
 struct ShapeSMD : ShapeS<P1> {};
 // measured (BP1 at ~1M dofs, whole apply incl. memset and fix-up; gpurun_out/e12,
 // f5): single-element bricks pay off at p = 8 only (more edge lines elsewhere)
+template <> struct ShapeSMD<5> { static constexpr int BX = 2, BY = 2, NT = 160, MAXR = 128, CPS = 3; };
 template <> struct ShapeSMD<9> { static constexpr int BX = 1, BY = 1, NT = 128, MAXR = 96, CPS = 5; };
 #ifdef HOFEM_SM_P1
 struct ShapeSMOverride {
