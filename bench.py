@@ -383,8 +383,8 @@ def main():
     ap.add_argument("--e2e-reps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--ref-n", type=int, default=6, help="oracle sample: elements per axis")
-    ap.add_argument("--ref-iters", type=int, default=20)
+    ap.add_argument("--ref-n", type=int, default=10, help="oracle sample: elements per axis")
+    ap.add_argument("--ref-iters", type=int, default=3000)
     ap.add_argument("--sweep", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
