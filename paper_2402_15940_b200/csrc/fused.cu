@@ -307,8 +307,8 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
   // measured (gpurun_out/e15, e16): pays for small (launch/latency-bound)
   // problems, neutral or slower at ~30M dofs
   const long long npts = m->Nx * m->Ny * m->Nzl;
-  const bool infix = (infix_env == 1 ? npts <= (8LL << 20) : infix_env == 2) &&
-                     PL.variant == 1 && need_fix && grid <= nunits;
+  bool infix = (infix_env == 1 ? npts <= (8LL << 20) : infix_env == 2) &&
+               PL.variant == 1 && need_fix && grid <= nunits;
   if (infix && !op->d_bar) {
     if (cudaMalloc(&op->d_bar, sizeof(unsigned long long)) != cudaSuccess ||
         cudaMemset(op->d_bar, 0, sizeof(unsigned long long)) != cudaSuccess) {
@@ -333,13 +333,25 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
     ev = {prof_event(), prof_event()};
     cudaEventRecord(ev.first, s);
   }
-  switch (P1) {
-#define HOFEM_CASE(P)                                                            \
-  case P:                                                                        \
+  auto launch = [&]() {
+    switch (P1) {
+#define HOFEM_CASE(P)                                                                     \
+  case P:                                                                                 \
     ok = fused_launch<P>(kind, variant, op->Q, op->tab.B, op->tab.G, A, grid, s, &err); \
     break;
-    HOFEM_FOR_P1(HOFEM_CASE)
+      HOFEM_FOR_P1(HOFEM_CASE)
 #undef HOFEM_CASE
+    }
+  };
+  launch();
+  if (ok && infix && err == cudaErrorCooperativeLaunchTooLarge) {
+    // the device cannot hold the whole grid right now (e.g. shared by another
+    // context): plain launch, fix-up as its own kernel
+    cudaGetLastError();
+    infix = false;
+    A.infix = 0;
+    err = cudaSuccess;
+    launch();
   }
   if (!ok) {
     set_error("fused apply: no fused kernel for p=%d Q=%d", p, op->Q);
