@@ -267,6 +267,10 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
                     (long long)(nbx - 1) * (nchunks - 1) * m->Ny +
                     (long long)(nby - 1) * (nchunks - 1) * m->Nx;
   if (op->bc) nfixp += boundary_points(m);
+  if (nfixp >= (1LL << 31)) {  // the fix-up indexes its points in 32 bits
+    set_error("fused apply: %lld fix-up points exceed the 32-bit index range", nfixp);
+    return HOFEM_ERR_ARG;
+  }
   const bool need_fix = nfixp > 0;
   const long long nfixb = need_fix ? (nfixp + 255) / 256 : 0;
   if (fdot && op->dotp_len < grid + nfixb) {

@@ -259,32 +259,36 @@ __device__ __forceinline__ BndCount bnd_count(const FixArgs& F) {
   b.nx = F.bc ? 2LL * (F.Ny - 2) * b.nk : 0;
   return b;
 }
-__device__ __forceinline__ double fixup_bnd(const FixArgs& F, const BndCount& b, long long g) {
+__device__ __forceinline__ double fixup_bnd(const FixArgs& F, const BndCount& b, long long g64) {
+  // 32-bit index arithmetic (the boundary of one slab has < 2^31 points)
+  unsigned g = (unsigned)g64;
+  const unsigned Nx = (unsigned)F.Nx, Ny = (unsigned)F.Ny, plane = Nx * Ny;
+  const unsigned nz = (unsigned)b.nz, ny = (unsigned)b.ny;
   int I, J, K;
-  const long long plane = (long long)F.Nx * F.Ny;
-  if (g < b.nz) {
+  if (g < nz) {
     K = (b.bot && g < plane) ? 0 : F.Nzl - 1;
-    const long long r = g % plane;
-    I = (int)(r % F.Nx);
-    J = (int)(r / F.Nx);
-  } else if ((g -= b.nz) < b.ny) {
-    const long long face = (long long)F.Nx * b.nk, r = g % face;
+    const unsigned r = g < plane ? g : g - plane;
+    I = (int)(r % Nx);
+    J = (int)(r / Nx);
+  } else if ((g -= nz) < ny) {
+    const unsigned face = Nx * (unsigned)b.nk;
+    const unsigned r = g < face ? g : g - face;
     J = g < face ? 0 : F.Ny - 1;
-    I = (int)(r % F.Nx);
-    K = b.kz0 + (int)(r / F.Nx);
+    I = (int)(r % Nx);
+    K = b.kz0 + (int)(r / Nx);
   } else {
-    g -= b.ny;
-    const long long face = (long long)(F.Ny - 2) * b.nk, r = g % face;
+    g -= ny;
+    const unsigned face = (Ny - 2) * (unsigned)b.nk;
+    const unsigned r = g < face ? g : g - face;
     I = g < face ? 0 : F.Nx - 1;
-    J = 1 + (int)(r % (F.Ny - 2));
-    K = b.kz0 + (int)(r / (F.Ny - 2));
+    J = 1 + (int)(r % (Ny - 2));
+    K = b.kz0 + (int)(r / (Ny - 2));
   }
   const long long l = I + (long long)F.Nx * (J + (long long)F.Ny * K);
   const double xl = F.x[l];
   F.y[l] = xl;
   return K < F.kown ? xl * xl : 0.0;
 }
-
 
 // Flat enumeration of the edge points, type by type: n0 x-y line points (along
 // z), then n1 x-z (along y, skipping y planes), then n2 y-z (along x).
@@ -297,13 +301,17 @@ __device__ __forceinline__ long long fixup_count(const FixArgs& F) {
   const BndCount b = bnd_count(F);
   return fixup_edges(F) + b.nz + b.ny + b.nx;
 }
-__device__ __forceinline__ double fixup_flat(const FixArgs& F, long long g) {
-  const long long n0 = (long long)F.nplX * F.nplY * F.Nzl, n1 = (long long)F.nplX * F.nplZ * F.Ny;
+__device__ __forceinline__ double fixup_flat(const FixArgs& F, long long g64) {
   const long long ne = fixup_edges(F);
-  if (g >= ne) return fixup_bnd(F, bnd_count(F), g - ne);
-  if (g < n0) return fixup_point(F, 0, (int)(g / F.Nzl), (int)(g % F.Nzl));
-  if (g < n0 + n1) return fixup_point(F, 1, (int)((g - n0) / F.Ny), (int)((g - n0) % F.Ny));
-  return fixup_point(F, 2, (int)((g - n0 - n1) / F.Nx), (int)((g - n0 - n1) % F.Nx));
+  if (g64 >= ne) return fixup_bnd(F, bnd_count(F), g64 - ne);
+  // 32-bit index arithmetic (< 2^31 edge points per slab)
+  const unsigned g = (unsigned)g64;
+  const unsigned n0 = (unsigned)F.nplX * F.nplY * F.Nzl, n1 = (unsigned)F.nplX * F.nplZ * F.Ny;
+  if (g < n0) return fixup_point(F, 0, (int)(g / (unsigned)F.Nzl), (int)(g % (unsigned)F.Nzl));
+  if (g < n0 + n1)
+    return fixup_point(F, 1, (int)((g - n0) / (unsigned)F.Ny), (int)((g - n0) % (unsigned)F.Ny));
+  return fixup_point(F, 2, (int)((g - n0 - n1) / (unsigned)F.Nx),
+                     (int)((g - n0 - n1) % (unsigned)F.Nx));
 }
 
 struct ColArgs {
