@@ -363,6 +363,22 @@ def run_sweep(args, hf, torch, stream):
                 bts, N, E = alg_bytes(n, n, n, p, Q, nc)
                 res[name] = {"gdof_s": N / t / 1e9, "ms": 1e3 * t,
                              "alg_gbs": bts / t / 1e9, "frac": bts / t / 1e9 / peak}
+            if bench == "bp5" and getattr(args, "bp5_cg", False):
+                # config 4: Dirichlet, manufactured RHS, CG to 1e-10 relative residual
+                opd = hf.Operator(m, kind=kind, rule=rule, bc=hf.BC_DIRICHLET)
+                b = opd.rhs()
+                xs = torch.zeros_like(b)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                st, stats, _ = opd.cg(b, xs, rel_tol=1e-10, max_iter=20000, check_every=50)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                t = e0.elapsed_time(e1) / 1e3
+                res["cg_1e-10"] = {"iterations": stats.iterations, "converged": bool(stats.converged),
+                                   "rel_res": stats.final_rel_res, "s": t,
+                                   "gdof_it_s": m.n_local * stats.iterations / t / 1e9}
+                opd.close()
             op.close()
             m.close()
             torch.cuda.empty_cache()
@@ -386,6 +402,8 @@ def main():
     ap.add_argument("--ref-n", type=int, default=10, help="oracle sample: elements per axis")
     ap.add_argument("--ref-iters", type=int, default=3000)
     ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--bp5-cg", action="store_true",
+                    help="with --sweep: BP5 CG solves to 1e-10 (BASELINE config 4)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
