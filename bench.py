@@ -363,6 +363,21 @@ def run_sweep(args, hf, torch, stream):
                 bts, N, E = alg_bytes(n, n, n, p, Q, nc)
                 res[name] = {"gdof_s": N / t / 1e9, "ms": 1e3 * t,
                              "alg_gbs": bts / t / 1e9, "frac": bts / t / 1e9 / peak}
+            if bench == "bp1" and getattr(args, "bp5_cg", False):
+                # config 2: 100 fixed CG iterations on the ~1M-dof mass operator
+                b = op.rhs()
+                xs = torch.zeros_like(b)
+                op.cg(b, xs, max_iter=5, fixed_iters=True)
+                xs.zero_()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                st, stats, _ = op.cg(b, xs, max_iter=100, fixed_iters=True)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                t = e0.elapsed_time(e1) / 1e3
+                res["cg_100"] = {"iterations": stats.iterations, "s": t,
+                                 "gdof_it_s": m.n_local * stats.iterations / t / 1e9}
             if bench == "bp5" and getattr(args, "bp5_cg", False):
                 # config 4: Dirichlet, manufactured RHS, CG to 1e-10 relative residual
                 opd = hf.Operator(m, kind=kind, rule=rule, bc=hf.BC_DIRICHLET)
@@ -403,7 +418,8 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=3000)
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--bp5-cg", action="store_true",
-                    help="with --sweep: BP5 CG solves to 1e-10 (BASELINE config 4)")
+                    help="with --sweep: BP5 CG solves to 1e-10 (BASELINE config 4) and "
+                         "100 fixed BP1 CG iterations (config 2)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
