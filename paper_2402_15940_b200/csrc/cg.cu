@@ -11,6 +11,9 @@
 // order: results are bitwise reproducible run to run.  Multi-rank: the scalar
 // partials are ncclAllReduce'd on the same stream before use.
 #include <math.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include <vector>
 
@@ -201,6 +204,49 @@ __global__ void __launch_bounds__(kDotThreads) pupdate_kernel(
   }
 }
 
+// Small single-rank problems: update + p-update in ONE cooperative kernel
+// (the first step of the fused CG iteration, §8(f) f1).  Phase 1: alpha =
+// rr/pAp, r -= alpha Ap, block partials of r.r; grid barrier; every block sums
+// the partials in block order (same value everywhere, deterministic), beta =
+// rr'/rr; phase 2: x += alpha p, p = r + beta p.  Saves a launch and the
+// last-block reduction per iteration.
+__global__ void __launch_bounds__(kDotThreads) upd_fused_kernel(
+    long long n, long long n_owned, const double* __restrict__ Ap, double* r, double* p,
+    double* __restrict__ x, const double* sc_rr, const double* sc_pAp, double* partials,
+    double* out, double* flag, unsigned long long* bar, unsigned long long target) {
+  __shared__ double sh[32];
+  if (!(*sc_pAp > 0.0) && blockIdx.x == 0 && threadIdx.x == 0) *flag = 1.0;
+  const double alpha = cg_alpha(sc_rr, sc_pAp);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  double s = 0.0;
+  for (long long i = t0; i < n; i += stride) {
+    const double v = fma(-alpha, Ap[i], r[i]);
+    r[i] = v;
+    if (i < n_owned) s = fma(v, v, s);
+  }
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+  grid_barrier(bar, target);
+  double rn = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) rn += __ldcg(partials + b);
+  rn = block_sum(rn, sh);
+  __shared__ double rn_sh;
+  if (threadIdx.x == 0) {
+    rn_sh = rn;
+    if (blockIdx.x == 0) *out = rn;
+  }
+  __syncthreads();
+  rn = rn_sh;
+  const double ro = *sc_rr;
+  const double beta = ro > 0.0 ? rn / ro : 0.0;
+  for (long long i = t0; i < n; i += stride) {
+    const double pv = p[i];
+    x[i] = fma(alpha, pv, x[i]);
+    p[i] = fma(beta, pv, r[i]);
+  }
+}
+
 }  // namespace
 
 hofem_status dot_local(Mesh* m, const double* a, const double* b, double* d_out,
@@ -258,6 +304,31 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
   HOFEM_CUDA(cudaStreamSynchronize(s));
 
   const unsigned vgrid = kDotBlocks;
+  // fused update + p-update (one cooperative kernel) for small single-rank
+  // problems; the grid is what the device holds co-resident (<= kDotBlocks)
+  static const int cgfuse_env = [] {
+    const char* e = getenv("HOFEM_CGFUSE");  // 0 = always separate kernels
+    return e ? atoi(e) : 1;
+  }();
+  int ugrid = 0;
+  if (cgfuse_env && m->nranks == 1 && n <= (8LL << 20)) {
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, upd_fused_kernel, kDotThreads, 0) ==
+            cudaSuccess &&
+        per > 0) {
+      ugrid = std::min(per * num_sms(), kDotBlocks);
+      if (!op->d_bar) {
+        if (cudaMalloc(&op->d_bar, sizeof(unsigned long long)) != cudaSuccess ||
+            cudaMemset(op->d_bar, 0, sizeof(unsigned long long)) != cudaSuccess) {
+          cudaGetLastError();
+          ugrid = 0;
+        }
+        op->bar_count = 0;
+      }
+    } else {
+      cudaGetLastError();
+    }
+  }
   int k = 0;
   hofem_status status = fixed_iters ? HOFEM_OK : HOFEM_NOT_CONVERGED;
   double rr_last = rr0;
@@ -273,14 +344,41 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
       HOFEM_TRY(dot_local(m, op->d_p, op->d_Ap, pAp, s));
     }
     HOFEM_TRY(allreduce_sum(m, pAp, 1, s));
-    update_kernel<<<kDotBlocks, kDotThreads, 0, s>>>(n, no, op->d_Ap, op->d_r, rr + k, pAp,
-                                                     m->d_partials, m->d_counter, rr + k + 1,
-                                                     flag);
-    HOFEM_LAUNCHED();
-    HOFEM_TRY(allreduce_sum(m, rr + k + 1, 1, s));
-    pupdate_kernel<<<vgrid, kDotThreads, 0, s>>>(n, op->d_r, op->d_p, x, rr + k + 1, rr + k,
-                                                 pAp);
-    HOFEM_LAUNCHED();
+    bool fused_upd = false;
+    if (ugrid > 0) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)ugrid);
+      cfg.blockDim = dim3(kDotThreads);
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      const unsigned long long target = op->bar_count + (unsigned long long)ugrid;
+      const cudaError_t e =
+          cudaLaunchKernelEx(&cfg, upd_fused_kernel, n, no, (const double*)op->d_Ap, op->d_r,
+                             op->d_p, x, (const double*)(rr + k), (const double*)pAp,
+                             m->d_partials, rr + k + 1, flag, op->d_bar, target);
+      if (e == cudaSuccess) {
+        op->bar_count = target;
+        count_launch();
+        fused_upd = true;
+      } else {
+        cudaGetLastError();  // e.g. grid no longer co-resident: separate kernels
+        ugrid = 0;
+      }
+    }
+    if (!fused_upd) {
+      update_kernel<<<kDotBlocks, kDotThreads, 0, s>>>(n, no, op->d_Ap, op->d_r, rr + k, pAp,
+                                                       m->d_partials, m->d_counter, rr + k + 1,
+                                                       flag);
+      HOFEM_LAUNCHED();
+      HOFEM_TRY(allreduce_sum(m, rr + k + 1, 1, s));
+      pupdate_kernel<<<vgrid, kDotThreads, 0, s>>>(n, op->d_r, op->d_p, x, rr + k + 1, rr + k,
+                                                   pAp);
+      HOFEM_LAUNCHED();
+    }
     ++k;
     if ((!fixed_iters && k % check_every == 0) || k == max_iter) {
       double h[2];

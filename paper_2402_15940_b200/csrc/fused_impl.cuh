@@ -357,29 +357,6 @@ __device__ __forceinline__ void block_sum_store(double v, double* out, double* r
   }
 }
 
-// Grid-wide barrier of a cooperative (co-resident) launch on a monotonic
-// 64-bit counter: every CTA adds 1 and waits for `target` (the host keeps the
-// running total of launched CTAs, so the counter is never reset).  Bounded
-// spin: a barrier that cannot complete traps (launch error) instead of
-// hanging the GPU.
-__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1ull);
-    unsigned long long v;
-    unsigned spins = 0;
-    do {
-      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
-      if (v >= target) break;
-      __nanosleep(100);
-    } while (++spins < (1u << 25));
-    if (v < target) __trap();
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 enum { KIND_MASS = 0, KIND_DIFF = 1, KIND_COLLOC = 2 };
 
 __device__ __forceinline__ double ld_stream(const double* p) {

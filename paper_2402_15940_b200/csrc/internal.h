@@ -19,6 +19,7 @@ constexpr int kNumSMs = 148;
 void set_error(const char* fmt, ...);
 hofem_status cuda_status(cudaError_t e, const char* what);
 void count_launch(long long n = 1);
+int num_sms();  // SM count of the current device (fused.cu)
 
 #define HOFEM_CUDA(call)                                                   \
   do {                                                                     \
@@ -134,5 +135,31 @@ inline bool is_ess(const Mesh* m, long long I, long long J, long long Kglob) {
   return I == 0 || I == m->Nx - 1 || J == 0 || J == m->Ny - 1 || Kglob == 0 ||
          Kglob == m->NzG - 1;
 }
+
+#ifdef __CUDACC__
+// Grid-wide barrier of a cooperative (co-resident) launch on a monotonic
+// 64-bit counter: every CTA adds 1 and waits for `target` (the host keeps the
+// running total of launched CTAs, so the counter is never reset).  Bounded
+// spin: a barrier that cannot complete traps (launch error) instead of
+// hanging the GPU.
+__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1ull);
+    unsigned long long v;
+    unsigned spins = 0;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
+      if (v >= target) break;
+      __nanosleep(100);
+    } while (++spins < (1u << 25));
+    if (v < target) __trap();
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+#endif
 
 }  // namespace hofem
