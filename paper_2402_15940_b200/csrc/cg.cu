@@ -204,6 +204,17 @@ __global__ void __launch_bounds__(kDotThreads) pupdate_kernel(
   }
 }
 
+// Fixed-order sum of n partials into *out (fallback when the fused update
+// cannot be launched after the operator left its p.Ap partials unsummed).
+__global__ void __launch_bounds__(256) sum_partials_kernel(const double* part, long long n,
+                                                           double* out) {
+  __shared__ double sh[32];
+  double v = 0.0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) v += part[i];
+  v = block_sum(v, sh);
+  if (threadIdx.x == 0) *out = v;
+}
+
 // Small single-rank problems: update + p-update in ONE cooperative kernel
 // (the first step of the fused CG iteration, §8(f) f1).  Phase 1: alpha =
 // rr/pAp, r -= alpha Ap, block partials of r.r; grid barrier; every block sums
@@ -212,11 +223,29 @@ __global__ void __launch_bounds__(kDotThreads) pupdate_kernel(
 // last-block reduction per iteration.
 __global__ void __launch_bounds__(kDotThreads) upd_fused_kernel(
     long long n, long long n_owned, const double* __restrict__ Ap, double* r, double* p,
-    double* __restrict__ x, const double* sc_rr, const double* sc_pAp, double* partials,
-    double* out, double* flag, unsigned long long* bar, unsigned long long target) {
+    double* __restrict__ x, const double* sc_rr, double* sc_pAp, const double* pparts,
+    long long npparts, double* partials, double* out, double* flag, unsigned long long* bar,
+    unsigned long long target) {
   __shared__ double sh[32];
-  if (!(*sc_pAp > 0.0) && blockIdx.x == 0 && threadIdx.x == 0) *flag = 1.0;
-  const double alpha = cg_alpha(sc_rr, sc_pAp);
+  __shared__ double pap_sh;
+  double pAp;
+  if (pparts) {
+    // the operator kernel's per-CTA p.Ap partials, summed here in fixed order
+    // (identical in every block) instead of by a separate launch
+    double v = 0.0;
+    for (long long i = threadIdx.x; i < npparts; i += blockDim.x) v += pparts[i];
+    v = block_sum(v, sh);
+    if (threadIdx.x == 0) {
+      pap_sh = v;
+      if (blockIdx.x == 0) *sc_pAp = v;
+    }
+    __syncthreads();
+    pAp = pap_sh;
+  } else {
+    pAp = *sc_pAp;
+  }
+  if (!(pAp > 0.0) && blockIdx.x == 0 && threadIdx.x == 0) *flag = 1.0;
+  const double alpha = pAp > 0.0 ? *sc_rr / pAp : 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   double s = 0.0;
@@ -337,8 +366,13 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
   while (!done && k < max_iter) {
     // Ap = A p and pAp = p.Ap: fused into the operator kernels when possible
     // (computed from the contributions they write), else a separate dot
+    const double* pparts = nullptr;
+    long long npparts = 0;
     if (fused_supported(op)) {
-      HOFEM_TRY(apply_fused(op, op->d_p, op->d_Ap, s, pAp));
+      if (ugrid > 0)
+        HOFEM_TRY(apply_fused(op, op->d_p, op->d_Ap, s, pAp, &pparts, &npparts));
+      else
+        HOFEM_TRY(apply_fused(op, op->d_p, op->d_Ap, s, pAp));
     } else {
       HOFEM_TRY(apply_unfused(op, op->d_p, op->d_Ap, s));
       HOFEM_TRY(dot_local(m, op->d_p, op->d_Ap, pAp, s));
@@ -358,7 +392,7 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
       const unsigned long long target = op->bar_count + (unsigned long long)ugrid;
       const cudaError_t e =
           cudaLaunchKernelEx(&cfg, upd_fused_kernel, n, no, (const double*)op->d_Ap, op->d_r,
-                             op->d_p, x, (const double*)(rr + k), (const double*)pAp,
+                             op->d_p, x, (const double*)(rr + k), pAp, pparts, npparts,
                              m->d_partials, rr + k + 1, flag, op->d_bar, target);
       if (e == cudaSuccess) {
         op->bar_count = target;
@@ -368,6 +402,10 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
         cudaGetLastError();  // e.g. grid no longer co-resident: separate kernels
         ugrid = 0;
       }
+    }
+    if (!fused_upd && pparts) {  // deferred p.Ap sum (fallback path)
+      sum_partials_kernel<<<1, 256, 0, s>>>(pparts, npparts, pAp);
+      HOFEM_LAUNCHED();
     }
     if (!fused_upd) {
       update_kernel<<<kDotBlocks, kDotThreads, 0, s>>>(n, no, op->d_Ap, op->d_r, rr + k, pAp,

@@ -226,7 +226,7 @@ hofem_status fused_info(const Op* op, hofem_fused_info* out) {
 }
 
 hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
-                         double* dot_out) {
+                         double* dot_out, const double** dot_parts, long long* dot_nparts) {
   Mesh* m = op->mesh;
   const int P1 = m->P1, p = m->p;
   const Plan PL = make_plan(op);
@@ -381,9 +381,14 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
     }
   }
   if (fdot) {
-    dot_partials_kernel<<<1, 256, 0, s>>>(op->d_dotp, grid + (need_fix && !infix ? nfixb : 0),
-                                          dot_out);
-    HOFEM_LAUNCHED();
+    const long long nparts = grid + (need_fix && !infix ? nfixb : 0);
+    if (dot_parts && dot_nparts) {
+      *dot_parts = op->d_dotp;  // summed by the caller's kernel, same fixed order
+      *dot_nparts = nparts;
+    } else {
+      dot_partials_kernel<<<1, 256, 0, s>>>(op->d_dotp, nparts, dot_out);
+      HOFEM_LAUNCHED();
+    }
   }
   HOFEM_TRY(exchange_planes(op, x, y, s));
   if (dot_out && !fdot) return dot_local(m, x, y, dot_out, s);  // owned dofs, after exchange

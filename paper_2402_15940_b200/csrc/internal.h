@@ -116,8 +116,12 @@ hofem_status apply_unfused(Op* op, const double* x, double* y, cudaStream_t s);
 // dot_out (device scalar, optional): the rank-local owned x.y, computed inside
 // the fused kernels from the contributions they write (deterministic); the
 // caller allreduces it.
+// With dot_parts non-null (and dot_out non-null) the final fixed-order sum of
+// the per-CTA x.y partials is left to the caller: *dot_parts / *dot_nparts
+// name the partial array (single rank only; used by the fused CG update).
 hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
-                         double* dot_out = nullptr);
+                         double* dot_out = nullptr, const double** dot_parts = nullptr,
+                         long long* dot_nparts = nullptr);
 // Rank-local a.b over owned dofs into *d_out (device), deterministic; no allreduce.
 hofem_status dot_local(Mesh* m, const double* a, const double* b, double* d_out, cudaStream_t s);
 hofem_status fused_info(const Op* op, hofem_fused_info* out);
