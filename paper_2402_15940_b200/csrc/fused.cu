@@ -322,14 +322,19 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
     }
     op->bar_count = 0;
   }
+  const bool zero_y = nbx > 1 || nby > 1 || nchunks > 1;  // face points are reduced into y
   A.infix = infix ? 1 : 0;
   A.bar = op->d_bar;
-  A.bar_target = infix ? op->bar_count + (unsigned long long)grid : 0;
+  // with infix the zeroing of y moves into the kernel too (first barrier)
+  A.zero_n = infix && zero_y ? m->Nx * m->Ny * m->Nzl : 0;
+  const unsigned long long nbar = infix ? (A.zero_n > 0 ? 2ULL : 1ULL) : 0ULL;
+  A.bar_target0 = op->bar_count + (unsigned long long)grid;
+  A.bar_target = op->bar_count + nbar * (unsigned long long)grid;
   A.fx = F;
   cudaError_t err = cudaSuccess;
   bool ok = false;
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
-  if (nbx > 1 || nby > 1 || nchunks > 1) {
+  if (zero_y && A.zero_n == 0) {
     // single-face points are completed by two-term reductions onto zero
     HOFEM_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * m->Nx * m->Ny * m->Nzl, s));
   }
@@ -350,11 +355,15 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
   launch();
   if (ok && infix && err == cudaErrorCooperativeLaunchTooLarge) {
     // the device cannot hold the whole grid right now (e.g. shared by another
-    // context): plain launch, fix-up as its own kernel
+    // context): memset + plain launch, fix-up as its own kernel
     cudaGetLastError();
     infix = false;
     A.infix = 0;
     err = cudaSuccess;
+    if (A.zero_n > 0) {
+      A.zero_n = 0;
+      HOFEM_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * m->Nx * m->Ny * m->Nzl, s));
+    }
     launch();
   }
   if (!ok) {
@@ -363,7 +372,7 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
   }
   count_launch();
   if (err != cudaSuccess) return cuda_status(err, "fused column kernel launch");
-  if (infix) op->bar_count += (unsigned long long)grid;  // every CTA arrives once
+  if (infix) op->bar_count = A.bar_target;  // every CTA arrived at each barrier
   if (g_prof.on) {
     cudaEventRecord(ev.second, s);
     g_prof.brick.push_back(ev);

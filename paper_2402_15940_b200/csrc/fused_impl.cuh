@@ -334,6 +334,10 @@ struct ColArgs {
   unsigned long long* bar;       // grid-barrier counter (monotonic)
   unsigned long long bar_target; // its value once every CTA of this launch arrived
   FixArgs fx;
+  // with infix: y (ny doubles) zeroed in-kernel before a first grid barrier
+  // (target bar_target0) instead of a cudaMemsetAsync
+  long long zero_n;
+  unsigned long long bar_target0;
 };
 
 // Fixed-order block sum; thread 0 stores it to *out.  All threads must call.
@@ -1607,6 +1611,13 @@ __global__ void __maxnreg__(MAXR)
   }
 
   FOR_ITEMS(i, C::SMEM_DOUBLES, NT, threadIdx.x) smem[i] = 0.0;
+  if (A.zero_n > 0) {
+    // y = 0 before any brick adds into it (small problems: no separate memset)
+    const long long st = (long long)gridDim.x * NT;
+    for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < A.zero_n; i += st)
+      A.y[i] = 0.0;
+    grid_barrier(A.bar, A.bar_target0);
+  }
   cta_sync();
   FOR_ITEMS(i, Q * P, NT, threadIdx.x) {
     TBs[(i / P) * PR + i % P] = T.B[i];
