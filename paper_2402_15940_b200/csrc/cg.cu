@@ -336,11 +336,12 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
   // fused update + p-update (one cooperative kernel) for small single-rank
   // problems; the grid is what the device holds co-resident (<= kDotBlocks)
   static const int cgfuse_env = [] {
-    const char* e = getenv("HOFEM_CGFUSE");  // 0 = always separate kernels
+    // 0 = always separate kernels, 2 = fused at any size, 1 = up to 8 Mi dofs
+    const char* e = getenv("HOFEM_CGFUSE");
     return e ? atoi(e) : 1;
   }();
   int ugrid = 0;
-  if (cgfuse_env && m->nranks == 1 && n <= (8LL << 20)) {
+  if (cgfuse_env && m->nranks == 1 && (cgfuse_env == 2 || n <= (8LL << 20))) {
     int per = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, upd_fused_kernel, kDotThreads, 0) ==
             cudaSuccess &&
