@@ -48,7 +48,7 @@ def alg_bytes(nx, ny, nz, p, Q, nc):
     return 16 * N + 8 * nc * E * Q ** 3, N, E
 
 
-KERNEL_NAMES = {0: "fused_elem_mma", 1: "fused_elem_simt", 2: "fused_column_colloc"}  # fused_info.variant
+KERNEL_NAMES = {1: "fused_elem_simt"}  # fused_info.variant
 
 
 class ClockSampler:

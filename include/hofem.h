@@ -18,9 +18,21 @@
  *    rank-local L-vectors of length n_local, lexicographic with x fastest:
  *    l = I + Nx*(J + Ny*K) (reading R3).  The two z-interface planes are
  *    duplicated on both neighbouring ranks and kept bitwise identical (R9).
+ *  - Vector pointers must be 16-byte aligned (the vector kernels use 16-byte
+ *    accesses); a misaligned pointer returns HOFEM_ERR_ARG.  Lengths are not
+ *    passed: every vector holds n_local doubles of its mesh (hofem_mesh_info);
+ *    the caller guarantees that (the Python binding checks it).
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *    Everything is stream-ordered and asynchronous, except the calls marked
- *    SYNC, which synchronize `stream` before returning.
+ *    SYNC, which synchronize `stream` before returning.  Stream-ordered calls
+ *    (hofem_op_apply included) may be captured into a CUDA graph and replayed:
+ *    the in-kernel grid barriers reset themselves and keep no host state.
+ *  - Single-stream handles: an operator (and the mesh it was built on) owns
+ *    scratch buffers (brick partials, reduction partials, the grid barrier) that
+ *    every call reuses, so calls on one operator or mesh must be ordered on ONE
+ *    stream (or otherwise serialised by the caller).  Concurrent calls on the
+ *    same handle from two streams race.  Distinct operators on distinct meshes
+ *    are independent.
  *  - Opaque handles are owned by the library; each destroy frees exactly what
  *    the matching create allocated.  The library never frees caller buffers.
  *  - x and y must not alias; y is fully overwritten.
@@ -160,6 +172,8 @@ typedef struct {
  * check_every iterations: the only device->host copy), or runs exactly max_iter
  * iterations when fixed_iters = 1.  x: in x0, out the iterate.
  * rr_history (host, nullable, length max_iter+1) receives r_k.r_k.
+ * Small single-rank problems run the whole solve in one persistent kernel
+ * (HOFEM_OPT_CG_PERSISTENT), which tests convergence every iteration.
  * Returns HOFEM_NOT_CONVERGED if max_iter was hit in tolerance mode,
  * HOFEM_ERR_BREAKDOWN if pAp <= 0. */
 hofem_status hofem_cg(void* op, const double* b, double* x, double rel_tol, int max_iter,
@@ -185,14 +199,12 @@ hofem_status hofem_profile_enable(int enable);
 hofem_status hofem_profile_read(hofem_profile_stats* out);
 
 /* How hofem_op_apply runs this operator (for the bench's roofline figure):
- * fused kernel variant (0 tensor-core DMMA, 1 SIMT thread-per-line incl. the
- * collocated BP5 form, 2 the older collocated column kernel; -1 the operator
- * has no fused kernel and apply uses the unfused path), brick shape,
- * work-unit z chunking, and the number of local lattice points the fused
- * kernel completes itself (interior points, and single-face points by two
- * order-independent reductions) vs. through the fix-up kernel (edge lines of
- * the brick grid).  Host-only, no device work.  The variant follows the per-p default
- * unless the environment variable HOFEM_FUSED=mma|simt overrides it. */
+ * fused kernel variant (1 = the SIMT thread-per-line brick kernel, incl. its
+ * collocated BP5 form; -1 the operator has no fused kernel and apply uses the
+ * unfused path), brick shape, work-unit z chunking, and the number of local
+ * lattice points the fused kernel completes itself (interior points, and
+ * single-face points by two order-independent reductions) vs. through the
+ * fix-up (edge lines of the brick grid).  Host-only, no device work. */
 typedef struct {
   int variant;
   int bx, by;            /* elements per brick in x, y (one element layer in z) */
@@ -201,12 +213,28 @@ typedef struct {
   long long direct_points, fixup_points;
 } hofem_fused_info;
 hofem_status hofem_op_fused_info(const void* op, hofem_fused_info* out);
-/* Select the fused kernel of hofem_op_apply for this operator: -1 default
- * (HOFEM_FUSED env or the measured per-p choice), 0 DMMA, 1 SIMT.  For a
- * collocated (BP5) operator: 1 (default) the SIMT kernel with B = I, 0 the
- * older column kernel.  All compute the same operator (parity-tested); only
- * the schedule differs.  HOFEM_ERR_ARG if out of range. */
-hofem_status hofem_op_set_fused_variant(void* op, int variant);
+/* Per-operator schedule options.  Every setting computes the same operator /
+ * the same CG recurrence (parity-tested); only the kernel schedule differs.
+ * Values: 0 = never, 1 = auto (the measured default: a size threshold),
+ * 2 = always (L2_PREFETCH: 0 / 1).  HOFEM_ERR_ARG for an unknown option or value.
+ *  INFIX          edge-line fix-up (and the zeroing of y) inside the brick kernel
+ *                 behind a grid barrier (cooperative launch) instead of a memset +
+ *                 separate fix-up kernel; auto = local meshes <= 8 Mi points.
+ *  CG_FUSED_UPDATE  per-iteration CG: r/x/p updates and both dot products in one
+ *                 cooperative kernel; auto = single rank, <= 8 Mi dofs.
+ *  CG_PERSISTENT  hofem_cg runs the whole solve in ONE cooperative kernel (brick
+ *                 pass, fix-up, p.Ap, updates, r.r, stop test, all behind grid
+ *                 barriers; §2.3); single rank only; auto =
+ *                 <= 8 Mi dofs.  Convergence is then tested every iteration.
+ *  L2_PREFETCH    bulk-prefetch the next brick's qdata into L2. */
+typedef enum {
+  HOFEM_OPT_INFIX = 1,
+  HOFEM_OPT_CG_FUSED_UPDATE = 2,
+  HOFEM_OPT_CG_PERSISTENT = 3,
+  HOFEM_OPT_L2_PREFETCH = 4
+} hofem_option;
+hofem_status hofem_op_set_option(void* op, hofem_option opt, int value);
+hofem_status hofem_op_get_option(const void* op, hofem_option opt, int* value);
 
 /* Number of kernel launches the library issued since the last reset (for the
  * bench's gpu_launches claim); counts every <<<>>> launch of this library. */

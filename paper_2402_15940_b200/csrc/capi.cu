@@ -5,6 +5,7 @@
 #include <string.h>
 
 #include <atomic>
+#include <cstdint>
 
 #include "internal.h"
 
@@ -69,11 +70,24 @@ void free_op(Op* op) {
   cudaFree(op->d_B); cudaFree(op->d_G); cudaFree(op->d_qdata);
   cudaFree(op->d_ein); cudaFree(op->d_eout); cudaFree(op->d_bbuf);
   cudaFree(op->d_r); cudaFree(op->d_p); cudaFree(op->d_Ap); cudaFree(op->d_cg);
-  cudaFree(op->d_dotp); cudaFree(op->d_bar);
+  cudaFree(op->d_dotp); cudaFree(op->d_bar); cudaFree(op->d_cgparts);
   delete op;
 }
 
 inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Vector arguments must be 16-byte aligned (the vector kernels use 16-byte
+// loads); a misaligned pointer is an argument error, never a device fault.
+inline bool aligned(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+#define HOFEM_ALIGNED(fn, ...)                                                       \
+  do {                                                                               \
+    const void* ps_[] = {__VA_ARGS__};                                               \
+    for (const void* q_ : ps_)                                                       \
+      if (!aligned(q_)) {                                                            \
+        set_error("%s: vector pointer %p is not 16-byte aligned", fn, q_);           \
+        return HOFEM_ERR_ARG;                                                        \
+      }                                                                              \
+  } while (0)
 
 }  // namespace
 }  // namespace hofem
@@ -90,12 +104,36 @@ hofem_status hofem_profile_read(hofem_profile_stats* out) {
   return profile_read(out);
 }
 
-hofem_status hofem_op_set_fused_variant(void* op, int variant) {
-  if (!op || variant < -1 || variant > 1) {
-    set_error("hofem_op_set_fused_variant: need op != NULL and variant in {-1, 0, 1}");
+namespace {
+int* option_slot(Op* op, int opt) {
+  switch (opt) {
+    case HOFEM_OPT_INFIX: return &op->opt_infix;
+    case HOFEM_OPT_CG_FUSED_UPDATE: return &op->opt_cg_fuse;
+    case HOFEM_OPT_CG_PERSISTENT: return &op->opt_cg_persist;
+    case HOFEM_OPT_L2_PREFETCH: return &op->opt_l2pf;
+  }
+  return nullptr;
+}
+}  // namespace
+
+hofem_status hofem_op_set_option(void* op, hofem_option opt, int value) {
+  int* slot = op ? option_slot(static_cast<Op*>(op), opt) : nullptr;
+  const int vmax = opt == HOFEM_OPT_L2_PREFETCH ? 1 : 2;
+  if (!slot || value < 0 || value > vmax) {
+    set_error("hofem_op_set_option: need op != NULL, a known option and 0 <= value <= %d", vmax);
     return HOFEM_ERR_ARG;
   }
-  static_cast<Op*>(op)->fused_variant = variant;
+  *slot = value;
+  return HOFEM_OK;
+}
+
+hofem_status hofem_op_get_option(const void* op, hofem_option opt, int* value) {
+  int* slot = op ? option_slot(const_cast<Op*>(static_cast<const Op*>(op)), opt) : nullptr;
+  if (!slot || !value) {
+    set_error("hofem_op_get_option: need op != NULL, a known option and value != NULL");
+    return HOFEM_ERR_ARG;
+  }
+  *value = *slot;
   return HOFEM_OK;
 }
 
@@ -222,6 +260,7 @@ hofem_status hofem_op_create(void* mesh, hofem_kind kind, hofem_rule rule, int q
 hofem_status hofem_op_apply(void* op_, const double* x, double* y, void* stream) {
   Op* op = static_cast<Op*>(op_);
   if (!op || !x || !y || x == y) { set_error("hofem_op_apply: NULL or aliased x/y"); return HOFEM_ERR_ARG; }
+  HOFEM_ALIGNED("hofem_op_apply", x, y);
   return apply_any(op, x, y, S(stream));
 }
 
@@ -232,6 +271,7 @@ hofem_status hofem_op_apply_dot(void* op_, const double* x, double* y, double* d
     set_error("hofem_op_apply_dot: NULL or aliased x/y");
     return HOFEM_ERR_ARG;
   }
+  HOFEM_ALIGNED("hofem_op_apply_dot", x, y);
   Mesh* m = op->mesh;
   if (fused_supported(op)) {
     HOFEM_TRY(apply_fused(op, x, y, S(stream), m->d_scalars));
@@ -249,6 +289,7 @@ hofem_status hofem_op_apply_dot(void* op_, const double* x, double* y, double* d
 hofem_status hofem_op_apply_unfused(void* op_, const double* x, double* y, void* stream) {
   Op* op = static_cast<Op*>(op_);
   if (!op || !x || !y || x == y) { set_error("hofem_op_apply_unfused: NULL or aliased x/y"); return HOFEM_ERR_ARG; }
+  HOFEM_ALIGNED("hofem_op_apply_unfused", x, y);
   return apply_unfused(op, x, y, S(stream));
 }
 
@@ -270,6 +311,7 @@ hofem_status hofem_op_nq1d(const void* op_, int* q) {
 hofem_status hofem_rhs_manufactured(void* op_, double* b, void* stream) {
   Op* op = static_cast<Op*>(op_);
   if (!op || !b) { set_error("hofem_rhs_manufactured: NULL"); return HOFEM_ERR_ARG; }
+  HOFEM_ALIGNED("hofem_rhs_manufactured", b);
   HOFEM_TRY(build_rhs(op, b, S(stream)));
   return exchange_planes(op, nullptr, b, S(stream));
 }
@@ -277,6 +319,7 @@ hofem_status hofem_rhs_manufactured(void* op_, double* b, void* stream) {
 hofem_status hofem_fill_random(const void* mesh, unsigned long long seed, double* x, void* stream) {
   const Mesh* m = static_cast<const Mesh*>(mesh);
   if (!m || !x) { set_error("hofem_fill_random: NULL"); return HOFEM_ERR_ARG; }
+  HOFEM_ALIGNED("hofem_fill_random", x);
   return fill_random(m, seed, x, S(stream));
 }
 
@@ -287,6 +330,7 @@ hofem_status hofem_cg(void* op_, const double* b, double* x, double rel_tol, int
                       hofem_cg_stats* stats, void* stream) {
   Op* op = static_cast<Op*>(op_);
   if (!op || !b || !x || b == x) { set_error("hofem_cg: NULL or aliased b/x"); return HOFEM_ERR_ARG; }
+  HOFEM_ALIGNED("hofem_cg", b, x);
   return cg_solve(op, b, x, rel_tol, max_iter, fixed_iters, check_every, rr_history, stats,
                   S(stream));
 }
@@ -295,6 +339,7 @@ hofem_status hofem_dot(const void* mesh, const double* a, const double* b, doubl
                        void* stream) {
   Mesh* m = const_cast<Mesh*>(static_cast<const Mesh*>(mesh));
   if (!m || !a || !b || !out_host) { set_error("hofem_dot: NULL"); return HOFEM_ERR_ARG; }
+  HOFEM_ALIGNED("hofem_dot", a, b);
   HOFEM_TRY(dot_device(m, a, b, m->d_scalars, S(stream)));
   HOFEM_CUDA(cudaMemcpyAsync(out_host, m->d_scalars, sizeof(double), cudaMemcpyDeviceToHost,
                              S(stream)));

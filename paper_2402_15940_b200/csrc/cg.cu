@@ -224,8 +224,7 @@ __global__ void __launch_bounds__(256) sum_partials_kernel(const double* part, l
 __global__ void __launch_bounds__(kDotThreads) upd_fused_kernel(
     long long n, long long n_owned, const double* __restrict__ Ap, double* r, double* p,
     double* __restrict__ x, const double* sc_rr, double* sc_pAp, const double* pparts,
-    long long npparts, double* partials, double* out, double* flag, unsigned long long* bar,
-    unsigned long long target) {
+    long long npparts, double* partials, double* out, double* flag, GridBar* bar) {
   __shared__ double sh[32];
   __shared__ double pap_sh;
   double pAp;
@@ -256,7 +255,7 @@ __global__ void __launch_bounds__(kDotThreads) upd_fused_kernel(
   }
   s = block_sum(s, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
-  grid_barrier(bar, target);
+  grid_barrier(bar);
   double rn = 0.0;
   for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) rn += __ldcg(partials + b);
   rn = block_sum(rn, sh);
@@ -333,27 +332,59 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
   HOFEM_CUDA(cudaStreamSynchronize(s));
 
   const unsigned vgrid = kDotBlocks;
+  // Whole solve in one persistent cooperative kernel (§8(f) f1): single rank,
+  // fused operator; auto = local problems up to 8 Mi dofs (the launch- and
+  // latency-bound regime), 2 = always.  Convergence is tested every iteration
+  // on the device (check_every does not apply).
+  const bool persist = m->nranks == 1 && fused_supported(op) &&
+                       (op->opt_cg_persist == 2 || (op->opt_cg_persist == 1 && n <= (8LL << 20)));
+  if (persist && !(rr0 == 0.0 && !fixed_iters)) {
+    int* dres = reinterpret_cast<int*>(flag + 1);
+    HOFEM_CUDA(cudaMemsetAsync(dres, 0, 2 * sizeof(int), s));
+    hofem_status st = cg_persistent(op, x, op->d_r, op->d_p, op->d_Ap, rr, max_iter, fixed_iters,
+                                    rel_tol, dres, s);
+    if (st == HOFEM_OK) {
+      int res[2] = {0, 0};
+      HOFEM_CUDA(cudaMemcpyAsync(res, dres, sizeof(res), cudaMemcpyDeviceToHost, s));
+      HOFEM_CUDA(cudaStreamSynchronize(s));
+      const int k = res[0];
+      double rr_last = rr0;
+      if (k > 0) HOFEM_CUDA(cudaMemcpy(&rr_last, rr + k, sizeof(double), cudaMemcpyDeviceToHost));
+      hofem_status status = HOFEM_OK;
+      if (res[1]) status = HOFEM_ERR_BREAKDOWN;
+      else if (!fixed_iters && !(rr_last == 0.0 || sqrt(rr_last) <= rel_tol * sqrt(rr0)))
+        status = HOFEM_NOT_CONVERGED;
+      if (rr_history)
+        HOFEM_CUDA(cudaMemcpy(rr_history, rr, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost));
+      if (stats) {
+        stats->iterations = k;
+        stats->converged = status == HOFEM_OK ? 1 : 0;
+        stats->r0_norm = sqrt(rr0);
+        stats->final_rel_res = rr0 > 0.0 ? sqrt(rr_last / rr0) : 0.0;
+      }
+      if (status == HOFEM_ERR_BREAKDOWN) set_error("hofem_cg: breakdown (p^T A p <= 0) at k=%d", k);
+      if (status == HOFEM_NOT_CONVERGED) set_error("hofem_cg: max_iter=%d reached", max_iter);
+      return status;
+    }
+    if (op->opt_cg_persist == 2) return st;
+    cudaGetLastError();  // e.g. grid not co-resident right now: per-iteration kernels
+  }
   // fused update + p-update (one cooperative kernel) for small single-rank
   // problems; the grid is what the device holds co-resident (<= kDotBlocks)
-  static const int cgfuse_env = [] {
-    // 0 = always separate kernels, 2 = fused at any size, 1 = up to 8 Mi dofs
-    const char* e = getenv("HOFEM_CGFUSE");
-    return e ? atoi(e) : 1;
-  }();
   int ugrid = 0;
-  if (cgfuse_env && m->nranks == 1 && (cgfuse_env == 2 || n <= (8LL << 20))) {
+  if (op->opt_cg_fuse && m->nranks == 1 && (op->opt_cg_fuse == 2 || n <= (8LL << 20))) {
     int per = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, upd_fused_kernel, kDotThreads, 0) ==
             cudaSuccess &&
         per > 0) {
       ugrid = std::min(per * num_sms(), kDotBlocks);
       if (!op->d_bar) {
-        if (cudaMalloc(&op->d_bar, sizeof(unsigned long long)) != cudaSuccess ||
-            cudaMemset(op->d_bar, 0, sizeof(unsigned long long)) != cudaSuccess) {
+        if (cudaMalloc(&op->d_bar, sizeof(GridBar)) != cudaSuccess ||
+            cudaMemset(op->d_bar, 0, sizeof(GridBar)) != cudaSuccess) {
           cudaGetLastError();
+          op->d_bar = nullptr;
           ugrid = 0;
         }
-        op->bar_count = 0;
       }
     } else {
       cudaGetLastError();
@@ -390,13 +421,11 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
       at[0].val.cooperative = 1;
       cfg.attrs = at;
       cfg.numAttrs = 1;
-      const unsigned long long target = op->bar_count + (unsigned long long)ugrid;
       const cudaError_t e =
           cudaLaunchKernelEx(&cfg, upd_fused_kernel, n, no, (const double*)op->d_Ap, op->d_r,
                              op->d_p, x, (const double*)(rr + k), pAp, pparts, npparts,
-                             m->d_partials, rr + k + 1, flag, op->d_bar, target);
+                             m->d_partials, rr + k + 1, flag, op->d_bar);
       if (e == cudaSuccess) {
-        op->bar_count = target;
         count_launch();
         fused_upd = true;
       } else {

@@ -14,14 +14,15 @@
 namespace hofem {
 
 #define HOFEM_FOR_P1(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9)
-#define HOFEM_DECL(P1)                                                                     \
-  template <>                                                                              \
-  bool fused_launch<P1>(int, int, int, const double*, const double*, const ColArgs&, int,  \
-                        cudaStream_t, cudaError_t*);                                       \
-  template <>                                                                              \
-  FusedLaunch fused_shape<P1>(int, int);                                                   \
-  template <>                                                                              \
-  int fused_default_variant<P1>(int);
+#define HOFEM_DECL(P1)                                                                      \
+  template <>                                                                               \
+  bool fused_launch<P1>(int, int, const double*, const double*, const ColArgs&, int, bool,  \
+                        cudaStream_t, cudaError_t*);                                        \
+  template <>                                                                               \
+  bool cg_launch<P1>(int, int, const double*, const double*, const ColArgs&, const CGArgs&, \
+                     int, cudaStream_t, cudaError_t*);                                      \
+  template <>                                                                               \
+  FusedLaunch fused_shape<P1>(int, int);
 HOFEM_FOR_P1(HOFEM_DECL)
 #undef HOFEM_DECL
 
@@ -45,34 +46,11 @@ __global__ void __launch_bounds__(256) dot_partials_kernel(const double* part, l
   block_sum_store(v, out, red);
 }
 
-// Tuning knob HOFEM_FUSED = "mma" | "simt" overrides the per-p default kernel.
-int fused_variant() {
-  static const int v = [] {
-    const char* e = getenv("HOFEM_FUSED");
-    if (!e) return -1;
-    if (!strcmp(e, "mma")) return 0;
-    if (!strcmp(e, "simt")) return 1;
-    return -1;
-  }();
-  return v;
-}
-
-int default_variant(int P1, int kind) {
+FusedLaunch shape_for(int P1, int kind, int Q) {
   switch (P1) {
 #define HOFEM_CASE(P) \
   case P:             \
-    return fused_default_variant<P>(kind);
-    HOFEM_FOR_P1(HOFEM_CASE)
-#undef HOFEM_CASE
-  }
-  return 0;
-}
-
-FusedLaunch shape_for(int P1, int kind, int variant) {
-  switch (P1) {
-#define HOFEM_CASE(P) \
-  case P:             \
-    return fused_shape<P>(kind, variant);
+    return fused_shape<P>(kind, Q);
     HOFEM_FOR_P1(HOFEM_CASE)
 #undef HOFEM_CASE
   }
@@ -174,9 +152,10 @@ long long boundary_points(const Mesh* m) {
   return m->Nx * m->Ny * ((bot ? 1 : 0) + (top ? 1 : 0)) + 2 * m->Nx * nk + 2 * (m->Ny - 2) * nk;
 }
 
+
 namespace {
 struct Plan {
-  int variant, kind;
+  int kind;
   FusedLaunch L;
   int nbx, nby, zc, nchunks, grid;
   long long ncol, nbricks, nunits;
@@ -185,14 +164,7 @@ Plan make_plan(const Op* op) {
   const Mesh* m = op->mesh;
   Plan P;
   P.kind = fused_kind(op);
-  const int v = op->fused_variant >= 0 ? op->fused_variant : fused_variant();
-  // variant: 0 DMMA, 1 SIMT (mass / diffusion / collocated), 2 the older
-  // collocated column kernel (requested as 0 for a collocated operator)
-  if (P.kind == KIND_COLLOC)
-    P.variant = (v < 0 || v == 1) ? 1 : 2;
-  else
-    P.variant = v < 0 ? default_variant(m->P1, P.kind) : v;
-  P.L = shape_for(m->P1, P.kind, P.variant == 2 ? 0 : P.variant);
+  P.L = shape_for(m->P1, P.kind, op->Q);
   P.nbx = (m->nx + P.L.BX - 1) / P.L.BX;
   P.nby = (m->ny + P.L.BY - 1) / P.L.BY;
   P.ncol = (long long)P.nbx * P.nby;
@@ -205,6 +177,111 @@ Plan make_plan(const Op* op) {
   P.grid = (int)(P.nunits < G0 ? P.nunits : G0);
   return P;
 }
+
+// Everything one launch of the fused kernels needs (ColArgs incl. the fix-up's
+// FixArgs), with the operator's scratch buffers sized for it.
+struct Prepared {
+  Plan PL;
+  ColArgs A;
+  long long nfixp = 0, nfixb = 0, npts = 0;
+  bool need_fix = false, zero_y = false;
+};
+
+template <class T>
+hofem_status grow(T** p, long long* len, long long need, const char* what) {
+  if (*len >= need) return HOFEM_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *len = 0;
+  if (cudaMalloc(p, sizeof(T) * need) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("fused apply: out of device memory for %s", what);
+    return HOFEM_ERR_OOM;
+  }
+  *len = need;
+  return HOFEM_OK;
+}
+
+hofem_status ensure_bar(Op* op) {
+  if (op->d_bar) return HOFEM_OK;
+  if (cudaMalloc(&op->d_bar, sizeof(GridBar)) != cudaSuccess ||
+      cudaMemset(op->d_bar, 0, sizeof(GridBar)) != cudaSuccess) {
+    cudaGetLastError();
+    op->d_bar = nullptr;
+    set_error("fused apply: out of device memory for the grid barrier");
+    return HOFEM_ERR_OOM;
+  }
+  return HOFEM_OK;
+}
+
+hofem_status prepare(Op* op, const double* x, double* y, bool fdot, Prepared* out) {
+  Mesh* m = op->mesh;
+  const int p = m->p;
+  Prepared& R = *out;
+  R.PL = make_plan(op);
+  const Plan& PL = R.PL;
+  const FusedLaunch L = PL.L;
+  HOFEM_TRY(grow(&op->d_bbuf, &op->bbuf_len, PL.nbricks * L.face_block,
+                 "the brick-interface buffer"));
+  ColArgs& A = R.A;
+  A = ColArgs{};
+  A.x = x; A.y = y; A.qd = op->d_qdata; A.bbuf = op->d_bbuf;
+  A.nx = m->nx; A.ny = m->ny; A.nzl = m->nzl;
+  A.nbx = PL.nbx; A.nby = PL.nby; A.zc = PL.zc; A.nunits = (int)PL.nunits;
+  A.Nx = m->Nx; A.Ny = m->Ny; A.Nzl = m->Nzl;
+  A.K0 = (long long)p * m->z0; A.NzG = m->NzG;
+  A.bc = op->bc;
+  A.l2pf = op->opt_l2pf ? 1 : 0;
+  // fix-up work: edge-line points, plus the Dirichlet boundary points
+  // (fixup_bnd; same count as bnd_count in fused_impl.cuh)
+  R.nfixp = (long long)(PL.nbx - 1) * (PL.nby - 1) * m->Nzl +
+            (long long)(PL.nbx - 1) * (PL.nchunks - 1) * m->Ny +
+            (long long)(PL.nby - 1) * (PL.nchunks - 1) * m->Nx;
+  if (op->bc) R.nfixp += boundary_points(m);
+  if (R.nfixp >= (1LL << 31)) {  // the fix-up indexes its points in 32 bits
+    set_error("fused apply: %lld fix-up points exceed the 32-bit index range", R.nfixp);
+    return HOFEM_ERR_ARG;
+  }
+  R.need_fix = R.nfixp > 0;
+  R.nfixb = R.need_fix ? (R.nfixp + 255) / 256 : 0;
+  if (fdot) HOFEM_TRY(grow(&op->d_dotp, &op->dotp_len, PL.grid + R.nfixb, "the dot partials"));
+  A.dotp = fdot ? op->d_dotp : nullptr;
+  A.kown = m->n_owned / (m->Nx * m->Ny);
+  FixArgs F;
+  F.x = x; F.y = y; F.bbuf = op->d_bbuf;
+  F.Nx = (int)m->Nx; F.Ny = (int)m->Ny; F.Nzl = (int)m->Nzl; F.K0 = A.K0; F.NzG = m->NzG;
+  F.p = p; F.PX = p * L.BX; F.PY = p * L.BY; F.PZU = p * PL.zc;
+  F.LX = F.PX + 1; F.LY = F.PY + 1;
+  F.nbx = PL.nbx; F.nby = PL.nby; F.nzl = m->nzl; F.bc = op->bc;
+  F.FYS = 2 * (p + 1); F.OY = 0; F.OZ = 2 * F.FYS;  // FaceLayout<>
+  F.FZS = F.LX * F.LY; F.FB = F.OZ + 2 * F.FZS;
+  if (F.FB != L.face_block) {
+    set_error("fused apply: face-block layout mismatch (%d vs %d)", F.FB, L.face_block);
+    return HOFEM_ERR_ARG;
+  }
+  F.nplZ = PL.nchunks - 1; F.nplY = PL.nby - 1; F.nplX = PL.nbx - 1;
+  F.dotp = fdot ? op->d_dotp + PL.grid : nullptr;
+  F.kown = (int)A.kown;
+  A.fx = F;
+  R.npts = m->Nx * m->Ny * m->Nzl;
+  R.zero_y = PL.nbx > 1 || PL.nby > 1 || PL.nchunks > 1;  // face points are reduced into y
+  A.infix = 0;
+  A.zero_n = 0;
+  A.bar = nullptr;
+  return HOFEM_OK;
+}
+
+bool launch_p1(int P1, int kind, const Op* op, const ColArgs& A, int grid, bool coop,
+               cudaStream_t s, cudaError_t* err) {
+  switch (P1) {
+#define HOFEM_CASE(P) \
+  case P:             \
+    return fused_launch<P>(kind, op->Q, op->tab.B, op->tab.G, A, grid, coop, s, err);
+    HOFEM_FOR_P1(HOFEM_CASE)
+#undef HOFEM_CASE
+  }
+  return false;
+}
 }  // namespace
 
 hofem_status fused_info(const Op* op, hofem_fused_info* out) {
@@ -214,10 +291,10 @@ hofem_status fused_info(const Op* op, hofem_fused_info* out) {
   }
   const Mesh* m = op->mesh;
   const Plan P = make_plan(op);
-  out->variant = P.variant;
+  out->variant = 1;
   out->bx = P.L.BX; out->by = P.L.BY; out->zc = P.zc; out->nchunks = P.nchunks;
   out->grid = P.grid;
-  // points on >= 2 interior brick planes (edge lines) go through fixup_kernel
+  // points on >= 2 interior brick planes (edge lines) go through the fix-up
   const long long N = m->Nx * m->Ny * m->Nzl;
   const long long ax = P.nbx - 1, ay = P.nby - 1, az = P.nchunks - 1;
   out->fixup_points = ax * ay * m->Nzl + ax * az * m->Ny + ay * az * m->Nx - 2 * ax * ay * az;
@@ -228,161 +305,60 @@ hofem_status fused_info(const Op* op, hofem_fused_info* out) {
 hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
                          double* dot_out, const double** dot_parts, long long* dot_nparts) {
   Mesh* m = op->mesh;
-  const int P1 = m->P1, p = m->p;
-  const Plan PL = make_plan(op);
-  const int kind = PL.kind, variant = PL.variant == 2 ? 0 : PL.variant;
-  const FusedLaunch L = PL.L;
-  const int nbx = PL.nbx, nby = PL.nby, zc = PL.zc, nchunks = PL.nchunks, grid = PL.grid;
-  const long long nbricks = PL.nbricks, nunits = PL.nunits;
-  if (nbricks == 0) return HOFEM_OK;
-  const long long need = nbricks * L.face_block;
-  if (op->bbuf_len < need) {
-    if (op->d_bbuf) cudaFree(op->d_bbuf);
-    op->d_bbuf = nullptr;
-    op->bbuf_len = 0;
-    if (cudaMalloc(&op->d_bbuf, sizeof(double) * need) != cudaSuccess) {
-      cudaGetLastError();
-      set_error("fused apply: out of device memory for the brick-interface buffer");
-      return HOFEM_ERR_OOM;
-    }
-    op->bbuf_len = need;
-  }
-  ColArgs A;
-  A.x = x; A.y = y; A.qd = op->d_qdata; A.bbuf = op->d_bbuf;
-  A.nx = m->nx; A.ny = m->ny; A.nzl = m->nzl;
-  A.nbx = nbx; A.nby = nby; A.zc = zc; A.nunits = (int)nunits;
-  A.Nx = m->Nx; A.Ny = m->Ny; A.Nzl = m->Nzl;
-  A.K0 = (long long)p * m->z0; A.NzG = m->NzG;
-  A.bc = op->bc;
-  static const int l2pf = [] {
-    const char* e = getenv("HOFEM_L2PF");  // tuning knob: 0 disables the L2 bulk prefetch
-    return e ? atoi(e) : 1;
-  }();
-  A.l2pf = l2pf;
-  // fused x.y: per-CTA partials of the brick kernel, then one per fix-up block
-  const bool fdot = dot_out != nullptr && PL.variant != 2;
-  // fix-up work: edge-line points, plus the Dirichlet boundary points
-  // (fixup_bnd; same count as bnd_count in fused_impl.cuh)
-  long long nfixp = (long long)(nbx - 1) * (nby - 1) * m->Nzl +
-                    (long long)(nbx - 1) * (nchunks - 1) * m->Ny +
-                    (long long)(nby - 1) * (nchunks - 1) * m->Nx;
-  if (op->bc) nfixp += boundary_points(m);
-  if (nfixp >= (1LL << 31)) {  // the fix-up indexes its points in 32 bits
-    set_error("fused apply: %lld fix-up points exceed the 32-bit index range", nfixp);
-    return HOFEM_ERR_ARG;
-  }
-  const bool need_fix = nfixp > 0;
-  const long long nfixb = need_fix ? (nfixp + 255) / 256 : 0;
-  if (fdot && op->dotp_len < grid + nfixb) {
-    if (op->d_dotp) cudaFree(op->d_dotp);
-    op->d_dotp = nullptr;
-    op->dotp_len = 0;
-    if (cudaMalloc(&op->d_dotp, sizeof(double) * (grid + nfixb)) != cudaSuccess) {
-      cudaGetLastError();
-      set_error("fused apply: out of device memory for the dot partials");
-      return HOFEM_ERR_OOM;
-    }
-    op->dotp_len = grid + nfixb;
-  }
-  A.dotp = fdot ? op->d_dotp : nullptr;
-  A.kown = m->n_owned / (m->Nx * m->Ny);
-  FixArgs F;
-  F.x = x; F.y = y; F.bbuf = op->d_bbuf;
-  F.Nx = (int)m->Nx; F.Ny = (int)m->Ny; F.Nzl = (int)m->Nzl; F.K0 = A.K0; F.NzG = m->NzG;
-  F.p = p; F.PX = p * L.BX; F.PY = p * L.BY; F.PZU = p * zc;
-  F.LX = F.PX + 1; F.LY = F.PY + 1;
-  F.nbx = nbx; F.nby = nby; F.nzl = m->nzl; F.bc = op->bc;
-  F.FYS = 2 * (p + 1); F.OY = 0; F.OZ = 2 * F.FYS;  // FaceLayout<>
-  F.FZS = F.LX * F.LY; F.FB = F.OZ + 2 * F.FZS;
-  if (F.FB != L.face_block) {
-    set_error("fused apply: face-block layout mismatch (%d vs %d)", F.FB, L.face_block);
-    return HOFEM_ERR_ARG;
-  }
-  F.nplZ = nchunks - 1; F.nplY = nby - 1; F.nplX = nbx - 1;
-  F.dotp = fdot ? op->d_dotp + grid : nullptr;
-  F.kown = (int)A.kown;
-  // in-kernel fix-up (SIMT kernel; cooperative launch with a grid barrier)
-  static const int infix_env = [] {
-    // tuning knob: 0 = always the separate fixup_kernel, 2 = always in-kernel,
-    // 1 (default) = in-kernel for local meshes up to 8 Mi lattice points
-    const char* e = getenv("HOFEM_INFIX");
-    return e ? atoi(e) : 1;
-  }();
-  // measured (gpurun_out/e15, e16): pays for small (launch/latency-bound)
-  // problems, neutral or slower at ~30M dofs
-  const long long npts = m->Nx * m->Ny * m->Nzl;
-  bool infix = (infix_env == 1 ? npts <= (8LL << 20) : infix_env == 2) &&
-               PL.variant == 1 && need_fix && grid <= nunits;
-  if (infix && !op->d_bar) {
-    if (cudaMalloc(&op->d_bar, sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMemset(op->d_bar, 0, sizeof(unsigned long long)) != cudaSuccess) {
-      cudaGetLastError();
-      set_error("fused apply: out of device memory for the grid barrier");
-      return HOFEM_ERR_OOM;
-    }
-    op->bar_count = 0;
-  }
-  const bool zero_y = nbx > 1 || nby > 1 || nchunks > 1;  // face points are reduced into y
+  const bool fdot = dot_out != nullptr;
+  Prepared R;
+  HOFEM_TRY(prepare(op, x, y, fdot, &R));
+  const Plan& PL = R.PL;
+  if (PL.nbricks == 0) return HOFEM_OK;
+  ColArgs& A = R.A;
+  // in-kernel fix-up (cooperative launch, grid barrier).  Measured (gpurun_out/
+  // e15, e16): pays for small (launch/latency-bound) problems, neutral or
+  // slower at ~30M dofs -- hence the size threshold of the auto setting.
+  bool infix = R.need_fix && (op->opt_infix == 2 || (op->opt_infix == 1 && R.npts <= (8LL << 20)));
+  if (infix) HOFEM_TRY(ensure_bar(op));
   A.infix = infix ? 1 : 0;
   A.bar = op->d_bar;
   // with infix the zeroing of y moves into the kernel too (first barrier)
-  A.zero_n = infix && zero_y ? m->Nx * m->Ny * m->Nzl : 0;
-  const unsigned long long nbar = infix ? (A.zero_n > 0 ? 2ULL : 1ULL) : 0ULL;
-  A.bar_target0 = op->bar_count + (unsigned long long)grid;
-  A.bar_target = op->bar_count + nbar * (unsigned long long)grid;
-  A.fx = F;
-  cudaError_t err = cudaSuccess;
-  bool ok = false;
-  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
-  if (zero_y && A.zero_n == 0) {
+  A.zero_n = infix && R.zero_y ? R.npts : 0;
+  if (R.zero_y && A.zero_n == 0) {
     // single-face points are completed by two-term reductions onto zero
-    HOFEM_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * m->Nx * m->Ny * m->Nzl, s));
+    HOFEM_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * R.npts, s));
   }
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
   if (g_prof.on) {
     ev = {prof_event(), prof_event()};
     cudaEventRecord(ev.first, s);
   }
-  auto launch = [&]() {
-    switch (P1) {
-#define HOFEM_CASE(P)                                                                     \
-  case P:                                                                                 \
-    ok = fused_launch<P>(kind, variant, op->Q, op->tab.B, op->tab.G, A, grid, s, &err); \
-    break;
-      HOFEM_FOR_P1(HOFEM_CASE)
-#undef HOFEM_CASE
-    }
-  };
-  launch();
+  cudaError_t err = cudaSuccess;
+  bool ok = launch_p1(m->P1, PL.kind, op, A, PL.grid, infix, s, &err);
   if (ok && infix && err == cudaErrorCooperativeLaunchTooLarge) {
     // the device cannot hold the whole grid right now (e.g. shared by another
     // context): memset + plain launch, fix-up as its own kernel
     cudaGetLastError();
     infix = false;
     A.infix = 0;
-    err = cudaSuccess;
     if (A.zero_n > 0) {
       A.zero_n = 0;
-      HOFEM_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * m->Nx * m->Ny * m->Nzl, s));
+      HOFEM_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * R.npts, s));
     }
-    launch();
+    ok = launch_p1(m->P1, PL.kind, op, A, PL.grid, false, s, &err);
   }
   if (!ok) {
-    set_error("fused apply: no fused kernel for p=%d Q=%d", p, op->Q);
+    set_error("fused apply: no fused kernel for p=%d Q=%d", m->p, op->Q);
     return HOFEM_ERR_ARG;
   }
   count_launch();
-  if (err != cudaSuccess) return cuda_status(err, "fused column kernel launch");
-  if (infix) op->bar_count = A.bar_target;  // every CTA arrived at each barrier
+  if (err != cudaSuccess) return cuda_status(err, "fused brick kernel launch");
   if (g_prof.on) {
     cudaEventRecord(ev.second, s);
     g_prof.brick.push_back(ev);
   }
-  if (need_fix && !infix) {
+  if (R.need_fix && !infix) {
     if (g_prof.on) {
       ev = {prof_event(), prof_event()};
       cudaEventRecord(ev.first, s);
     }
-    fixup_kernel<<<(unsigned)nfixb, 256, 0, s>>>(F);
+    fixup_kernel<<<(unsigned)R.nfixb, 256, 0, s>>>(A.fx);
     HOFEM_LAUNCHED();
     if (g_prof.on) {
       cudaEventRecord(ev.second, s);
@@ -390,7 +366,7 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
     }
   }
   if (fdot) {
-    const long long nparts = grid + (need_fix && !infix ? nfixb : 0);
+    const long long nparts = PL.grid + (R.need_fix && !infix ? R.nfixb : 0);
     if (dot_parts && dot_nparts) {
       *dot_parts = op->d_dotp;  // summed by the caller's kernel, same fixed order
       *dot_nparts = nparts;
@@ -399,8 +375,57 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
       HOFEM_LAUNCHED();
     }
   }
-  HOFEM_TRY(exchange_planes(op, x, y, s));
-  if (dot_out && !fdot) return dot_local(m, x, y, dot_out, s);  // owned dofs, after exchange
+  return exchange_planes(op, x, y, s);
+}
+
+hofem_status cg_persistent(Op* op, double* x, double* r, double* p, double* Ap, double* rr,
+                           int max_iter, int fixed, double rel_tol, int* d_result,
+                           cudaStream_t s) {
+  Mesh* m = op->mesh;
+  if (m->nranks != 1 || !fused_supported(op)) {
+    set_error("persistent CG: single rank, fused operator only");
+    return HOFEM_ERR_ARG;
+  }
+  Prepared R;
+  HOFEM_TRY(prepare(op, p, Ap, false, &R));
+  const Plan& PL = R.PL;
+  HOFEM_TRY(ensure_bar(op));
+  HOFEM_TRY(grow(&op->d_cgparts, &op->cgparts_len, 2LL * PL.grid, "the CG partials"));
+  ColArgs& A = R.A;
+  A.infix = 1;
+  A.zero_n = 0;  // the CG kernel zeroes Ap itself
+  A.bar = op->d_bar;
+  A.dotp = nullptr;
+  A.fx.dotp = nullptr;
+  CGArgs G;
+  G.n = m->n_local;
+  G.x = x; G.r = r; G.p = p; G.Ap = Ap; G.rr = rr;
+  G.parts = op->d_cgparts;
+  G.parts2 = op->d_cgparts + PL.grid;
+  G.result = d_result;
+  G.max_iter = max_iter;
+  G.fixed = fixed;
+  G.rel_tol = rel_tol;
+  G.zero_ap = R.zero_y ? 1 : 0;
+  cudaError_t err = cudaSuccess;
+  bool ok = false;
+  switch (m->P1) {
+#define HOFEM_CASE(P)                                                                   \
+  case P:                                                                               \
+    ok = cg_launch<P>(PL.kind, op->Q, op->tab.B, op->tab.G, A, G, PL.grid, s, &err); \
+    break;
+    HOFEM_FOR_P1(HOFEM_CASE)
+#undef HOFEM_CASE
+  }
+  if (!ok) {
+    set_error("persistent CG: no fused kernel for p=%d Q=%d", m->p, op->Q);
+    return HOFEM_ERR_ARG;
+  }
+  if (err != cudaSuccess) {
+    cudaGetLastError();
+    return cuda_status(err, "persistent CG kernel launch");
+  }
+  count_launch();
   return HOFEM_OK;
 }
 

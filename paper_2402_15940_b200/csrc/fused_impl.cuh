@@ -35,15 +35,6 @@
 
 #include "internal.h"
 
-#ifndef HOFEM_QLD
-#define HOFEM_QLD 1  // qdata register loads: 1 = __ldg, 2 = L1 no-allocate, 0 = L2 evict-first
-#endif
-#ifndef HOFEM_DEARLY
-#define HOFEM_DEARLY 0  // 1: tile-0 D values loaded at brick start; 0: at stage-3 start
-#endif
-#ifndef HOFEM_DBG_SKIP
-#define HOFEM_DBG_SKIP 0  // timing ablation only (wrong results): 1 epilogue, 2 D loads, 4 DMMAs, 8 face reductions
-#endif
 #ifndef HOFEM_SIMT_DSMEM
 #define HOFEM_SIMT_DSMEM -1  // SIMT: D staged in smem (1), from L2 in registers (0), per p (-1)
 #endif
@@ -78,9 +69,6 @@
 #ifndef HOFEM_SIMT_ENDBAR
 #define HOFEM_SIMT_ENDBAR -1  // SIMT: 1 = barrier at the end of every brick, 0 = folded (see
                                // kernel), -1 = per kind (measured, gpurun_out/e17)
-#endif
-#ifndef HOFEM_APF
-#define HOFEM_APF 0  // 1: stage 3 loads the next tile's A fragments before this tile's MMAs
 #endif
 
 namespace hofem {
@@ -331,13 +319,11 @@ struct ColArgs {
   // in-kernel fix-up (SIMT kernel, cooperative launch): after all bricks, a grid
   // barrier, then the edge points of fx
   int infix;
-  unsigned long long* bar;       // grid-barrier counter (monotonic)
-  unsigned long long bar_target; // its value once every CTA of this launch arrived
+  GridBar* bar;           // self-resetting grid barrier (internal.h)
   FixArgs fx;
-  // with infix: y (ny doubles) zeroed in-kernel before a first grid barrier
-  // (target bar_target0) instead of a cudaMemsetAsync
+  // with infix: y (zero_n doubles) zeroed in-kernel before a first grid barrier
+  // instead of a cudaMemsetAsync
   long long zero_n;
-  unsigned long long bar_target0;
 };
 
 // Fixed-order block sum; thread 0 stores it to *out.  All threads must call.
@@ -363,15 +349,6 @@ __device__ __forceinline__ void block_sum_store(double v, double* out, double* r
 
 enum { KIND_MASS = 0, KIND_DIFF = 1, KIND_COLLOC = 2 };
 
-__device__ __forceinline__ double ld_stream(const double* p) {
-  double v;
-  asm volatile(
-      "{ .reg .b64 pol; createpolicy.fractional.L2::evict_first.b64 pol, 1.0;"
-      " ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], pol; }"
-      : "=d"(v)
-      : "l"(p));
-  return v;
-}
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -391,40 +368,6 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
 }
 
-template <int KIND, int P1, int Q, int BX, int BY>
-struct Cfg {
-  static constexpr int p = P1 - 1;
-  static constexpr int NE = BX * BY;
-  static constexpr int LX = p * BX + 1, LY = p * BY + 1, LZ = P1;
-  static constexpr int BLAT = LX * LY * LZ;  // dense brick lattice (partial-buffer layout)
-  // x lattice in smem is x-SLOWEST: L[i][j][k] = k + LZ*j + LXS*i; stage 1 (lanes
-  // over (b,c), c fastest) reads nearly contiguous doubles; LXS odd.
-  static constexpr int LXS = ((LY * LZ) % 2 == 0) ? LY * LZ + 1 : LY * LZ;
-  static constexpr int LAT = LXS * LX;
-  static constexpr int Qp = (Q % 2 == 0) ? Q + 1 : Q;  // odd c-stride in T1
-  static constexpr int S2 = Qp * P1;                   // b-stride in T1
-  static constexpr int NT1 = (KIND == KIND_MASS) ? 1 : 2;
-  static constexpr int NT2 = (KIND == KIND_MASS) ? 1 : 3;
-  static constexpr int T1N = NT1 * S2 * P1;
-  // T2[comp][qy][c][qx]: qy-stride RS >= Q*P1, RS == Q (mod 16): stage-2 writes
-  // (lanes over qx + Q c) and stage-3 reads (lanes over qx + Q qy) are both
-  // conflict-free.
-  static constexpr int RS = Q * P1 + (((Q - Q * P1) % 16) + 16) % 16;
-  static constexpr int T2C = Q * RS;
-  static constexpr int T2N = NT2 * T2C;
-  static constexpr int SA = ((P1 * P1) % 2 == 0) ? P1 * P1 + 1 : P1 * P1;  // a-stride of y_e
-  static constexpr int YEN = (KIND == KIND_COLLOC) ? P1 * P1 * P1 : SA * P1;
-  static constexpr int WN = 3 * P1 * P1 * P1;  // collocated: w per element
-  static constexpr int cmax(int a, int b) { return a > b ? a : b; }
-  static constexpr int REGA = (KIND == KIND_COLLOC) ? NE * YEN : cmax(NE * T2N, NE * YEN);
-  static constexpr int REGB = (KIND == KIND_COLLOC) ? NE * WN : NE * T1N;
-  static constexpr int CARRY = LX * LY;
-  static constexpr int SMEM_BYTES = (REGA + REGB + 2 * LAT + 2 * CARRY) * 8;
-  static constexpr int NC = (KIND == KIND_MASS) ? 1 : 6;
-  static constexpr int NQ1 = (KIND == KIND_COLLOC) ? P1 : Q;  // points per 1D direction
-  static constexpr int ITEMS3 = NE * NQ1 * NQ1;              // stage-3 items
-  __device__ static constexpr int lat(int i, int j, int k) { return k + LZ * j + LXS * i; }
-};
 
 // ---------------------------------------------------------------------------
 // a4: items are (lattice row (j,k), element column s): a thread loads the row's
@@ -504,10 +447,7 @@ struct FaceLayout {
 };
 
 __device__ __forceinline__ void red_add(double* p, double v) {
-  if (HOFEM_DBG_SKIP & 8)
-    *p = v;  // timing ablation only (wrong results): face points stored, not reduced
-  else
-    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
 struct EpiRow {
@@ -787,44 +727,6 @@ __device__ __forceinline__ int stage_off(const ColArgs& A, int ex, int ey, int e
   return (int)(((e * per) & 15LL) >> 3);
 }
 
-// ---------------------------------------------------------------------------
-// Tensor-core (DMMA) kernel: mass (BP1) and diffusion (BP3), any (P1, Q).
-//
-// Each 1D contraction of the sum factorization is a small FP64 GEMM on the
-// tensor cores (mma.sync.m16n8k8.f64): rows = the brick's element "lines" (the
-// two untouched axes, batched over its NE elements), k = the contracted axis,
-// n = the output axis; the 1D matrix is the B operand (fragments built once per
-// stage from the constant bank).  Stage outputs go through shared memory in
-// [k][row] layouts whose k-stride is 4 (mod 16) doubles, so A-fragment loads are
-// bank-conflict-free.  Stage 3 keeps the z forward contraction, the pointwise D
-// and the z backward contraction in registers: the accumulator fragment of the
-// forward GEMM is reused as the A fragment of the backward GEMM by relabelling
-// its k index (qz = 2t, 2t+1 -> k = t, t+4), with the backward B operand
-// permuted accordingly.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void dmma(double (&d)[4], const double (&a)[4], const double (&b)[2]) {
-  if (HOFEM_DBG_SKIP & 4) {
-    d[0] += a[0] * b[0]; d[1] += a[1] * b[1]; d[2] += a[2]; d[3] += a[3];
-    return;
-  }
-  asm volatile(
-      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
-      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
-}
-
-constexpr int mod16_4(int n) { return n + (((4 - n) % 16) + 16) % 16; }  // >= n, == 4 (mod 16)
-
-// B-operand fragment of a 1D table M (rows x cols, row-major) for GEMM n index
-// `n` and k index `k`: value M[n][k] if TRANS == false (k runs over the table's
-// columns), M[k][n] if TRANS.  Out-of-range entries are zero padding.
-template <int ROWS, int COLS, bool TRANS>
-__device__ __forceinline__ double tabv(const double* M, int n, int k) {
-  const int r = TRANS ? k : n, c = TRANS ? n : k;
-  return (r < ROWS && c < COLS) ? M[r * COLS + c] : 0.0;
-}
-
 // Thread 0: warm L2 with brick b's qdata (one bulk prefetch per element).
 template <class C, int BX, int BY>
 __device__ __forceinline__ void prefetch_qdata_l2(const ColArgs& A, const Brick& b) {
@@ -853,487 +755,6 @@ __device__ __forceinline__ void prefetch_qdata_l2(const ColArgs& A, const Brick&
 }
 
 // ---------------------------------------------------------------------------
-// Warp-per-element tensor-core kernel (mass / diffusion).
-//
-// One warp runs ITS element's whole pipeline; stage outputs live in the warp's
-// private shared-memory region, so stages are separated by __syncwarp only.
-// GEMM rows are element-aligned and padded to 16 (compile-time tile
-// structure); every lane's shared-memory offsets are brick-invariant.  All
-// padding (rows, k slots, lattice columns) is zero-initialised once and never
-// written, so fragment loads need no predicates -- only stores are guarded.
-// ---------------------------------------------------------------------------
-template <int KIND, int P1, int Q, int BX, int BY>
-struct CfgE {
-  static constexpr int p = P1 - 1, P = P1, NE = BX * BY;
-  static constexpr int LX = p * BX + 1, LY = p * BY + 1, LZ = P1;
-  static constexpr int BLAT = LX * LY * LZ;
-  static constexpr int KP = (P + 7) / 8, KQ = (Q + 7) / 8;  // k-steps over P / Q
-  static constexpr int LXS = mod16_4(LY * LZ);               // lattice x-stride
-  static constexpr int LAT = LXS * LX;
-  static constexpr int R1 = P * P, R2 = Q * P, R3 = Q * Q;   // GEMM rows per element
-  static constexpr int M1 = (R1 + 15) / 16, M2 = (R2 + 15) / 16, M3 = (R3 + 15) / 16;
-  static constexpr int cmax(int a, int b) { return a > b ? a : b; }
-  // k-major arrays [k][row]: row stride == 4 (mod 16) doubles; padded rows are
-  // clamped on load and never stored, padded k slots are predicated to zero.
-  static constexpr int KS1 = mod16_4(R1);                    // R  [qx][r1]
-  static constexpr int KS2 = mod16_4(R2);                    // T1 [b][r2]
-  static constexpr int KS3 = mod16_4(R3);                    // T2 [c][r3]
-  static constexpr int NA = (KIND == KIND_MASS) ? 1 : 2;
-  static constexpr int NB = (KIND == KIND_MASS) ? 1 : 3;
-  static constexpr int T1A = cmax(P * KS2, Q * KS1);
-  static constexpr int T2A = P * KS3;
-  static constexpr int SA = ((P * P) % 2 == 0) ? P * P + 1 : P * P;
-  static constexpr int YEN = SA * P;
-  static constexpr int W1 = NA * T1A, W2 = cmax(NB * T2A, YEN);
-  static constexpr int WS = W1 + W2;  // doubles per warp (element)
-  static constexpr int CARRY = LX * LY;
-  static constexpr int SMEM_DOUBLES = NE * WS + 2 * LAT + 2 * CARRY;
-  static constexpr int SMEM_BYTES = SMEM_DOUBLES * 8;
-  static constexpr int NC = (KIND == KIND_MASS) ? 1 : 6;
-  static constexpr int NQ1 = Q;
-  __device__ static constexpr int lat(int i, int j, int k) { return k + LZ * j + LXS * i; }
-};
-
-__device__ __forceinline__ unsigned long long evict_first_policy() {
-  unsigned long long pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ double ld_policy(const double* ptr, unsigned long long pol) {
-#if HOFEM_QLD == 1
-  (void)pol;
-  return __ldg(ptr);  // L1-allocating read-only load, normal L2 priority
-#elif HOFEM_QLD == 2
-  double v;
-  (void)pol;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(ptr));
-  return v;
-#else
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
-               : "=d"(v)
-               : "l"(ptr), "l"(pol));
-  return v;
-#endif
-}
-
-template <int KIND, int P1, int Q, int BX, int BY, int MINB>
-__global__ void __launch_bounds__(32 * BX * BY, MINB)
-    fused_elem_mma(const __grid_constant__ Tab<P1, Q> T, const __grid_constant__ ColArgs A) {
-  using C = CfgE<KIND, P1, Q, BX, BY>;
-  constexpr int NE = C::NE, NT = 32 * NE;
-  constexpr int P = P1, p = P1 - 1;
-  constexpr int KP = C::KP, KQ = C::KQ, NPT = KP, NQT = KQ;
-  constexpr int Q2 = Q * Q, Q3 = Q * Q * Q;
-  constexpr bool DIFF = KIND == KIND_DIFF;
-  constexpr int NA = C::NA, NB = C::NB, NC = C::NC;
-  constexpr int M1 = C::M1, M2 = C::M2, M3 = C::M3;
-  extern __shared__ __align__(16) double smem[];
-  double* LB = smem + NE * C::WS;
-  double* CY = LB + 2 * C::LAT;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
-  double* W1 = smem + warp * C::WS;  // T1 / R arrays
-  double* W2 = W1 + C::W1;           // T2 / S arrays; y_e
-  const int exl = warp % BX, eyl = warp / BX;
-  const unsigned long long pol = evict_first_policy();
-
-  FOR_ITEMS(i, C::SMEM_DOUBLES, NT, tid) smem[i] = 0.0;
-  cta_sync();
-
-  Brick cur = unit_first(A, blockIdx.x);
-  if (cur.u >= A.nunits) {
-    if (A.dotp && threadIdx.x == 0) A.dotp[blockIdx.x] = 0.0;
-    return;
-  }
-  prefetch_qdata_l2<C, BX, BY>(A, cur);
-  issue_lattice<C, NT, BX>(A, LB, (long long)p * cur.bx * BX, (long long)p * cur.by * BY,
-                           (long long)p * cur.ez);
-  cp_async_wait_all();
-  cta_sync();
-
-  double dsum = 0.0;  // this thread's share of x.y (A.dotp)
-  for (int kb = 0; cur.u < A.nunits; ++kb) {
-    const Brick nxt = brick_next(A, cur);
-    const int ex0 = cur.bx * BX, ey0 = cur.by * BY, ez = cur.ez;
-    const long long I0 = (long long)p * ex0, J0 = (long long)p * ey0;
-    const double* L = LB + (kb & 1) * C::LAT;
-    if (nxt.u < A.nunits) {
-      issue_lattice<C, NT, BX>(A, LB + ((kb + 1) & 1) * C::LAT, (long long)p * nxt.bx * BX,
-                               (long long)p * nxt.by * BY, (long long)p * nxt.ez);
-      prefetch_qdata_l2<C, BX, BY>(A, nxt);
-    }
-    const int ex = ex0 + exl, ey = ey0 + eyl;
-    if (ex < A.nx && ey < A.ny) {
-      const double* qde =
-          A.qd + (ex + (long long)A.nx * (ey + (long long)A.ny * ez)) * (long long)(NC * Q3);
-      // D at this lane's stage-3 fragment positions of tile 0 (L2 hits)
-      double dn[NQT][4][NC];
-      auto load_d = [&](int tt, double (&d)[NQT][4][NC]) {
-#pragma unroll
-        for (int nt = 0; nt < NQT; ++nt)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int r = min(16 * tt + g + 8 * (q >> 1), C::R3 - 1);
-            const int qz = min(8 * nt + 2 * t + (q & 1), Q - 1);
-#pragma unroll
-            for (int m = 0; m < NC; ++m)
-              d[nt][q][m] = (HOFEM_DBG_SKIP & 2) ? 1.0 + m * 1e-3 : ld_policy(qde + m * Q3 + qz * Q2 + r, pol);
-          }
-      };
-      if (HOFEM_DEARLY) load_d(0, dn);
-
-      // ---- stage 1: contract x.  rows r1 = (b, c), k = a, n = qx.
-      {
-        double fb[NQT][KP][2], fg[NQT][KP][2];
-#pragma unroll
-        for (int nt = 0; nt < NQT; ++nt)
-#pragma unroll
-          for (int ks = 0; ks < KP; ++ks)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              fb[nt][ks][h] = tabv<Q, P, false>(T.B, 8 * nt + g, 8 * ks + t + 4 * h);
-              fg[nt][ks][h] = DIFF ? tabv<Q, P, false>(T.G, 8 * nt + g, 8 * ks + t + 4 * h) : 0.0;
-            }
-#pragma unroll
-        for (int tt = 0; tt < M1; ++tt) {
-          int lb[2], sb[2];
-          bool ok[2];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int r = 16 * tt + g + 8 * h, rc = min(r, C::R1 - 1);
-            const int b = rc / P, c = rc % P;
-            ok[h] = r < C::R1;
-            lb[h] = C::lat(p * exl + t, p * eyl + b, c);
-            sb[h] = b * C::KS2 + c + 2 * t * P;
-          }
-          double a[KP][4];
-#pragma unroll
-          for (int ks = 0; ks < KP; ++ks)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int k = 8 * ks + t + 4 * (q >> 1);
-              a[ks][q] = k < P ? L[lb[q & 1] + C::LXS * (8 * ks + 4 * (q >> 1))] : 0.0;
-            }
-#pragma unroll
-          for (int m = 0; m < NA; ++m)
-#pragma unroll
-            for (int nt = 0; nt < NQT; ++nt) {
-              double d[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-              for (int ks = 0; ks < KP; ++ks) dmma(d, a[ks], m == 0 ? fb[nt][ks] : fg[nt][ks]);
-              double* out = W1 + m * C::T1A;
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const int h = q >> 1, qx = 8 * nt + 2 * t + (q & 1);
-                if (ok[h] && qx < Q) out[sb[h] + P * (8 * nt + (q & 1))] = d[q];
-              }
-            }
-        }
-      }
-      __syncwarp();
-
-      // ---- stage 2: contract y.  rows r2 = (qx, c), k = b, n = qy.
-      {
-        double fb[NQT][KP][2], fg[NQT][KP][2];
-#pragma unroll
-        for (int nt = 0; nt < NQT; ++nt)
-#pragma unroll
-          for (int ks = 0; ks < KP; ++ks)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              fb[nt][ks][h] = tabv<Q, P, false>(T.B, 8 * nt + g, 8 * ks + t + 4 * h);
-              fg[nt][ks][h] = DIFF ? tabv<Q, P, false>(T.G, 8 * nt + g, 8 * ks + t + 4 * h) : 0.0;
-            }
-#pragma unroll
-        for (int tt = 0; tt < M2; ++tt) {
-          int sb[2];
-          bool ok[2];
-          const int r0 = min(16 * tt + g, C::R2 - 1), r1 = min(16 * tt + g + 8, C::R2 - 1);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int r = 16 * tt + g + 8 * h, rc = min(r, C::R2 - 1);
-            const int qx = rc / P, c = rc % P;
-            ok[h] = r < C::R2;
-            sb[h] = c * C::KS3 + qx + 2 * t * Q;
-          }
-          double aB[KP][4], aG[KP][4];
-#pragma unroll
-          for (int ks = 0; ks < KP; ++ks)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int k = 8 * ks + t + 4 * (q >> 1);
-              const int o = k * C::KS2 + ((q & 1) ? r1 : r0);
-              aB[ks][q] = k < P ? W1[o] : 0.0;
-              aG[ks][q] = (DIFF && k < P) ? W1[C::T1A + o] : 0.0;
-            }
-#pragma unroll
-          for (int nt = 0; nt < NQT; ++nt) {
-            double dBB[4] = {0, 0, 0, 0}, dBG[4] = {0, 0, 0, 0}, dGB[4] = {0, 0, 0, 0};
-#pragma unroll
-            for (int ks = 0; ks < KP; ++ks) {
-              dmma(dBB, aB[ks], fb[nt][ks]);
-              if (DIFF) {
-                dmma(dBG, aB[ks], fg[nt][ks]);
-                dmma(dGB, aG[ks], fb[nt][ks]);
-              }
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int h = q >> 1, qy = 8 * nt + 2 * t + (q & 1);
-              if (ok[h] && qy < Q) {
-                const int o = sb[h] + Q * (8 * nt + (q & 1));
-                if (DIFF) {
-                  W2[o] = dGB[q];              // G_x B_y  (-> u_x)
-                  W2[C::T2A + o] = dBG[q];     // B_x G_y  (-> u_y)
-                  W2[2 * C::T2A + o] = dBB[q]; // B_x B_y  (-> u_z)
-                } else {
-                  W2[o] = dBB[q];
-                }
-              }
-            }
-          }
-        }
-      }
-      __syncwarp();
-
-      // ---- stage 3: contract z, pointwise D, contract back -- in registers.
-      //      rows r3 = (qy, qx) (qx fastest), k = c / permuted qz.
-      {
-        double ff[NQT][KP][2], fz[NQT][KP][2];  // forward: n = qz, k = c
-        double bf[NPT][KQ][2], bz[NPT][KQ][2];  // backward: n = c, k = permuted qz
-#pragma unroll
-        for (int nt = 0; nt < NQT; ++nt)
-#pragma unroll
-          for (int ks = 0; ks < KP; ++ks)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              ff[nt][ks][h] = tabv<Q, P, false>(T.B, 8 * nt + g, 8 * ks + t + 4 * h);
-              fz[nt][ks][h] = DIFF ? tabv<Q, P, false>(T.G, 8 * nt + g, 8 * ks + t + 4 * h) : 0.0;
-            }
-#pragma unroll
-        for (int nt = 0; nt < NPT; ++nt)
-#pragma unroll
-          for (int ks = 0; ks < KQ; ++ks)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              bf[nt][ks][h] = tabv<Q, P, false>(T.B, 8 * ks + 2 * t + h, 8 * nt + g);
-              bz[nt][ks][h] = DIFF ? tabv<Q, P, false>(T.G, 8 * ks + 2 * t + h, 8 * nt + g) : 0.0;
-            }
-        if (!HOFEM_DEARLY) load_d(0, dn);
-        auto load_a = [&](int tt, double (&a)[NB][KP][4]) {
-          const int r0 = min(16 * tt + g, C::R3 - 1), r1 = min(16 * tt + g + 8, C::R3 - 1);
-#pragma unroll
-          for (int m = 0; m < NB; ++m)
-#pragma unroll
-            for (int ks = 0; ks < KP; ++ks)
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const int k = 8 * ks + t + 4 * (q >> 1);
-                a[m][ks][q] = k < P ? W2[m * C::T2A + k * C::KS3 + ((q & 1) ? r1 : r0)] : 0.0;
-              }
-        };
-        double an[NB][KP][4];
-        if (HOFEM_APF) load_a(0, an);
-#pragma unroll
-        for (int tt = 0; tt < M3; ++tt) {
-          double dc[NQT][4][NC];
-#pragma unroll
-          for (int nt = 0; nt < NQT; ++nt)
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-              for (int m = 0; m < NC; ++m) dc[nt][q][m] = dn[nt][q][m];
-          if (tt + 1 < M3) load_d(tt + 1, dn);
-          const int r0 = min(16 * tt + g, C::R3 - 1), r1 = min(16 * tt + g + 8, C::R3 - 1);
-          const bool ok0 = 16 * tt + g < C::R3, ok1 = 16 * tt + g + 8 < C::R3;
-          double a[NB][KP][4];
-          if (HOFEM_APF) {
-#pragma unroll
-            for (int m = 0; m < NB; ++m)
-#pragma unroll
-              for (int ks = 0; ks < KP; ++ks)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) a[m][ks][q] = an[m][ks][q];
-            if (tt + 1 < M3) load_a(tt + 1, an);
-          } else {
-            load_a(tt, a);
-          }
-          double w[NB][NQT][4];
-#pragma unroll
-          for (int nt = 0; nt < NQT; ++nt) {
-            double u[NB][4];
-#pragma unroll
-            for (int m = 0; m < NB; ++m) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q) u[m][q] = 0.0;
-#pragma unroll
-              for (int ks = 0; ks < KP; ++ks)
-                dmma(u[m], a[m][ks], (DIFF && m == 2) ? fz[nt][ks] : ff[nt][ks]);
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const double* dd = dc[nt][q];
-              if (DIFF) {
-                w[0][nt][q] = dd[0] * u[0][q] + dd[1] * u[1][q] + dd[2] * u[2][q];
-                w[1][nt][q] = dd[1] * u[0][q] + dd[3] * u[1][q] + dd[4] * u[2][q];
-                w[2][nt][q] = dd[2] * u[0][q] + dd[4] * u[1][q] + dd[5] * u[2][q];
-              } else {
-                w[0][nt][q] = dd[0] * u[0][q];
-              }
-            }
-          }
-#pragma unroll
-          for (int nt = 0; nt < NPT; ++nt)
-#pragma unroll
-            for (int m = 0; m < NB; ++m) {
-              double sacc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-              for (int ks = 0; ks < KQ; ++ks) {
-                const double aw[4] = {w[m][ks][0], w[m][ks][2], w[m][ks][1], w[m][ks][3]};
-                dmma(sacc, aw, (DIFF && m == 2) ? bz[nt][ks] : bf[nt][ks]);
-              }
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const int c = 8 * nt + 2 * t + (q & 1);
-                if (((q >> 1) ? ok1 : ok0) && c < P)
-                  W2[m * C::T2A + c * C::KS3 + ((q >> 1) ? r1 : r0)] = sacc[q];
-              }
-            }
-        }
-      }
-      __syncwarp();
-
-      // ---- stage 2^T: contract qy.  rows r2 = (qx, c), k = qy, n = b.
-      {
-        double fb[NPT][KQ][2], fg[NPT][KQ][2];
-#pragma unroll
-        for (int nt = 0; nt < NPT; ++nt)
-#pragma unroll
-          for (int ks = 0; ks < KQ; ++ks)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              fb[nt][ks][h] = tabv<Q, P, true>(T.B, 8 * nt + g, 8 * ks + t + 4 * h);
-              fg[nt][ks][h] = DIFF ? tabv<Q, P, true>(T.G, 8 * nt + g, 8 * ks + t + 4 * h) : 0.0;
-            }
-#pragma unroll
-        for (int tt = 0; tt < M2; ++tt) {
-          int lb[2], sb[2];
-          bool ok[2];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int r = 16 * tt + g + 8 * h, rc = min(r, C::R2 - 1);
-            const int qx = rc / P, c = rc % P;
-            ok[h] = r < C::R2;
-            lb[h] = c * C::KS3 + qx + t * Q;
-            sb[h] = qx * C::KS1 + c + 2 * t * P;
-          }
-          double a[NB][KQ][4];
-#pragma unroll
-          for (int m = 0; m < NB; ++m)
-#pragma unroll
-            for (int ks = 0; ks < KQ; ++ks)
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const int k = 8 * ks + t + 4 * (q >> 1);
-                a[m][ks][q] = k < Q ? W2[m * C::T2A + lb[q & 1] + Q * (8 * ks + 4 * (q >> 1))] : 0.0;
-              }
-#pragma unroll
-          for (int nt = 0; nt < NPT; ++nt) {
-            double rg[4] = {0, 0, 0, 0}, rb[4] = {0, 0, 0, 0};
-#pragma unroll
-            for (int ks = 0; ks < KQ; ++ks) {
-              if (DIFF) {
-                dmma(rg, a[0][ks], fb[nt][ks]);  // S_x B_y^T  (-> G_x^T)
-                dmma(rb, a[1][ks], fg[nt][ks]);  // S_y G_y^T  (-> B_x^T)
-                dmma(rb, a[2][ks], fb[nt][ks]);  // S_z B_y^T  (-> B_x^T)
-              } else {
-                dmma(rb, a[0][ks], fb[nt][ks]);
-              }
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int h = q >> 1, b = 8 * nt + 2 * t + (q & 1);
-              if (ok[h] && b < P) {
-                const int o = sb[h] + P * (8 * nt + (q & 1));
-                W1[o] = rb[q];
-                if (DIFF) W1[C::T1A + o] = rg[q];
-              }
-            }
-          }
-        }
-      }
-      __syncwarp();
-
-      // ---- stage 1^T: contract qx.  rows r1 = (b, c), k = qx, n = a -> y_e.
-      {
-        double fb[NPT][KQ][2], fg[NPT][KQ][2];
-#pragma unroll
-        for (int nt = 0; nt < NPT; ++nt)
-#pragma unroll
-          for (int ks = 0; ks < KQ; ++ks)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              fb[nt][ks][h] = tabv<Q, P, true>(T.B, 8 * nt + g, 8 * ks + t + 4 * h);
-              fg[nt][ks][h] = DIFF ? tabv<Q, P, true>(T.G, 8 * nt + g, 8 * ks + t + 4 * h) : 0.0;
-            }
-#pragma unroll
-        for (int tt = 0; tt < M1; ++tt) {
-          int sb[2];
-          bool ok[2];
-          const int r0 = min(16 * tt + g, C::R1 - 1), r1 = min(16 * tt + g + 8, C::R1 - 1);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int r = 16 * tt + g + 8 * h, rc = min(r, C::R1 - 1);
-            const int b = rc / P, c = rc % P;
-            ok[h] = r < C::R1;
-            sb[h] = c + P * b + 2 * t * C::SA;
-          }
-          double aB[KQ][4], aG[KQ][4];
-#pragma unroll
-          for (int ks = 0; ks < KQ; ++ks)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int k = 8 * ks + t + 4 * (q >> 1);
-              const int o = k * C::KS1 + ((q & 1) ? r1 : r0);
-              aB[ks][q] = k < Q ? W1[o] : 0.0;
-              aG[ks][q] = (DIFF && k < Q) ? W1[C::T1A + o] : 0.0;
-            }
-#pragma unroll
-          for (int nt = 0; nt < NPT; ++nt) {
-            double y[4] = {0, 0, 0, 0};
-#pragma unroll
-            for (int ks = 0; ks < KQ; ++ks) {
-              dmma(y, aB[ks], fb[nt][ks]);
-              if (DIFF) dmma(y, aG[ks], fg[nt][ks]);
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int h = q >> 1, a = 8 * nt + 2 * t + (q & 1);
-              if (ok[h] && a < P) W2[sb[h] + C::SA * (8 * nt + (q & 1))] = y[q];
-            }
-          }
-        }
-      }
-    }
-    cta_sync();
-
-    const long long brick = cur.bx + (long long)A.nbx * (cur.by + (long long)A.nby * ez);
-    if (!(HOFEM_DBG_SKIP & 1)) brick_epilogue<C, NT, BX, BY, false, C::WS, C::W1>(
-        A, smem, CY + ((ez + 1) & 1) * C::CARRY, CY + (ez & 1) * C::CARRY, brick, ex0, ey0, I0,
-        J0, (long long)p * ez, ez == cur.z0, ez + 1 == cur.z1, L, dsum);
-    cp_async_wait_all();
-    cta_sync();
-    cur = nxt;
-  }
-  if (A.dotp) block_sum_store(dsum, A.dotp + blockIdx.x, smem);
-}
-
-template <int KIND, int P1, int Q, int BX, int BY>
-constexpr int smem_bytes_elem() {
-  return CfgE<KIND, P1, Q, BX, BY>::SMEM_BYTES;
-}
-
-// ---------------------------------------------------------------------------
 // SIMT kernel (mass / diffusion): thread-per-line sum factorization.
 //
 // Every 1D contraction is an item = one line of the element tensor held in
@@ -1353,6 +774,12 @@ constexpr int smem_bytes_elem() {
 // conflict-free; SP (the T2 point stride) is odd so S3 is conflict-free
 // (scripts/simt_layout.py checks the layouts).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 // Volatile read-only load: stays in program order w.r.t. the other volatile
 // loads, so a register pipeline written in the source is kept.
 __device__ __forceinline__ double ld_nc_v(const double* ptr) {
@@ -1572,9 +999,15 @@ constexpr bool simt_cb() {
       ld_row<P, PR>(T##M##s + (q) * PR, r);           \
   } while (0)
 
+// One pass of the brick pipeline over all of this CTA's work units: y = A x
+// (A.x -> A.y) for the CTA's bricks, edge-line partials to A.bbuf, x.y terms of
+// the values written into dsum.  Shared memory must have been set up by
+// simt_prologue; qbar / qphase carry the D-staging mbarrier state (DSM) across
+// passes.  A CTA without a work unit returns at once.
 template <int KIND, int P1, int Q, int BX, int BY, int NT, int MAXR, bool EO>
-__global__ void __maxnreg__(MAXR)
-    fused_elem_simt(const __grid_constant__ Tab<P1, Q> T, const __grid_constant__ ColArgs A) {
+__device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
+                                          unsigned long long* qbar, unsigned& qphase,
+                                          double& dsum) {
   using C = CfgS<KIND, P1, Q, BX, BY>;
   constexpr int P = P1, p = P1 - 1, NE = C::NE;
   constexpr int Q2 = Q * Q, Q3 = Q * Q * Q;
@@ -1604,34 +1037,11 @@ __global__ void __maxnreg__(MAXR)
   double* TBs = smem + C::TOFF;  // B[q][c], row stride PR (16-byte aligned)
   double* TGs = TBs + Q * PR;
   double* QS = smem + C::QOFF;  // staged D of the current brick (DSM)
-  __shared__ __align__(8) unsigned long long qbar;
-  if (C::DSM && threadIdx.x == 0) {
-    mbar_init(&qbar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-
-  FOR_ITEMS(i, C::SMEM_DOUBLES, NT, threadIdx.x) smem[i] = 0.0;
-  if (A.zero_n > 0) {
-    // y = 0 before any brick adds into it (small problems: no separate memset)
-    const long long st = (long long)gridDim.x * NT;
-    for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < A.zero_n; i += st)
-      A.y[i] = 0.0;
-    grid_barrier(A.bar, A.bar_target0);
-  }
-  cta_sync();
-  FOR_ITEMS(i, Q * P, NT, threadIdx.x) {
-    TBs[(i / P) * PR + i % P] = T.B[i];
-    TGs[(i / P) * PR + i % P] = T.G[i];
-  }
-  cta_sync();
-
+  (void)TBs; (void)TGs; (void)QS; (void)CY;
   Brick cur = unit_first(A, blockIdx.x);
-  if (cur.u >= A.nunits) {  // never with infix: the host launches grid <= units
-    if (A.dotp && threadIdx.x == 0) A.dotp[blockIdx.x] = 0.0;
-    return;
-  }
+  if (cur.u >= A.nunits) return;  // no work unit for this CTA
   if (C::DSM) {
-    issue_qdata<C, BX, BY>(A, cur, QS, &qbar);
+    issue_qdata<C, BX, BY>(A, cur, QS, qbar);
   } else {
     prefetch_qdata_l2<C, BX, BY>(A, cur);
     if (HOFEM_L2PF_AHEAD > 1) prefetch_qdata_l2<C, BX, BY>(A, brick_next(A, cur));
@@ -1640,9 +1050,6 @@ __global__ void __maxnreg__(MAXR)
                            (long long)p * cur.ez);
   cp_async_wait_all();
   cta_sync();
-  unsigned qphase = 0;
-
-  double dsum = 0.0;  // this thread's share of x.y (A.dotp)
   constexpr int DPOL = eo_dpol<P1>();
   unsigned long long dpol = 0;
   if (DPOL) dpol = evict_first_policy();
@@ -1839,7 +1246,7 @@ __global__ void __maxnreg__(MAXR)
     //      Streamed over qz: u(qz) -> w(qz) = D u -> s += B/G(qz) w.  D(qz+1)
     //      is loaded (volatile, in program order) while qz computes.
     if (C::DSM) {
-      mbar_wait(&qbar, qphase);
+      mbar_wait(qbar, qphase);
       qphase ^= 1u;
     }
     FOR_ITEMS(it, NE * Q2, NT, tid) {
@@ -2062,7 +1469,7 @@ __global__ void __maxnreg__(MAXR)
       }
     }
     cta_sync();
-    if (C::DSM) issue_qdata<C, BX, BY>(A, nxt, QS, &qbar);  // D(k) consumed
+    if (C::DSM) issue_qdata<C, BX, BY>(A, nxt, QS, qbar);  // D(k) consumed
 
     // ---- S2T: contract qy.  item (el, qx, c), c fastest.
     FOR_ITEMS(it, NE * Q * P, NT, tid) {
@@ -2233,15 +1640,160 @@ __global__ void __maxnreg__(MAXR)
     }
     cur = nxt;
   }
+}
+
+// Per-launch shared-memory setup: zero everything (padding included), tables
+// into shared memory (non-constant-bank variants), the D-staging mbarrier.
+template <int KIND, int P1, int Q, int BX, int BY, int NT, int MAXR, bool EO>
+__device__ __forceinline__ void simt_prologue(const Tab<P1, Q>& T, unsigned long long* qbar) {
+  using C = CfgS<KIND, P1, Q, BX, BY>;
+  constexpr int P = P1, PR = C::PR;
+  extern __shared__ __align__(16) double smem[];
+  double* TBs = smem + C::TOFF;
+  double* TGs = TBs + Q * PR;
+  if (C::DSM && threadIdx.x == 0) {
+    mbar_init(qbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  FOR_ITEMS(i, C::SMEM_DOUBLES, NT, threadIdx.x) smem[i] = 0.0;
+  cta_sync();
+  FOR_ITEMS(i, Q * P, NT, threadIdx.x) {
+    TBs[(i / P) * PR + i % P] = T.B[i];
+    TGs[(i / P) * PR + i % P] = T.G[i];
+  }
+  cta_sync();
+}
+
+// The fused operator kernel: y = A x over the whole local mesh (persistent
+// grid), then -- with A.infix, in a cooperative launch -- the edge-line fix-up
+// behind a grid barrier; A.zero_n > 0 zeroes y in-kernel first.
+template <int KIND, int P1, int Q, int BX, int BY, int NT, int MAXR, bool EO>
+__global__ void __maxnreg__(MAXR)
+    fused_elem_simt(const __grid_constant__ Tab<P1, Q> T, const __grid_constant__ ColArgs A) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(8) unsigned long long qbar;
+  simt_prologue<KIND, P1, Q, BX, BY, NT, MAXR, EO>(T, &qbar);
+  if (A.zero_n > 0) {
+    // y = 0 before any brick adds into it (small problems: no separate memset)
+    const long long st = (long long)gridDim.x * NT;
+    for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < A.zero_n; i += st)
+      A.y[i] = 0.0;
+    grid_barrier(A.bar);
+  }
+  unsigned qphase = 0;
+  double dsum = 0.0;  // this thread's share of x.y (A.dotp)
+  simt_pass<KIND, P1, Q, BX, BY, NT, MAXR, EO>(T, A, &qbar, qphase, dsum);
   if (A.infix) {
     // all bricks' partials and face reductions are in memory: the edge points
-    grid_barrier(A.bar, A.bar_target);
+    grid_barrier(A.bar);
     const long long nfx = fixup_count(A.fx);
     for (long long g = (long long)blockIdx.x * NT + threadIdx.x; g < nfx;
          g += (long long)gridDim.x * NT)
       dsum += fixup_flat(A.fx, g);
   }
   if (A.dotp) block_sum_store(dsum, A.dotp + blockIdx.x, smem);
+}
+
+// ---------------------------------------------------------------------------
+// Persistent CG (§2.3: "fused ... BP
+// kernels" with Cooperative Groups grid synchronisation): the WHOLE
+// unpreconditioned CG solve of reading R7 in one cooperative launch.  Per
+// iteration k, with rr_k known to every CTA:
+//   pass:  Ap = A p (brick pipeline, y = Ap pre-zeroed), p.Ap terms  | barrier
+//   fix-up of the edge-line / Dirichlet points, p.Ap terms -> parts[cta] | barrier
+//   pAp = sum parts (every CTA, same fixed order); alpha = rr_k / pAp
+//   r -= alpha Ap; r.r terms -> parts2[cta]                           | barrier
+//   rr_{k+1} = sum parts2; beta = rr_{k+1} / rr_k
+//   x += alpha p; p = r + beta p; Ap = 0 (for the next pass)           | barrier
+// Every CTA computes the scalars from the same partials in the same order, so
+// they agree bitwise and take the same stop decision (tolerance, breakdown) --
+// no host round trip, no launch gaps.  Deterministic run to run.
+// ---------------------------------------------------------------------------
+struct CGArgs {
+  long long n;           // local vector length (single rank: all owned)
+  double* x;
+  double* r;
+  double* p;             // == ColArgs::x
+  double* Ap;            // == ColArgs::y
+  double* rr;            // rr[0] (input, r0.r0) .. rr[k] (output)
+  double* parts;         // [gridDim.x] p.Ap partials
+  double* parts2;        // [gridDim.x] r.r partials
+  int* result;           // [0] iterations done, [1] 1 = breakdown (p.Ap <= 0)
+  int max_iter, fixed;
+  double rel_tol;
+  int zero_ap;           // Ap must be zero before each pass (face reductions)
+};
+
+// Fixed-order sum of gridDim.x partials; every thread of every CTA gets the same
+// value.  `red` = blockDim.x doubles of shared scratch.
+template <int NT>
+__device__ __forceinline__ double grid_sum(const double* parts, double* red) {
+  double v = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) v += __ldcg(parts + i);
+  __shared__ double total;
+  block_sum_store(v, &total, red);
+  cta_sync();
+  return total;
+}
+
+template <int KIND, int P1, int Q, int BX, int BY, int NT, int MAXR, bool EO>
+__global__ void __maxnreg__(MAXR)
+    cg_persistent_simt(const __grid_constant__ Tab<P1, Q> T, const __grid_constant__ ColArgs A,
+                       const __grid_constant__ CGArgs G) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(8) unsigned long long qbar;
+  simt_prologue<KIND, P1, Q, BX, BY, NT, MAXR, EO>(T, &qbar);
+  unsigned qphase = 0;
+  const long long st = (long long)gridDim.x * NT;
+  const long long t0 = (long long)blockIdx.x * NT + threadIdx.x;
+  if (G.zero_ap)
+    for (long long i = t0; i < G.n; i += st) G.Ap[i] = 0.0;
+  grid_barrier(A.bar);
+  const double rr0 = __ldcg(G.rr);
+  double rr = rr0;
+  int k = 0;
+  bool brk = false;
+  const bool stop0 = !G.fixed && rr0 == 0.0;
+  while (!stop0 && k < G.max_iter) {
+    double dsum = 0.0;
+    simt_pass<KIND, P1, Q, BX, BY, NT, MAXR, EO>(T, A, &qbar, qphase, dsum);
+    grid_barrier(A.bar);
+    const long long nfx = fixup_count(A.fx);
+    for (long long g = t0; g < nfx; g += st) dsum += fixup_flat(A.fx, g);
+    block_sum_store(dsum, G.parts + blockIdx.x, smem);
+    grid_barrier(A.bar);
+    const double pAp = grid_sum<NT>(G.parts, smem);
+    if (!(pAp > 0.0)) {  // same value in every CTA: all stop here
+      brk = true;
+      break;
+    }
+    const double alpha = rr / pAp;
+    double s = 0.0;
+    for (long long i = t0; i < G.n; i += st) {
+      const double v = fma(-alpha, __ldcg(G.Ap + i), G.r[i]);
+      G.r[i] = v;
+      s = fma(v, v, s);
+    }
+    block_sum_store(s, G.parts2 + blockIdx.x, smem);
+    grid_barrier(A.bar);
+    const double rn = grid_sum<NT>(G.parts2, smem);
+    const double beta = rr > 0.0 ? rn / rr : 0.0;
+    for (long long i = t0; i < G.n; i += st) {
+      const double pv = G.p[i];
+      G.x[i] = fma(alpha, pv, G.x[i]);
+      G.p[i] = fma(beta, pv, G.r[i]);
+      if (G.zero_ap) G.Ap[i] = 0.0;
+    }
+    ++k;
+    rr = rn;
+    if (blockIdx.x == 0 && threadIdx.x == 0) G.rr[k] = rn;
+    if (!G.fixed && (rn == 0.0 || sqrt(rn) <= G.rel_tol * sqrt(rr0))) break;
+    grid_barrier(A.bar);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    G.result[0] = k;
+    G.result[1] = brk ? 1 : 0;
+  }
 }
 
 // SIMT kernel shapes: brick BX x BY elements, NT threads (>= the stage-3 item
@@ -2318,193 +1870,21 @@ template <int KIND, int P1>
 using ShapeSK = std::conditional_t<KIND == KIND_COLLOC, ShapeSC<P1>,
                                    std::conditional_t<KIND == KIND_MASS, ShapeSM<P1>, ShapeS<P1>>>;
 
-// ---------------------------------------------------------------------------
-// Collocated diffusion kernel (BP5: GLL points = nodes, B1d = I, Q = P1).
-// u_x = G_x x, u_y = G_y x, u_z = G_z x; w = D u; y = G_x^T w_x + G_y^T w_y + G_z^T w_z.
-// ---------------------------------------------------------------------------
-template <int P1, int BX, int BY, int NT, int NBUF, int MAXR>
-__global__ void __maxnreg__(MAXR) fused_column_colloc(const __grid_constant__ Tab<P1, P1> T, const __grid_constant__ ColArgs A) {
-  using C = Cfg<KIND_COLLOC, P1, P1, BX, BY>;
-  using SG = Stage<C>;
-  constexpr int p = P1 - 1, NE = C::NE, N2 = P1 * P1, N3 = P1 * P1 * P1;
-  static_assert(NT >= C::ITEMS3, "one item per thread");
-  extern __shared__ __align__(16) double smem[];
-  double* QS = smem;
-  double* RA = QS + NBUF * NE * SG::SLOT;
-  double* RB = RA + C::REGA;
-  double* LB = RB + C::REGB;
-  double* CY = LB + 2 * C::LAT;
-  __shared__ __align__(8) unsigned long long bars[2];
-  const int tid = threadIdx.x;
-  const bool has3 = tid < C::ITEMS3;
-  const int el3 = tid / N2, item = tid % N2, i = item % P1, j = item / P1;
-  if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  cta_sync();
-
-  Brick cur = unit_first(A, blockIdx.x);
-  if (cur.u >= A.nunits) {
-    if (A.dotp && threadIdx.x == 0) A.dotp[blockIdx.x] = 0.0;
-    return;
-  }
-  issue_qdata<C, BX, BY>(A, cur, QS, &bars[0]);
-  issue_lattice<C, NT, BX>(A, LB, (long long)p * cur.bx * BX, (long long)p * cur.by * BY,
-                       (long long)p * cur.ez);
-  cp_async_wait_all();
-  cta_sync();
-  unsigned phase = 0;
-
-  for (int k = 0; cur.u < A.nunits; ++k) {
-    const int tid = vtid();
-    const Brick nxt = brick_next(A, cur);
-    const int ex0 = cur.bx * BX, ey0 = cur.by * BY, ez = cur.ez;
-    const long long I0 = (long long)p * ex0, J0 = (long long)p * ey0;
-    const int qb = NBUF == 2 ? (k & 1) : 0;
-    double* L = LB + (k & 1) * C::LAT;
-    if (nxt.u < A.nunits) {
-      issue_lattice<C, NT, BX>(A, LB + ((k + 1) & 1) * C::LAT, (long long)p * nxt.bx * BX,
-                           (long long)p * nxt.by * BY, (long long)p * nxt.ez);
-      if (NBUF == 2) issue_qdata<C, BX, BY>(A, nxt, QS + ((k + 1) & 1) * NE * SG::SLOT,
-                                            &bars[(k + 1) & 1]);
-    }
-
-    // ---- forward: item (el, i, j), i fastest; z-column k in registers.
-    mbar_wait(&bars[qb], (phase >> qb) & 1);
-    phase ^= 1u << qb;
-    if (has3 && ex0 + el3 % BX < A.nx && ey0 + el3 / BX < A.ny) {
-      const double* xl = L + C::lat(p * (el3 % BX), p * (el3 / BX), 0);
-      const double* dq = QS + (qb * NE + el3) * SG::SLOT + item;
-      double Gi[P1], Gj[P1], xz[P1];
-#pragma unroll
-      for (int a = 0; a < P1; ++a) {
-        Gi[a] = T.G[i * P1 + a];
-        Gj[a] = T.G[j * P1 + a];
-        xz[a] = xl[C::lat(i, j, a)];
-      }
-      double* w = RB + el3 * C::WN + item;
-#pragma unroll
-      for (int kz = 0; kz < P1; ++kz) {
-        double ux = 0.0, uy = 0.0, uz = 0.0;
-#pragma unroll
-        for (int a = 0; a < P1; ++a) {
-          ux = fma(Gi[a], xl[C::lat(a, j, kz)], ux);
-          uy = fma(Gj[a], xl[C::lat(i, a, kz)], uy);
-          uz = fma(T.G[kz * P1 + a], xz[a], uz);
-        }
-        const double* d = dq + kz * N2;
-        const double d00 = d[0], d01 = d[N3], d02 = d[2 * N3], d11 = d[3 * N3], d12 = d[4 * N3],
-                     d22 = d[5 * N3];
-        w[N2 * kz] = d00 * ux + d01 * uy + d02 * uz;
-        w[N3 + N2 * kz] = d01 * ux + d11 * uy + d12 * uz;
-        w[2 * N3 + N2 * kz] = d02 * ux + d12 * uy + d22 * uz;
-      }
-    }
-    cta_sync();
-    if (NBUF == 1 && nxt.u < A.nunits) issue_qdata<C, BX, BY>(A, nxt, QS, &bars[0]);
-
-    // ---- transpose: item (el, a, b) -> y_e[a + P1 b + P1^2 c] for all c.
-    FOR_ITEMS(it, NE * N2, NT, tid) {
-      const int el = it / N2, itm = it % N2, a = itm % P1, b = itm / P1;
-      const double* w = RB + el * C::WN;
-      double Ga[P1], Gb[P1], wz[P1];
-#pragma unroll
-      for (int kz = 0; kz < P1; ++kz) {
-        Ga[kz] = T.G[kz * P1 + a];
-        Gb[kz] = T.G[kz * P1 + b];
-        wz[kz] = w[2 * N3 + itm + N2 * kz];
-      }
-      double* ye = RA + el * C::YEN + itm;
-#pragma unroll
-      for (int c = 0; c < P1; ++c) {
-        double s = 0.0;
-#pragma unroll
-        for (int kz = 0; kz < P1; ++kz) {
-          s = fma(Ga[kz], w[kz + P1 * b + N2 * c], s);      // G_x^T w_x
-          s = fma(Gb[kz], w[N3 + a + P1 * kz + N2 * c], s);  // G_y^T w_y
-          s = fma(T.G[kz * P1 + c], wz[kz], s);              // G_z^T w_z
-        }
-        ye[N2 * c] = s;
-      }
-    }
-    cta_sync();
-
-    const long long brick = cur.bx + (long long)A.nbx * (cur.by + (long long)A.nby * ez);
-    double dsum_unused = 0.0;  // no fused dot for this kernel (A.dotp == nullptr)
-    brick_epilogue<C, NT, BX, BY, true>(A, RA, CY + ((ez + 1) & 1) * C::CARRY,
-                                        CY + (ez & 1) * C::CARRY, brick, ex0, ey0, I0, J0,
-                                        (long long)p * ez, ez == cur.z0, ez + 1 == cur.z1, L,
-                                        dsum_unused);
-    cp_async_wait_all();
-    cta_sync();
-    cur = nxt;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Per-P1 launch configuration: brick BX x BY x 1 elements, threads per CTA (one
-// stage-3 item per thread), qdata staging buffers.
-// ---------------------------------------------------------------------------
-template <int P1>
-struct Shape;
-//                                   BX BY  NT  NBUF  MAXR (registers per thread)
-template <> struct Shape<2> { static constexpr int BX = 8, BY = 4, NT = 288, NBUF = 2, MAXR = 128; };
-template <> struct Shape<3> { static constexpr int BX = 4, BY = 4, NT = 256, NBUF = 2, MAXR = 128; };
-template <> struct Shape<4> { static constexpr int BX = 4, BY = 2, NT = 224, NBUF = 2, MAXR = 128; };
-template <> struct Shape<5> { static constexpr int BX = 2, BY = 2, NT = 160, NBUF = 2, MAXR = 168; };
-template <> struct Shape<6> { static constexpr int BX = 2, BY = 2, NT = 224, NBUF = 2, MAXR = 168; };
-template <> struct Shape<7> { static constexpr int BX = 2, BY = 2, NT = 256, NBUF = 1, MAXR = 168; };
-template <> struct Shape<8> { static constexpr int BX = 2, BY = 1, NT = 192, NBUF = 2, MAXR = 232; };
-template <> struct Shape<9> { static constexpr int BX = 1, BY = 1, NT = 128, NBUF = 2, MAXR = 232; };
-
-template <int KIND, int P1, int Q, int BX, int BY, int NBUF>
-constexpr int smem_bytes() {
-  using C = Cfg<KIND, P1, Q, BX, BY>;
-  return C::SMEM_BYTES + NBUF * C::NE * Stage<C>::SLOT * 8;
-}
-
-// Tensor-core kernel shapes (mass / diffusion): brick = one warp per element,
-// CTAs per SM.
-template <int P1>
-struct ShapeED;
-//                                     BX BY MINB
-template <> struct ShapeED<2> { static constexpr int BX = 4, BY = 2, MINB = 2; };
-template <> struct ShapeED<3> { static constexpr int BX = 4, BY = 2, MINB = 2; };
-template <> struct ShapeED<4> { static constexpr int BX = 4, BY = 2, MINB = 2; };
-template <> struct ShapeED<5> { static constexpr int BX = 2, BY = 2, MINB = 3; };
-template <> struct ShapeED<6> { static constexpr int BX = 2, BY = 2, MINB = 3; };
-template <> struct ShapeED<7> { static constexpr int BX = 2, BY = 2, MINB = 2; };
-template <> struct ShapeED<8> { static constexpr int BX = 2, BY = 1, MINB = 3; };
-template <> struct ShapeED<9> { static constexpr int BX = 2, BY = 1, MINB = 2; };
-// Tuning override: -DHOFEM_SE_P1=6 -DHOFEM_SE_BX=1 -DHOFEM_SE_BY=1 -DHOFEM_SE_MINB=12.
-#ifdef HOFEM_SE_P1
-struct ShapeEOverride {
-  static constexpr int BX = HOFEM_SE_BX, BY = HOFEM_SE_BY, MINB = HOFEM_SE_MINB;
-};
-template <int P1>
-struct ShapeE : std::conditional_t<P1 == HOFEM_SE_P1, ShapeEOverride, ShapeED<P1>> {};
-#else
-template <int P1>
-struct ShapeE : ShapeED<P1> {};
-#endif
-
 struct FusedLaunch {
   int BX, BY, face_block, ctas_per_sm;  // face_block = FaceLayout<>::FB
 };
 
 // Defined per P1 in fused_p.cu: kind in {KIND_MASS, KIND_DIFF, KIND_COLLOC},
-// Q in {P1, P1+1} for MASS/DIFF and Q == P1 for COLLOC.  Returns false if the
-// combination is not instantiated.
-// variant: 0 = tensor-core kernel (fused_elem_mma), 1 = SIMT (fused_elem_simt);
-// ignored for COLLOC.
+// Q in {P1, P1+1} for MASS/DIFF and Q == P1 for COLLOC.  Return false if the
+// combination is not instantiated.  cooperative: launch with
+// cudaLaunchAttributeCooperative (all CTAs co-resident or the launch fails).
 template <int P1>
-bool fused_launch(int kind, int variant, int Q, const double* B, const double* G,
-                  const ColArgs& A, int grid, cudaStream_t s, cudaError_t* err);
+bool fused_launch(int kind, int Q, const double* B, const double* G, const ColArgs& A, int grid,
+                  bool cooperative, cudaStream_t s, cudaError_t* err);
 template <int P1>
-FusedLaunch fused_shape(int kind, int variant);
+bool cg_launch(int kind, int Q, const double* B, const double* G, const ColArgs& A,
+               const CGArgs& CG, int grid, cudaStream_t s, cudaError_t* err);
 template <int P1>
-int fused_default_variant(int kind);
+FusedLaunch fused_shape(int kind, int Q);
 
 }  // namespace hofem

@@ -77,6 +77,13 @@ struct Mesh {
   double* d_send = nullptr;                 // 2 planes staging (copies of own planes)
 };
 
+// Grid-wide barrier state of a cooperative launch: arrival count and
+// generation word (zeroed once at allocation; self-resetting, no host state).
+struct GridBar {
+  unsigned int count;
+  unsigned int gen;
+};
+
 struct Op {
   Mesh* mesh = nullptr;
   int kind = HOFEM_DIFFUSION, rule = HOFEM_GAUSS, Q = 0, nc = 6, bc = 0;
@@ -91,11 +98,17 @@ struct Op {
   // fused brick scratch (boundary partials)
   double* d_bbuf = nullptr;
   long long bbuf_len = 0;
-  int fused_variant = -1;   // -1: HOFEM_FUSED env / per-p default; 0 DMMA; 1 SIMT
   double* d_dotp = nullptr; // per-CTA partials of the fused x.y (CG)
   long long dotp_len = 0;
-  unsigned long long* d_bar = nullptr;  // grid-barrier counter of the in-kernel fix-up
-  unsigned long long bar_count = 0;     // CTAs launched against it so far
+  GridBar* d_bar = nullptr; // self-resetting grid barrier (cooperative launches)
+  double* d_cgparts = nullptr;  // persistent CG: 2 x grid partials
+  long long cgparts_len = 0;
+  // per-operator schedule options (hofem_op_set_option); 0 never, 1 auto (size
+  // threshold, the measured default), 2 always
+  int opt_infix = 1;        // HOFEM_OPT_INFIX: edge-line fix-up inside the brick kernel
+  int opt_cg_fuse = 1;      // HOFEM_OPT_CG_FUSED_UPDATE: one cooperative update kernel
+  int opt_cg_persist = 1;   // HOFEM_OPT_CG_PERSISTENT: whole CG solve in one kernel
+  int opt_l2pf = 1;         // HOFEM_OPT_L2_PREFETCH: bulk-prefetch next brick's qdata
   // CG scratch
   double *d_r = nullptr, *d_p = nullptr, *d_Ap = nullptr;
   double* d_cg = nullptr;   // device CG scalars / history
@@ -125,6 +138,13 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
 // Rank-local a.b over owned dofs into *d_out (device), deterministic; no allreduce.
 hofem_status dot_local(Mesh* m, const double* a, const double* b, double* d_out, cudaStream_t s);
 hofem_status fused_info(const Op* op, hofem_fused_info* out);
+// The whole CG solve (r, p, rr[0] initialised by the caller) in one cooperative
+// kernel (fused.cu / fused_impl.cuh cg_persistent_simt); d_result[0] =
+// iterations, d_result[1] = breakdown flag.  Returns HOFEM_ERR_CUDA with
+// cudaErrorCooperativeLaunchTooLarge if the grid cannot be co-resident.
+hofem_status cg_persistent(Op* op, double* x, double* r, double* p, double* Ap, double* rr,
+                           int max_iter, int fixed, double rel_tol, int* d_result,
+                           cudaStream_t s);
 bool fused_supported(const Op* op);
 
 // ---- comm (comm.cu): sum duplicated interface planes, fix BC there
@@ -141,24 +161,39 @@ inline bool is_ess(const Mesh* m, long long I, long long J, long long Kglob) {
 }
 
 #ifdef __CUDACC__
-// Grid-wide barrier of a cooperative (co-resident) launch on a monotonic
-// 64-bit counter: every CTA adds 1 and waits for `target` (the host keeps the
-// running total of launched CTAs, so the counter is never reset).  Bounded
-// spin: a barrier that cannot complete traps (launch error) instead of
-// hanging the GPU.
-__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long target) {
+// Grid-wide barrier of a cooperative (co-resident) launch.  Self-resetting: each
+// CTA reads the generation word, then arrives on the counter; the last CTA to
+// arrive zeroes the counter and publishes generation + 1, which releases the
+// others.  No host-side state, so a launch may be captured into a CUDA graph and
+// replayed.  The wait is bounded by %globaltimer (20 s): a barrier that cannot
+// complete traps instead of hanging the GPU.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void grid_barrier(GridBar* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    unsigned int g;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(&bar->gen) : "memory");
     __threadfence();
-    atomicAdd(bar, 1ull);
-    unsigned long long v;
-    unsigned spins = 0;
-    do {
-      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
-      if (v >= target) break;
-      __nanosleep(100);
-    } while (++spins < (1u << 25));
-    if (v < target) __trap();
+    const unsigned int arrived = atomicAdd(&bar->count, 1u);
+    if (arrived == gridDim.x - 1) {
+      bar->count = 0u;
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&bar->gen), "r"(g + 1u) : "memory");
+    } else {
+      const unsigned long long t0 = global_ns();
+      unsigned int v;
+      unsigned spins = 0;
+      while (true) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&bar->gen) : "memory");
+        if (v != g) break;
+        if ((++spins & 1023u) == 0u && global_ns() - t0 > 20000000000ull) __trap();
+        __nanosleep(32);
+      }
+    }
     __threadfence();
   }
   __syncthreads();

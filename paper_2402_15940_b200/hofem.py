@@ -20,6 +20,10 @@ MASS, DIFFUSION = 1, 2
 GAUSS, GLL = 1, 2
 BC_NONE, BC_DIRICHLET = 0, 1
 
+# hofem_option
+OPT_INFIX, OPT_CG_FUSED_UPDATE, OPT_CG_PERSISTENT, OPT_L2_PREFETCH = 1, 2, 3, 4
+NEVER, AUTO, ALWAYS = 0, 1, 2
+
 OK, ERR_ARG, ERR_MESH, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_BREAKDOWN, NOT_CONVERGED = range(8)
 _NAMES = ["OK", "ERR_ARG", "ERR_MESH", "ERR_CUDA", "ERR_NCCL", "ERR_OOM", "ERR_BREAKDOWN",
           "NOT_CONVERGED"]
@@ -83,7 +87,8 @@ SIGNATURES = {
     "hofem_dot": (_I, [_V, _V, _V, ctypes.POINTER(_D), _V]),
     "hofem_op_apply_dot": (_I, [_V, _V, _V, ctypes.POINTER(_D), _V]),
     "hofem_op_fused_info": (_I, [_V, ctypes.POINTER(FusedInfo)]),
-    "hofem_op_set_fused_variant": (_I, [_V, _I]),
+    "hofem_op_set_option": (_I, [_V, _I, _I]),
+    "hofem_op_get_option": (_I, [_V, _I, ctypes.POINTER(_I)]),
     "hofem_profile_enable": (_I, [_I]),
     "hofem_profile_read": (_I, [ctypes.POINTER(ProfileStats)]),
     "hofem_launch_count": (_LL, []),
@@ -118,9 +123,18 @@ def _stream(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def _ptr(t: torch.Tensor):
+def _ptr(t: torch.Tensor, n: int | None = None):
+    """Device pointer of a vector argument, after the checks the C ABI relies on:
+    contiguous float64 on the current CUDA device, n elements (when given) and
+    16-byte aligned (hofem.h conventions).  Raises ValueError otherwise."""
     if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
         raise ValueError("expected a contiguous torch.float64 CUDA tensor")
+    if t.device.index != torch.cuda.current_device():
+        raise ValueError(f"tensor on {t.device}, library calls run on cuda:{torch.cuda.current_device()}")
+    if n is not None and t.numel() != n:
+        raise ValueError(f"expected {n} elements, got {t.numel()}")
+    if t.data_ptr() % 16:
+        raise ValueError("tensor data must be 16-byte aligned (e.g. not a view at an odd offset)")
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -193,18 +207,19 @@ class Mesh:
 
     def coords(self, stream=None) -> torch.Tensor:
         out = torch.empty(3 * self.n_local, dtype=torch.float64, device="cuda")
-        _check(lib().hofem_mesh_coords(self.handle, _ptr(out), _stream(stream)))
+        _check(lib().hofem_mesh_coords(self.handle, _ptr(out, 3 * self.n_local), _stream(stream)))
         return out.view(3, self.n_local)
 
     def random(self, seed: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         out = torch.empty(self.n_local, dtype=torch.float64, device="cuda") if out is None else out
-        _check(lib().hofem_fill_random(self.handle, ctypes.c_ulonglong(seed), _ptr(out),
+        _check(lib().hofem_fill_random(self.handle, ctypes.c_ulonglong(seed), _ptr(out, self.n_local),
                                        _stream(stream)))
         return out
 
     def dot(self, a: torch.Tensor, b: torch.Tensor, stream=None) -> float:
         v = ctypes.c_double()
-        _check(lib().hofem_dot(self.handle, _ptr(a), _ptr(b), ctypes.byref(v), _stream(stream)))
+        _check(lib().hofem_dot(self.handle, _ptr(a, self.n_local), _ptr(b, self.n_local),
+                               ctypes.byref(v), _stream(stream)))
         return v.value
 
     def close(self):
@@ -228,31 +243,39 @@ class Operator:
 
     def apply(self, x: torch.Tensor, y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         y = torch.empty_like(x) if y is None else y
-        _check(lib().hofem_op_apply(self.handle, _ptr(x), _ptr(y), _stream(stream)))
+        n = self.mesh.n_local
+        _check(lib().hofem_op_apply(self.handle, _ptr(x, n), _ptr(y, n), _stream(stream)))
         return y
 
     def fused_info(self) -> FusedInfo:
-        """How apply() runs: fused kernel variant (0 DMMA, 1 SIMT, 2 collocated,
-        -1 unfused), brick shape, chunking, direct vs fix-up lattice points."""
+        """How apply() runs: fused kernel variant (1 SIMT brick kernel, -1
+        unfused), brick shape, chunking, direct vs fix-up lattice points."""
         s = FusedInfo()
         _check(lib().hofem_op_fused_info(self.handle, ctypes.byref(s)))
         return s
 
-    def set_fused_variant(self, variant: int):
-        """-1 default, 0 DMMA tensor-core kernel, 1 SIMT kernel."""
-        _check(lib().hofem_op_set_fused_variant(self.handle, int(variant)))
+    def set_option(self, opt: int, value: int):
+        """hofem_op_set_option: OPT_* schedule option, value NEVER/AUTO/ALWAYS."""
+        _check(lib().hofem_op_set_option(self.handle, int(opt), int(value)))
+
+    def get_option(self, opt: int) -> int:
+        v = ctypes.c_int()
+        _check(lib().hofem_op_get_option(self.handle, int(opt), ctypes.byref(v)))
+        return v.value
 
     def apply_dot(self, x: torch.Tensor, y: torch.Tensor | None = None, stream=None):
         """y = A x and x.y over owned dofs (fused into the operator kernels)."""
         y = torch.empty_like(x) if y is None else y
         v = ctypes.c_double()
-        _check(lib().hofem_op_apply_dot(self.handle, _ptr(x), _ptr(y), ctypes.byref(v),
+        n = self.mesh.n_local
+        _check(lib().hofem_op_apply_dot(self.handle, _ptr(x, n), _ptr(y, n), ctypes.byref(v),
                                         _stream(stream)))
         return y, v.value
 
     def apply_unfused(self, x: torch.Tensor, y: torch.Tensor | None = None, stream=None):
         y = torch.empty_like(x) if y is None else y
-        _check(lib().hofem_op_apply_unfused(self.handle, _ptr(x), _ptr(y), _stream(stream)))
+        n = self.mesh.n_local
+        _check(lib().hofem_op_apply_unfused(self.handle, _ptr(x, n), _ptr(y, n), _stream(stream)))
         return y
 
     def qdata(self) -> torch.Tensor:
@@ -262,7 +285,8 @@ class Operator:
 
     def rhs(self, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         out = torch.empty(self.mesh.n_local, dtype=torch.float64, device="cuda") if out is None else out
-        _check(lib().hofem_rhs_manufactured(self.handle, _ptr(out), _stream(stream)))
+        _check(lib().hofem_rhs_manufactured(self.handle, _ptr(out, self.mesh.n_local),
+                                            _stream(stream)))
         return out
 
     def cg(self, b: torch.Tensor, x: torch.Tensor, rel_tol=1e-10, max_iter=1000,
@@ -270,7 +294,8 @@ class Operator:
         """Returns (status, stats, rr_history or None).  x is updated in place."""
         stats = CGStats()
         hist = (ctypes.c_double * (max_iter + 1))() if history else None
-        st = lib().hofem_cg(self.handle, _ptr(b), _ptr(x), rel_tol, max_iter, int(fixed_iters),
+        n = self.mesh.n_local
+        st = lib().hofem_cg(self.handle, _ptr(b, n), _ptr(x, n), rel_tol, max_iter, int(fixed_iters),
                             check_every, hist, ctypes.byref(stats), _stream(stream))
         if st not in (OK, NOT_CONVERGED):
             _check(st)

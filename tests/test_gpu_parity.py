@@ -102,17 +102,17 @@ def oracle_apply(om, kind, rule, x, bc, p, Q=None):
 @pytest.mark.parametrize("nx,ny,nz,p,bench", CASES)
 @pytest.mark.parametrize("bc", [0, 1])
 def test_fused_and_unfused_match_oracle(hf, nx, ny, nz, p, bench, bc):
-    """Both fused kernels (DMMA and SIMT; BP5 has its own collocated kernel)
-    and the unfused path against the oracle."""
+    """The fused brick kernel with both fix-up schedules (separate fix-up kernel
+    after a memset of y; in-kernel fix-up and zeroing behind grid barriers) and
+    the unfused path, against the oracle."""
     m, op, om, kind, rule = make(hf, nx, ny, nz, p, bench, bc=bc)
-    variants = (0, 1)  # bp5: 0 = older column kernel, 1 = SIMT with B = I
     for seed in (1, 2):
         x = m.random(seed)
         ref = oracle_apply(om, kind, rule, host(x), bc, p)
-        for v in variants:
-            op.set_fused_variant(v)
+        for infix in (hf.NEVER, hf.ALWAYS):
+            op.set_option(hf.OPT_INFIX, infix)
             yf = host(op.apply(x))
-            assert rel(yf, ref) <= APPLY_TOL, (v, rel(yf, ref))
+            assert rel(yf, ref) <= APPLY_TOL, (infix, rel(yf, ref))
         yu = host(op.apply_unfused(x))
         assert rel(yu, ref) <= APPLY_TOL, rel(yu, ref)
 
@@ -124,22 +124,23 @@ def test_q_override(hf, p, q, bench):
     m, op, om, kind, rule = make(hf, 3, 2, 2, p, bench, q=q)
     x = m.random(5)
     ref = O.apply_dense(om, kind, rule, host(x), Q=q)
-    for v in (0, 1):
-        op.set_fused_variant(v)
-        assert rel(host(op.apply(x)), ref) <= APPLY_TOL, v
+    for infix in (hf.NEVER, hf.ALWAYS):
+        op.set_option(hf.OPT_INFIX, infix)
+        assert rel(host(op.apply(x)), ref) <= APPLY_TOL, infix
     assert rel(host(op.apply_unfused(x)), ref) <= APPLY_TOL
 
 
-@pytest.mark.parametrize("nx,ny,nz,p,bench,bc,variant", [
-    (5, 3, 4, 2, "bp3", 1, 1), (7, 5, 6, 5, "bp3", 1, 0), (7, 5, 6, 5, "bp3", 1, 1),
-    (5, 3, 3, 3, "bp1", 0, 1), (3, 3, 2, 6, "bp3", 0, 1), (5, 4, 3, 4, "bp5", 1, -1),
-    (5, 4, 3, 4, "bp5", 1, 0), (9, 5, 3, 1, "bp3", 1, 1), (3, 2, 2, 8, "bp3", 1, 1)])
-def test_fused_dot_matches_separate_dot(hf, nx, ny, nz, p, bench, bc, variant):
+@pytest.mark.parametrize("nx,ny,nz,p,bench,bc", [
+    (5, 3, 4, 2, "bp3", 1), (7, 5, 6, 5, "bp3", 1), (5, 3, 3, 3, "bp1", 0),
+    (3, 3, 2, 6, "bp3", 0), (5, 4, 3, 4, "bp5", 1), (9, 5, 3, 1, "bp3", 1),
+    (3, 2, 2, 8, "bp3", 1)])
+@pytest.mark.parametrize("infix", [0, 2])
+def test_fused_dot_matches_separate_dot(hf, nx, ny, nz, p, bench, bc, infix):
     """hofem_op_apply_dot: the x.y accumulated inside the fused kernels equals
     the plain owned-dof dot of the same x and y (and the oracle's x.Ax) up to
     summation order, and y is the ordinary apply."""
     m, op, om, kind, rule = make(hf, nx, ny, nz, p, bench, bc=bc)
-    op.set_fused_variant(variant)
+    op.set_option(hf.OPT_INFIX, infix)
     x = m.random(11)
     y, d = op.apply_dot(x)
     y2 = host(op.apply(x))
@@ -153,10 +154,10 @@ def test_fused_dot_matches_separate_dot(hf, nx, ny, nz, p, bench, bc, variant):
     assert d3 == d  # deterministic
 
 
-@pytest.mark.parametrize("variant", [0, 1])
-def test_fused_bitwise_deterministic(hf, variant):
+@pytest.mark.parametrize("infix", [0, 2])
+def test_fused_bitwise_deterministic(hf, infix):
     m, op, _, _, _ = make(hf, 7, 5, 6, 5, "bp3", bc=1)
-    op.set_fused_variant(variant)
+    op.set_option(hf.OPT_INFIX, infix)
     x = m.random(3)
     y1 = host(op.apply(x))
     for _ in range(3):
@@ -164,20 +165,68 @@ def test_fused_bitwise_deterministic(hf, variant):
         assert np.array_equal(y1.view(np.uint64), y2.view(np.uint64))
 
 
-@pytest.mark.parametrize("bench,p,variant", [("bp3", 5, 0), ("bp3", 5, 1), ("bp1", 3, 1),
-                                             ("bp5", 4, -1), ("bp5", 4, 0), ("bp3", 2, 1)])
-def test_fused_info_partition(hf, bench, p, variant):
+@pytest.mark.parametrize("bench,p", [("bp3", 5), ("bp1", 3), ("bp5", 4), ("bp3", 2)])
+def test_fused_info_partition(hf, bench, p):
     """hofem_op_fused_info: the direct / fix-up split covers every lattice point
-    once, and the reported variant is the one that ran."""
+    once; options round-trip and reject bad values."""
     m, op, _, _, _ = make(hf, 7, 5, 6, p, bench, bc=1)
-    op.set_fused_variant(variant)
     info = op.fused_info()
     assert info.direct_points + info.fixup_points == m.n_local
-    expect = {-1: 1, 0: 2, 1: 1}[variant] if bench == "bp5" else variant
-    assert info.variant == expect
+    assert info.variant == 1
     assert info.grid >= 1 and info.zc * info.nchunks >= 6
+    for opt in (hf.OPT_INFIX, hf.OPT_CG_FUSED_UPDATE, hf.OPT_CG_PERSISTENT):
+        assert op.get_option(opt) == hf.AUTO
+        op.set_option(opt, hf.ALWAYS)
+        assert op.get_option(opt) == hf.ALWAYS
+        with pytest.raises(hf.HofemError):
+            op.set_option(opt, 3)
     with pytest.raises(hf.HofemError):
-        op.set_fused_variant(7)
+        op.set_option(hf.OPT_L2_PREFETCH, 2)
+    with pytest.raises(hf.HofemError):
+        op.set_option(99, 0)
+
+
+@pytest.mark.parametrize("infix", [0, 2])
+def test_apply_graph_replay_bitwise(hf, infix):
+    """hofem_op_apply captured into a CUDA graph and replayed: the in-kernel grid
+    barriers reset themselves (no host-side counter), so every replay and a
+    later eager call give the eager result bit for bit."""
+    m, op, _, _, _ = make(hf, 7, 5, 6, 5, "bp3", bc=1)
+    op.set_option(hf.OPT_INFIX, infix)
+    x = m.random(4)
+    ref = host(op.apply(x))
+    y = torch.empty_like(x)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        op.apply(x, y)  # warm-up (lazy allocations) outside the capture
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        op.apply(x, y)
+    for _ in range(4):
+        y.fill_(7.0)
+        g.replay()
+        assert np.array_equal(host(y).view(np.uint64), ref.view(np.uint64))
+    assert np.array_equal(host(op.apply(x)).view(np.uint64), ref.view(np.uint64))
+
+
+def test_binding_and_abi_reject_bad_vectors(hf):
+    """Wrong length / misaligned vectors never reach a kernel: the binding raises
+    ValueError, the C ABI itself returns HOFEM_ERR_ARG for a misaligned pointer."""
+    import ctypes
+    m, op, _, _, _ = make(hf, 3, 3, 3, 2, "bp3")
+    x = m.random(1)
+    with pytest.raises(ValueError):
+        op.apply(x[:-1])
+    big = torch.zeros(m.n_local + 1, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        op.apply(big[1:], torch.empty_like(x))
+    y = torch.empty(m.n_local + 1, dtype=torch.float64, device="cuda")
+    st = hf.lib().hofem_op_apply(op.handle, ctypes.c_void_p(x.data_ptr()),
+                                 ctypes.c_void_p(y.data_ptr() + 8),
+                                 ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert st == 1
 
 
 def test_affine_extents_and_volume(hf):
@@ -207,10 +256,29 @@ def test_dot_owned(hf):
 
 
 # ----------------------------------------------------------------------------- CG
-def test_cg_config1_iterates(hf):
-    """Config 1 (BP3 2x2x2 p=2, Dirichlet, manufactured RHS): every CG iterate
-    x_k, k <= k_conv, within 1e-10 of the oracle's (reading R14)."""
+# CG schedules (hofem_op_set_option): the whole solve in one persistent kernel;
+# per-iteration kernels with the fused cooperative update and in-kernel fix-up;
+# per-iteration kernels with separate update / p-update / dot and the separate
+# fix-up after a memset (the path large meshes take by default).
+CG_MODES = {
+    "persistent": {"OPT_CG_PERSISTENT": 2},
+    "fused": {"OPT_CG_PERSISTENT": 0, "OPT_CG_FUSED_UPDATE": 2, "OPT_INFIX": 2},
+    "separate": {"OPT_CG_PERSISTENT": 0, "OPT_CG_FUSED_UPDATE": 0, "OPT_INFIX": 0},
+}
+
+
+def set_mode(hf, op, mode):
+    for k, v in CG_MODES[mode].items():
+        op.set_option(getattr(hf, k), v)
+
+
+@pytest.mark.parametrize("mode", list(CG_MODES))
+def test_cg_config1_iterates(hf, mode):
+    """Config 1 (BP3 2x2x2 p=2, Dirichlet, manufactured RHS; 125 dofs, an odd
+    length): every CG iterate x_k, k <= k_conv, within 1e-10 of the oracle's
+    (reading R14), in every CG schedule."""
     m, op, om, kind, rule = make(hf, 2, 2, 2, 2, "bp3", bc=1)
+    set_mode(hf, op, mode)
     b = op.rhs()
     bref = O.rhs(om, kind, rule, bc=1)
     Ae = O.element_matrices(om, kind, rule)
@@ -222,37 +290,56 @@ def test_cg_config1_iterates(hf):
         st, stats, rr = op.cg(b, x, max_iter=k, fixed_iters=True, history=True)
         assert stats.iterations == k
         assert rel(host(x), xh[k]) <= 1e-10, (k, rel(host(x), xh[k]))
+        assert abs(rr[k] - rr_o[k]) <= 1e-10 * rr_o[0], (k, rr[k], rr_o[k])
     x = torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
     st, stats, rr = op.cg(b, x, rel_tol=1e-14, max_iter=200, history=True)
     assert stats.converged and abs(stats.iterations - kconv) <= 1
     assert rel(host(x), xo) <= 1e-12
 
 
-@pytest.mark.parametrize("bench,p,n", [("bp3", 3, 4), ("bp5", 4, 3), ("bp1", 2, 4)])
-def test_cg_iterates_small(hf, bench, p, n):
+@pytest.mark.parametrize("mode", list(CG_MODES))
+@pytest.mark.parametrize("bench,p,n", [("bp3", 3, 4), ("bp5", 4, 3), ("bp1", 2, 4), ("bp3", 5, 3)])
+def test_cg_iterates_small(hf, bench, p, n, mode):
     kind, rule = KINDS[bench]
     bc = 0 if bench == "bp1" else 1
     m, op, om, kind, rule = make(hf, n, n, n, p, bench, bc=bc)
+    set_mode(hf, op, mode)
     b = op.rhs()
     Ae = O.element_matrices(om, kind, rule)
     bo = O.rhs(om, kind, rule, bc=bc)
-    xo, st, kconv, rr_o, _ = O.cg(bo, m=om, Ae=Ae, bc=bc, rel_tol=1e-13, max_iter=500)
+    xo, st, kconv, rr_o, _ = O.cg(bo, m=om, Ae=Ae, bc=bc, rel_tol=1e-13, max_iter=800)
     assert st == 0
     # DESIGN.md reading R14: iterates are compared while ||r_k||/||r_0|| > 1e-4
     # (moderate iteration counts; past that, two correct CG runs drift apart by
     # rounding-driven loss of orthogonality and only re-meet at convergence).
     kwin = next(k for k in range(len(rr_o)) if np.sqrt(rr_o[k] / rr_o[0]) <= 1e-4)
     kmax = min(kwin, 200)
-    _, _, _, _, xh = O.cg(bo, m=om, Ae=Ae, bc=bc, max_iter=kmax, fixed_iters=True, history=True)
-    for k in sorted({1, 5, kmax // 2, kmax}):
+    _, _, _, _, xh = O.cg(bo, m=om, Ae=Ae, bc=bc, max_iter=kmax, fixed_iters=True,
+                          history=True)
+    for k in sorted({1, 2, 5, kmax // 2, kmax}):
         x = torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
         op.cg(b, x, max_iter=k, fixed_iters=True)
         assert rel(host(x), xh[k]) <= 1e-10, k
-    # converged solutions (both to rel-res 1e-13) agree to 1e-12
+    # converged solutions (both to rel-res 1e-13) agree to 1e-11
     x = torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
-    st, stats, _ = op.cg(b, x, rel_tol=1e-13, max_iter=500)
+    st, stats, _ = op.cg(b, x, rel_tol=1e-13, max_iter=800)
     assert st == 0 and abs(stats.iterations - kconv) <= 2
     assert rel(host(x), xo) <= 1e-11
+
+
+@pytest.mark.parametrize("mode", list(CG_MODES))
+def test_cg_schedules_bitwise_deterministic(hf, mode):
+    """Same inputs, same schedule => bitwise-identical iterate (fixed reduction
+    orders everywhere)."""
+    m, op, _, _, _ = make(hf, 5, 4, 3, 3, "bp3", bc=1)
+    set_mode(hf, op, mode)
+    b = op.rhs()
+    xs = []
+    for _ in range(2):
+        x = torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
+        op.cg(b, x, max_iter=30, fixed_iters=True)
+        xs.append(host(x))
+    assert np.array_equal(xs[0].view(np.uint64), xs[1].view(np.uint64))
 
 
 def test_cg_converges_manufactured(hf):
@@ -267,47 +354,121 @@ def test_cg_converges_manufactured(hf):
 
 
 # ----------------------------------------------------------------------------- at scale
-@pytest.mark.parametrize("bench,p", [("bp3", 5), ("bp1", 8), ("bp5", 6)])
-def test_sampled_elements_full_size(hf, bench, p):
-    """Sampled-element parity at the bench's full size:
-    element-interior dofs of y = A x depend on one element only; 256 seeded
-    elements compared against the oracle's dense-B element action."""
+def _contributors(I, J, K, p, n):
+    """Elements (and local node indices) whose closure holds lattice point
+    (I, J, K) of an n^3-element mesh: 1 (interior), 2 (face), 4 (edge), 8."""
+    def axis(L):
+        if L % p == 0:
+            return [(e, L - p * e) for e in (L // p - 1, L // p) if 0 <= e < n]
+        return [(L // p, L % p)]
+    out = []
+    for ez, c in axis(K):
+        for ey, b in axis(J):
+            for ex, a in axis(I):
+                out.append((ex + n * (ey + n * ez), a + (p + 1) * (b + (p + 1) * c)))
+    return out
+
+
+def _sample_points(rng, p, n, bc):
+    """Seeded lattice points of every contribution class: element interiors,
+    x / y / z single-face points (2 elements: the points the fused kernel
+    completes by two-term reductions onto the zeroed y), edge-line points (4:
+    the fix-up's partial sums), vertices (8), and with bc the Dirichlet faces."""
+    N = p * n + 1
+    lo = 1 if bc else 0
+    def coord(on_plane):
+        while True:
+            v = int(rng.integers(lo, N - lo))
+            if (v % p == 0) == on_plane and (not bc or 0 < v < N - 1):
+                return v
+    pts = []
+    if p > 1:
+        pts += [(coord(False), coord(False), coord(False)) for _ in range(96)]
+        for axis in range(3):
+            for _ in range(48):
+                c = [coord(False), coord(False), coord(False)]
+                c[axis] = coord(True)
+                pts.append(tuple(c))
+        for axis in range(3):
+            for _ in range(24):
+                c = [coord(True), coord(True), coord(True)]
+                c[axis] = coord(False)
+                pts.append(tuple(c))
+    pts += [(coord(True), coord(True), coord(True)) for _ in range(32)]
+    if bc:
+        pts += [(0, int(rng.integers(0, N)), int(rng.integers(0, N))) for _ in range(8)]
+        pts += [(int(rng.integers(0, N)), int(rng.integers(0, N)), N - 1) for _ in range(8)]
+    return pts
+
+
+@pytest.mark.parametrize("bench,p,bc", [("bp3", 5, 1), ("bp3", 5, 0), ("bp1", 8, 0),
+                                        ("bp5", 6, 1), ("bp3", 4, 1), ("bp3", 6, 0)])
+def test_sampled_points_full_size(hf, bench, p, bc):
+    """Sampled parity at the bench's full size and launch configuration (SURVEY.md
+    §8(c) "parity at scale"; default options, so the memset + separate fix-up
+    path the bench times): y at seeded lattice points of every contribution
+    class against the oracle's dense-B element actions of the 1-8 elements that
+    hold each point, summed; Dirichlet rows y = x (reading R6)."""
     kind, rule = KINDS[bench]
     n = W.bp3_sweep_n(p) if bench != "bp1" else W.bp1_sweep_n(p)
     m = hf.Mesh(n, n, n, p, alpha=W.ALPHA)
-    op = hf.Operator(m, kind=kind, rule=rule)
+    op = hf.Operator(m, kind=kind, rule=rule, bc=bc)
     om = O.Mesh(n, n, n, p, alpha=W.ALPHA)
     x = m.random(11)
     y = host(op.apply(x))
     xh = host(x)
-    rng = np.random.default_rng(7)
-    elems = rng.choice(om.n_elems, 256, replace=False)
-    ye = O.element_apply_sample(om, kind, rule, xh, elems)
-    Nx = p * n + 1
+    N = p * n + 1
+    xz = xh
+    if bc:  # z = x with the Dirichlet entries zeroed (reading R6)
+        xz = xh.reshape(N, N, N).copy()
+        xz[0, :, :] = xz[-1, :, :] = 0.0
+        xz[:, 0, :] = xz[:, -1, :] = 0.0
+        xz[:, :, 0] = xz[:, :, -1] = 0.0
+        xz = xz.reshape(-1)
+    rng = np.random.default_rng(7 + p + 10 * bc)
+    pts = _sample_points(rng, p, n, bc)
+    contrib = {pt: _contributors(*pt, p, n) for pt in pts}
+    elems = np.array(sorted({e for c in contrib.values() for e, _ in c}))
+    ye = O.element_apply_sample(om, kind, rule, xz, elems)
+    row = {e: i for i, e in enumerate(elems)}
+    scale = np.abs(ye).max()
     num = den = 0.0
-    for k, e in enumerate(elems):
-        ex, ey, ez = e % n, (e // n) % n, e // (n * n)
-        for c in range(1, p):
-            for b in range(1, p):
-                for a in range(1, p):
-                    g = (p * ex + a) + Nx * ((p * ey + b) + Nx * (p * ez + c))
-                    r = ye[k, a + (p + 1) * (b + (p + 1) * c)]
-                    num += (y[g] - r) ** 2
-                    den += r ** 2
-    if p > 1:
-        assert np.sqrt(num / den) <= APPLY_TOL
-    # vertex dofs: sum of the 8 neighbouring elements' contributions
-    verts = rng.integers(1, n, size=(32, 3))
-    for (vx, vy, vz) in verts:
-        es, loc = [], []
-        for dz in (0, 1):
-            for dy in (0, 1):
-                for dx in (0, 1):
-                    ex, ey, ez = vx - 1 + dx, vy - 1 + dy, vz - 1 + dz
-                    es.append(ex + n * (ey + n * ez))
-                    loc.append((p * (1 - dx)) + (p + 1) * ((p * (1 - dy)) + (p + 1) * (p * (1 - dz))))
-        ye8 = O.element_apply_sample(om, kind, rule, xh, np.array(es))
-        ref = sum(ye8[i, loc[i]] for i in range(8))
-        g = p * vx + Nx * (p * vy + Nx * p * vz)
-        scale = np.abs(ye8).max()
-        assert abs(y[g] - ref) <= 1e-12 * scale * 8
+    for (I, J, K), c in contrib.items():
+        g = I + N * (J + N * K)
+        if bc and (min(I, J, K) == 0 or max(I, J, K) == N - 1):
+            assert y[g] == xh[g]
+            continue
+        r = sum(ye[row[e], loc] for e, loc in c)
+        assert abs(y[g] - r) <= 1e-12 * scale * len(c), ((I, J, K), len(c), y[g], r)
+        num += (y[g] - r) ** 2
+        den += r ** 2
+    assert np.sqrt(num / den) <= APPLY_TOL
+
+
+def test_cg_full_size_properties(hf):
+    """The bench's CG (BP3 p=5, 62^3 elements, Dirichlet, manufactured RHS) at
+    full size, where the oracle cannot run the solve: x_1 = alpha_0 b with
+    alpha_0 = b.b / b.Ab; after k iterations ||b - A x_k||^2 equals the
+    recurrence's r_k.r_k; the per-iteration schedule (default at this size)
+    and the persistent kernel give the same iterates up to reduction order."""
+    n = W.bp3_sweep_n(5)
+    m = hf.Mesh(n, n, n, 5, alpha=W.ALPHA)
+    op = hf.Operator(m, kind=hf.DIFFUSION, rule=hf.GAUSS, bc=hf.BC_DIRICHLET)
+    b = op.rhs()
+    bb = m.dot(b, b)
+    bAb = m.dot(b, op.apply(b))
+    x = torch.zeros_like(b)
+    op.cg(b, x, max_iter=1, fixed_iters=True)
+    assert rel(host(x), (bb / bAb) * host(b)) <= 1e-12
+    k = 6
+    xs = {}
+    for mode in ("separate", "fused", "persistent"):
+        set_mode(hf, op, mode)
+        x = torch.zeros_like(b)
+        st, stats, rr = op.cg(b, x, max_iter=k, fixed_iters=True, history=True)
+        assert stats.iterations == k
+        r = b - op.apply(x)
+        assert abs(m.dot(r, r) - rr[k]) <= 1e-10 * rr[0], (mode, m.dot(r, r), rr[k])
+        xs[mode] = host(x)
+    assert rel(xs["fused"], xs["separate"]) <= 1e-12
+    assert rel(xs["persistent"], xs["separate"]) <= 1e-12

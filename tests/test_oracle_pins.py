@@ -379,3 +379,83 @@ def test_splitmix64_golden():
     assert [int(v) for v in z] == [int(h, 16) for h in g["seed0_outputs_hex"]]
     x = W.random_vector(5, np.arange(100000))
     assert x.min() >= -1.0 and x.max() < 1.0 and abs(x.mean()) < 0.01
+
+
+# --------------------------------------------------------------------------- round-2 pins
+def test_curved_phi_golden():
+    """Reading R4, hand-evaluated (tests/golden/phi_curved.json): two nodes of the
+    deformed 2x2x2 p=2 mesh.  A transposed cos argument (u_{i-1} instead of
+    u_{i+1}) or a wrong amplitude moves both points by ~0.035."""
+    g = golden("phi_curved.json")
+    n, p, alpha = g["mesh"]["n"], g["mesh"]["p"], g["mesh"]["alpha"]
+    m = O.Mesh(n, n, n, p, alpha=alpha)
+    xyz = O.mesh_coords(m)
+    N = p * n + 1
+    for pt in g["points"]:
+        I, J, K = pt["lattice"]
+        l = I + N * (J + N * K)
+        np.testing.assert_allclose(xyz[:, l], pt["xyz"], rtol=0, atol=2e-16)
+
+
+def _rhs_1d(p, n, rule):
+    """b_i = int_0^1 sin(pi x) l_i(x) dx by the SAME 1D rule the 3D oracle
+    tensorises (Gauss Q = p+2 from numpy's Legendre rule, or GLL Q = p+1 with
+    the mpmath nodes of tests/ref1d.py and weights int l_i), assembled over n
+    affine elements.  On an affine box the 3D rule of a separable integrand is
+    exactly the product of the 1D rules."""
+    nodes_mp = ref1d.gll_nodes_mp(p)
+    L = ref1d.lagrange_polys(nodes_mp)
+    if rule == O.GAUSS:
+        t, w = np.polynomial.legendre.leggauss(p + 2)
+        t, w = (t + 1) / 2, w / 2
+    else:
+        t = np.array([float(v) for v in nodes_mp])
+        w = np.array([float(ref1d._pint01(l)) for l in L])
+    B = np.array([[float(mpmath_polyval(l, tq)) for l in L] for tq in t])  # [q][i]
+    h = 1.0 / n
+    b = np.zeros(p * n + 1)
+    for e in range(n):
+        xq = (e + t) * h
+        b[p * e: p * e + p + 1] += B.T @ (w * h * np.sin(np.pi * xq))
+    return b
+
+
+def mpmath_polyval(coeffs, x):
+    import mpmath
+    return sum(c * mpmath.mpf(x) ** i for i, c in enumerate(coeffs))
+
+
+@pytest.mark.parametrize("kind,rule,p,dims,bc", [
+    (O.DIFFUSION, O.GAUSS, 2, (3, 2, 2), 1), (O.MASS, O.GAUSS, 3, (2, 2, 3), 0),
+    (O.DIFFUSION, O.GLL, 3, (2, 3, 2), 1), (O.MASS, O.GAUSS, 1, (4, 3, 2), 0)])
+def test_rhs_affine_kronecker(kind, rule, p, dims, bc):
+    """Reading R11 on the affine unit cube: f = c * prod sin(pi x_j) with c = 3 pi^2
+    (diffusion) or 1 (mass), so b = c * (b_z (x) b_y (x) b_x) with the 1D vectors
+    of _rhs_1d; Dirichlet rows zeroed (reading R6).  Pins f, its constant, W,
+    detJ, the basis and the assembly of orc_rhs (both branches)."""
+    nx, ny, nz = dims
+    m = O.Mesh(nx, ny, nz, p, alpha=0.0)
+    b = O.rhs(m, kind, rule, bc=bc)
+    c = 3 * np.pi ** 2 if kind == O.DIFFUSION else 1.0
+    ref = c * ref1d.kron3(_rhs_1d(p, nz, rule)[:, None], _rhs_1d(p, ny, rule)[:, None],
+                          _rhs_1d(p, nx, rule)[:, None]).ravel()
+    if bc:
+        ref[O.boundary_mask(m)] = 0.0
+    assert np.abs(b - ref).max() <= 1e-14 * np.abs(ref).max()
+
+
+def test_l2_error_closed_forms():
+    """orc_l2_error: ||0 - u||_{L2} = ||prod sin(pi x_j)|| = (1/2)^{3/2} exactly on
+    the unit cube (affine, and curved, whose discrete domain is still the cube);
+    u_h = 2 u_I gives ~ ||u|| again; a missing square root or weight fails."""
+    exact = 0.5 ** 1.5
+    m = O.Mesh(3, 3, 3, 2, alpha=0.0)
+    z = np.zeros(O.mesh_coords(m).shape[1])
+    assert abs(O.l2_error(m, z, Qover=10) - exact) <= 1e-13
+    mc = O.Mesh(3, 3, 3, 2, alpha=0.1)
+    assert abs(O.l2_error(mc, z, Qover=12) - exact) <= 1e-6
+    X = O.mesh_coords(mc)
+    uI = np.sin(np.pi * X[0]) * np.sin(np.pi * X[1]) * np.sin(np.pi * X[2])
+    e1 = O.l2_error(mc, uI, Qover=12)
+    assert e1 < 0.02 * exact
+    assert abs(O.l2_error(mc, 2 * uI, Qover=12) - exact) <= e1 + 1e-6
