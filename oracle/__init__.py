@@ -58,6 +58,8 @@ def lib():
             "orc_gll": (i, [i, P, P]),
             "orc_gauss": (i, [i, P, P]),
             "orc_tabulate": (i, [i, i, i, P, P]),
+            "orc_dg_mass_matrices": (i, [M, i, P]),
+            "orc_dg_apply": (i, [M, P, P, P]),
             "orc_num_dofs": (ll, [M]),
             "orc_num_elems": (ll, [M]),
             "orc_mesh_coords": (i, [M, P]),
@@ -203,6 +205,27 @@ def element_apply_sample(m: Mesh, kind, rule, x, elems, Q=None):
     if st:
         raise ValueError(f"orc_element_apply_sample status {st}")
     return ye
+
+
+def dg_mass_matrices(m: Mesh, Q=None):
+    """DG (L2, Gauss-Legendre nodal) element mass matrices [E][nd][nd] (f4)."""
+    Q = Q or default_q(m.p, GAUSS)
+    nd = (m.p + 1) ** 3
+    Me = np.zeros((m.n_elems, nd, nd))
+    mc = m.c()
+    st = lib().orc_dg_mass_matrices(ctypes.byref(mc), Q, _p(Me))
+    if st:
+        raise ValueError(f"orc_dg_mass_matrices status {st}")
+    return Me
+
+
+def dg_apply(m: Mesh, Me, x):
+    """y_e = M_e x_e over the element-major DG vector x [E * P1^3]."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros_like(x)
+    mc = m.c()
+    lib().orc_dg_apply(ctypes.byref(mc), _p(Me), _p(x), _p(y))
+    return y
 
 
 def assemble_dense(m: Mesh, Ae):

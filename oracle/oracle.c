@@ -684,6 +684,73 @@ double orc_l2_error(const orc_mesh *m, const double *uh, int Qover) {
 }
 
 /* ------------------------------------------------------------------------- */
+/* DG (L2) mass, SURVEY.md §8(f) f4 (§2.4.1 "matrix-free    */
+/* discontinuous Galerkin"; fig:dgpa-perf "DG mass operators").               */
+/* Space: discontinuous Q_p per element with the nodal basis at the p+1 Gauss- */
+/* Legendre points (reading R16: MFEM's default L2 basis); geometry = the H1   */
+/* mesh's isoparametric map (element_nodes).  No inter-element coupling, so   */
+/* the operator is block diagonal: y_e = M_e x_e with                          */
+/*   M_e[al][be] = sum_q W_q detJ_q psi_al(xi_q) psi_be(xi_q)                  */
+/* by brute-force quadrature (Gauss Q points, reading R2).  DG vectors are    */
+/* element-major [E][P1^3], x fastest inside an element (reading R16).         */
+/* ------------------------------------------------------------------------- */
+int orc_dg_mass_matrices(const orc_mesh *m, int Q, double *Me) {
+  orc_basis bs; /* geometry (GLL nodes) and the quadrature rule */
+  if (basis_build(&bs, m->p, ORC_GAUSS, Q)) return 1;
+  int p = m->p, P1 = bs.P1, nd = bs.nd, nq = bs.nq;
+  double gn[ORC_MAXP1], gw[ORC_MAXP1];
+  if (orc_gauss(P1, gn, gw)) { basis_free(&bs); return 1; }
+  double *psi = (double *)malloc(sizeof(double) * nq * nd); /* [q][al] */
+  for (int qz = 0; qz < Q; ++qz)
+    for (int qy = 0; qy < Q; ++qy)
+      for (int qx = 0; qx < Q; ++qx) {
+        int q = qx + Q * (qy + Q * qz);
+        for (int c = 0; c <= p; ++c)
+          for (int b = 0; b <= p; ++b)
+            for (int a = 0; a <= p; ++a)
+              psi[(long long)q * nd + a + P1 * (b + P1 * c)] =
+                  lagrange(p, gn, a, bs.t[qx]) * lagrange(p, gn, b, bs.t[qy]) *
+                  lagrange(p, gn, c, bs.t[qz]);
+      }
+  long long E = orc_num_elems(m);
+  int bad = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(| : bad)
+  for (long long e = 0; e < E; ++e) {
+    double *X = (double *)malloc(sizeof(double) * 3 * nd);
+    double *A = Me + e * (long long)nd * nd;
+    element_nodes(m, &bs, e, X);
+    memset(A, 0, sizeof(double) * nd * nd);
+    for (int q = 0; q < nq; ++q) {
+      double D[6];
+      if (point_data(&bs, X, q, ORC_MASS, D) <= 0.0) bad = 1;
+      const double *ps = psi + (long long)q * nd;
+      for (int al = 0; al < nd; ++al)
+        for (int be = 0; be < nd; ++be) A[(long long)al * nd + be] += D[0] * ps[al] * ps[be];
+    }
+    free(X);
+  }
+  free(psi);
+  basis_free(&bs);
+  return bad ? 2 : 0;
+}
+
+/* y_e = M_e x_e for every element (block-diagonal DG operator). */
+int orc_dg_apply(const orc_mesh *m, const double *Me, const double *x, double *y) {
+  long long E = orc_num_elems(m);
+  int P1 = m->p + 1, nd = P1 * P1 * P1;
+#pragma omp parallel for schedule(static)
+  for (long long e = 0; e < E; ++e) {
+    const double *A = Me + e * (long long)nd * nd;
+    for (int al = 0; al < nd; ++al) {
+      double s = 0.0;
+      for (int be = 0; be < nd; ++be) s += A[(long long)al * nd + be] * x[e * nd + be];
+      y[e * nd + al] = s;
+    }
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
 /* CG (reading R7).                             */
 /* ------------------------------------------------------------------------- */
 static double dot(long long n, const double *a, const double *b) {
