@@ -156,6 +156,35 @@ hofem_status hofem_fill_random(const void* mesh, unsigned long long seed, double
 
 void hofem_op_destroy(void* op);
 
+/* ------------------------------------------------- DG (L2) mass (§8(f) f4) */
+/* Matrix-free discontinuous Galerkin mass operator on the same hex mesh
+ * (§2.4.1 "matrix-free discontinuous Galerkin"; fig:dgpa-perf
+ * "DG mass operators").  Space: discontinuous Q_p per element with the nodal
+ * basis at the p+1 Gauss-Legendre points (reading R16).  Vectors are
+ * element-major E-vectors of n_local = elems_local * (p+1)^3 doubles: entry
+ * e*(p+1)^3 + a + (p+1)(b + (p+1)c), elements lexicographic (x fastest), local
+ * element e of rank r is global element e + z0*nx*ny.  The operator is block
+ * diagonal, y_e = B^T D_e B x_e, D_e = W detJ at the Gauss points (the BP1
+ * qdata): no inter-element coupling, hence no scatter and no communication.
+ * Geometry: the mesh's isoparametric map.  Only the Gauss rule Q = p+2 is
+ * instantiated (q_override 0 or p+2, else HOFEM_ERR_ARG). */
+typedef struct {
+  long long n_local;    /* E-vector length on this rank */
+  long long n_global;   /* all ranks */
+  long long elems_local;
+  int p, Q, dofs_per_elem;
+  int grid;             /* CTAs of the last apply (0 before the first) */
+} hofem_dg_info;
+/* SYNC.  Builds the DG operator (qdata, tables); HOFEM_ERR_MESH if detJ <= 0. */
+hofem_status hofem_dg_create(void* mesh, int q_override, void* stream, void** dg_out);
+hofem_status hofem_dg_info_get(const void* dg, hofem_dg_info* info_out);
+/* y = M_DG x (one persistent kernel: asynchronous copies of x, one bulk (TMA)
+ * copy of D per element batch, sum factorization, coalesced stores of y). */
+hofem_status hofem_dg_apply(void* dg, const double* x, double* y, void* stream);
+/* R12 random E-vector indexed by the GLOBAL DG dof (global element * (p+1)^3 + node). */
+hofem_status hofem_dg_fill_random(const void* dg, unsigned long long seed, double* x, void* stream);
+void hofem_dg_destroy(void* dg);
+
 /* -------------------------------------------------------------------- CG (a10) */
 typedef struct {
   int iterations;        /* iterations performed */

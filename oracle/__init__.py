@@ -60,6 +60,7 @@ def lib():
             "orc_tabulate": (i, [i, i, i, P, P]),
             "orc_dg_mass_matrices": (i, [M, i, P]),
             "orc_dg_apply": (i, [M, P, P, P]),
+            "orc_dg_apply_sample": (i, [M, i, P, ll, P, P]),
             "orc_num_dofs": (ll, [M]),
             "orc_num_elems": (ll, [M]),
             "orc_mesh_coords": (i, [M, P]),
@@ -226,6 +227,19 @@ def dg_apply(m: Mesh, Me, x):
     mc = m.c()
     lib().orc_dg_apply(ctypes.byref(mc), _p(Me), _p(x), _p(y))
     return y
+
+
+def dg_apply_sample(m: Mesh, x, elems, Q=None):
+    """y_e = M_e x_e for the listed elements of the E-vector x (sampled parity)."""
+    Q = Q or default_q(m.p, GAUSS)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    elems = np.ascontiguousarray(elems, dtype=np.int64)
+    ye = np.zeros((len(elems), (m.p + 1) ** 3))
+    mc = m.c()
+    st = lib().orc_dg_apply_sample(ctypes.byref(mc), Q, _p(x), len(elems), _p(elems), _p(ye))
+    if st:
+        raise ValueError(f"orc_dg_apply_sample status {st}")
+    return ye
 
 
 def assemble_dense(m: Mesh, Ae):

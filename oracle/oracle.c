@@ -694,13 +694,13 @@ double orc_l2_error(const orc_mesh *m, const double *uh, int Qover) {
 /* by brute-force quadrature (Gauss Q points, reading R2).  DG vectors are    */
 /* element-major [E][P1^3], x fastest inside an element (reading R16).         */
 /* ------------------------------------------------------------------------- */
-int orc_dg_mass_matrices(const orc_mesh *m, int Q, double *Me) {
-  orc_basis bs; /* geometry (GLL nodes) and the quadrature rule */
-  if (basis_build(&bs, m->p, ORC_GAUSS, Q)) return 1;
-  int p = m->p, P1 = bs.P1, nd = bs.nd, nq = bs.nq;
+/* psi[q][al] = psi_a(t_qx) psi_b(t_qy) psi_c(t_qz), psi = Lagrange on the P1
+ * Gauss-Legendre points (product formula). */
+static double *dg_basis(const orc_basis *bs) {
+  int p = bs->p, P1 = bs->P1, nd = bs->nd, Q = bs->Q;
   double gn[ORC_MAXP1], gw[ORC_MAXP1];
-  if (orc_gauss(P1, gn, gw)) { basis_free(&bs); return 1; }
-  double *psi = (double *)malloc(sizeof(double) * nq * nd); /* [q][al] */
+  if (orc_gauss(P1, gn, gw)) return NULL;
+  double *psi = (double *)malloc(sizeof(double) * bs->nq * nd);
   for (int qz = 0; qz < Q; ++qz)
     for (int qy = 0; qy < Q; ++qy)
       for (int qx = 0; qx < Q; ++qx) {
@@ -709,25 +709,64 @@ int orc_dg_mass_matrices(const orc_mesh *m, int Q, double *Me) {
           for (int b = 0; b <= p; ++b)
             for (int a = 0; a <= p; ++a)
               psi[(long long)q * nd + a + P1 * (b + P1 * c)] =
-                  lagrange(p, gn, a, bs.t[qx]) * lagrange(p, gn, b, bs.t[qy]) *
-                  lagrange(p, gn, c, bs.t[qz]);
+                  lagrange(p, gn, a, bs->t[qx]) * lagrange(p, gn, b, bs->t[qy]) *
+                  lagrange(p, gn, c, bs->t[qz]);
       }
-  long long E = orc_num_elems(m);
+  return psi;
+}
+
+/* M_e[al][be] = sum_q W_q detJ_q psi_al psi_be (brute force). */
+static int dg_element_matrix(const orc_mesh *m, const orc_basis *bs, const double *psi,
+                             long long e, double *A) {
+  int nd = bs->nd, bad = 0;
+  double *X = (double *)malloc(sizeof(double) * 3 * nd);
+  element_nodes(m, bs, e, X);
+  memset(A, 0, sizeof(double) * nd * nd);
+  for (int q = 0; q < bs->nq; ++q) {
+    double D[6];
+    if (point_data(bs, X, q, ORC_MASS, D) <= 0.0) bad = 1;
+    const double *ps = psi + (long long)q * nd;
+    for (int al = 0; al < nd; ++al)
+      for (int be = 0; be < nd; ++be) A[(long long)al * nd + be] += D[0] * ps[al] * ps[be];
+  }
+  free(X);
+  return bad;
+}
+
+int orc_dg_mass_matrices(const orc_mesh *m, int Q, double *Me) {
+  orc_basis bs; /* geometry (GLL nodes) and the quadrature rule */
+  if (basis_build(&bs, m->p, ORC_GAUSS, Q)) return 1;
+  double *psi = dg_basis(&bs);
+  if (!psi) { basis_free(&bs); return 1; }
+  long long E = orc_num_elems(m), nd2 = (long long)bs.nd * bs.nd;
   int bad = 0;
 #pragma omp parallel for schedule(dynamic, 1) reduction(| : bad)
-  for (long long e = 0; e < E; ++e) {
-    double *X = (double *)malloc(sizeof(double) * 3 * nd);
-    double *A = Me + e * (long long)nd * nd;
-    element_nodes(m, &bs, e, X);
-    memset(A, 0, sizeof(double) * nd * nd);
-    for (int q = 0; q < nq; ++q) {
-      double D[6];
-      if (point_data(&bs, X, q, ORC_MASS, D) <= 0.0) bad = 1;
-      const double *ps = psi + (long long)q * nd;
-      for (int al = 0; al < nd; ++al)
-        for (int be = 0; be < nd; ++be) A[(long long)al * nd + be] += D[0] * ps[al] * ps[be];
+  for (long long e = 0; e < E; ++e) bad |= dg_element_matrix(m, &bs, psi, e, Me + e * nd2);
+  free(psi);
+  basis_free(&bs);
+  return bad ? 2 : 0;
+}
+
+/* Sampled DG parity at scale: y_e = M_e x_e for the listed elements only
+ * (x is the whole E-vector; ye[k] holds element elems[k]). */
+int orc_dg_apply_sample(const orc_mesh *m, int Q, const double *x, long long nel,
+                        const long long *elems, double *ye) {
+  orc_basis bs;
+  if (basis_build(&bs, m->p, ORC_GAUSS, Q)) return 1;
+  double *psi = dg_basis(&bs);
+  if (!psi) { basis_free(&bs); return 1; }
+  int nd = bs.nd, bad = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(| : bad)
+  for (long long k = 0; k < nel; ++k) {
+    double *A = (double *)malloc(sizeof(double) * nd * nd);
+    long long e = elems[k];
+    bad |= dg_element_matrix(m, &bs, psi, e, A);
+    for (int al = 0; al < nd; ++al) {
+      double s = 0.0;
+      for (int be = 0; be < nd; ++be) s += A[(long long)al * nd + be] * x[e * nd + be];
+      ye[k * nd + al] = s;
     }
-    free(X);
+    free(A);
   }
   free(psi);
   basis_free(&bs);

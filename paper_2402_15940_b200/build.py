@@ -50,9 +50,9 @@ def _jobs():
     jobs = []
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cu"))):
         name = os.path.splitext(os.path.basename(src))[0]
-        if name == "fused_p":
+        if name.endswith("_p"):  # per-P1 instantiation units (fused_p.cu, dg_p.cu)
             for p1 in P1S:
-                jobs.append((src, os.path.join(BUILD, f"fused_p{p1}.o"), [f"-DHOFEM_P1={p1}"]))
+                jobs.append((src, os.path.join(BUILD, f"{name}{p1}.o"), [f"-DHOFEM_P1={p1}"]))
         else:
             jobs.append((src, os.path.join(BUILD, f"{name}.o"), []))
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cpp"))):
@@ -69,7 +69,7 @@ def _deps_mtime():
 def _compile(job, verbose):
     src, obj, extra = job
     cmd = [NVCC] + _common_flags() + extra + ["-c", src, "-o", obj]
-    if verbose and "fused_p" in obj:
+    if verbose and "_p" in os.path.basename(obj):
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

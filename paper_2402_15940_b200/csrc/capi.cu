@@ -335,6 +335,44 @@ hofem_status hofem_cg(void* op_, const double* b, double* x, double rel_tol, int
                   S(stream));
 }
 
+hofem_status hofem_dg_create(void* mesh, int q_override, void* stream, void** dg_out) {
+  Mesh* m = static_cast<Mesh*>(mesh);
+  if (!m || !dg_out || q_override < 0) { set_error("hofem_dg_create: bad argument"); return HOFEM_ERR_ARG; }
+  DGOp* dg = nullptr;
+  HOFEM_TRY(dg_create(m, q_override, S(stream), &dg));
+  hofem_status st = cuda_status(cudaStreamSynchronize(S(stream)), "hofem_dg_create sync");
+  if (st != HOFEM_OK) { dg_destroy(dg); return st; }
+  *dg_out = dg;
+  return HOFEM_OK;
+}
+
+hofem_status hofem_dg_info_get(const void* dg_, hofem_dg_info* info) {
+  const DGOp* dg = static_cast<const DGOp*>(dg_);
+  if (!dg || !info) { set_error("hofem_dg_info_get: NULL"); return HOFEM_ERR_ARG; }
+  const Mesh* m = dg->mesh;
+  info->n_local = dg->n_local;
+  info->n_global = (long long)m->desc.nx * m->desc.ny * m->desc.nz_global * dg->nd;
+  info->elems_local = m->elems;
+  info->p = m->p; info->Q = dg->Q; info->dofs_per_elem = dg->nd; info->grid = dg->grid;
+  return HOFEM_OK;
+}
+
+hofem_status hofem_dg_apply(void* dg_, const double* x, double* y, void* stream) {
+  DGOp* dg = static_cast<DGOp*>(dg_);
+  if (!dg || !x || !y || x == y) { set_error("hofem_dg_apply: NULL or aliased x/y"); return HOFEM_ERR_ARG; }
+  HOFEM_ALIGNED("hofem_dg_apply", x, y);
+  return dg_apply(dg, x, y, S(stream));
+}
+
+hofem_status hofem_dg_fill_random(const void* dg_, unsigned long long seed, double* x, void* stream) {
+  const DGOp* dg = static_cast<const DGOp*>(dg_);
+  if (!dg || !x) { set_error("hofem_dg_fill_random: NULL"); return HOFEM_ERR_ARG; }
+  HOFEM_ALIGNED("hofem_dg_fill_random", x);
+  return dg_fill_random(dg, seed, x, S(stream));
+}
+
+void hofem_dg_destroy(void* dg) { dg_destroy(static_cast<DGOp*>(dg)); }
+
 hofem_status hofem_dot(const void* mesh, const double* a, const double* b, double* out_host,
                        void* stream) {
   Mesh* m = const_cast<Mesh*>(static_cast<const Mesh*>(mesh));

@@ -395,7 +395,9 @@ hofem_status cg_persistent(Op* op, double* x, double* r, double* p, double* Ap, 
   A.infix = 1;
   A.zero_n = 0;  // the CG kernel zeroes Ap itself
   A.bar = op->d_bar;
-  A.dotp = nullptr;
+  // the brick epilogue accumulates x.y terms only when dotp is non-null; the
+  // CG kernel stores its own per-CTA sums (G.parts), never A.dotp
+  A.dotp = op->d_cgparts;
   A.fx.dotp = nullptr;
   CGArgs G;
   G.n = m->n_local;

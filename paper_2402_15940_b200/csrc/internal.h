@@ -53,6 +53,7 @@ struct Tables1D {
 };
 int build_tables(int p, int Q, int rule, Tables1D* out);  // 0 ok
 void gll_nodes_weights(int p, double* x, double* w);
+int build_dg_table(int p, int Q, double* B);  // DG basis (Gauss-Legendre nodes) at Gauss points
 
 struct Mesh {
   hofem_mesh_desc desc{};
@@ -115,10 +116,26 @@ struct Op {
   int cg_cap = 0;
 };
 
+// DG (L2) mass operator (dg.cu, dg_impl.cuh; §8(f) f4)
+struct DGOp {
+  Mesh* mesh = nullptr;
+  Op* geo = nullptr;            // W*detJ qdata at the Gauss points (BP1 layout)
+  int Q = 0, nd = 0, grid = 0;
+  long long n_local = 0;        // E * P1^3
+  double B[kMaxQ * (kMaxP + 1)];  // B[k*P1+i] = psi_i(t_k), psi on Gauss-Legendre nodes
+};
+hofem_status dg_create(Mesh* m, int q_override, cudaStream_t s, DGOp** out);
+hofem_status dg_apply(DGOp* dg, const double* x, double* y, cudaStream_t s);
+hofem_status dg_fill_random(const DGOp* dg, unsigned long long seed, double* x, cudaStream_t s);
+void dg_destroy(DGOp* dg);
+
 // ---- mesh / setup kernels (mesh.cu)
 hofem_status mesh_build_coords(Mesh* m, cudaStream_t s);
 hofem_status mesh_build_restriction(Mesh* m, cudaStream_t s);
 hofem_status fill_random(const Mesh* m, unsigned long long seed, double* x, cudaStream_t s);
+// x[l] = R12 random value of global index g0 + l, l < n
+hofem_status fill_random_range(unsigned long long seed, long long g0, long long n, double* x,
+                               cudaStream_t s);
 
 // ---- qdata / rhs (qdata.cu)
 hofem_status build_qdata(Op* op, cudaStream_t s, int* bad_host);

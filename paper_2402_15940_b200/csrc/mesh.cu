@@ -152,8 +152,13 @@ hofem_status mesh_build_restriction(Mesh* m, cudaStream_t s) {
 }
 
 hofem_status fill_random(const Mesh* m, unsigned long long seed, double* x, cudaStream_t s) {
-  long long g0 = m->plane * (long long)m->p * m->z0;
-  random_kernel<<<grid_for(m->n_local, 256), 256, 0, s>>>(seed, g0, m->n_local, x);
+  return fill_random_range(seed, m->plane * (long long)m->p * m->z0, m->n_local, x, s);
+}
+
+hofem_status fill_random_range(unsigned long long seed, long long g0, long long n, double* x,
+                               cudaStream_t s) {
+  if (n <= 0) return HOFEM_OK;
+  random_kernel<<<grid_for(n, 256), 256, 0, s>>>(seed, g0, n, x);
   HOFEM_LAUNCHED();
   return HOFEM_OK;
 }

@@ -136,4 +136,35 @@ int build_tables(int p, int Q, int rule, Tables1D* T) {
   return 0;
 }
 
+// DG (L2) basis of §8(f) f4 (reading R16): Lagrange polynomials on the p+1
+// Gauss-Legendre points, evaluated at the Q Gauss quadrature points:
+// B[k*P1+i] = psi_i(t_k) (barycentric form; psi_i(t_k) = delta when the point sets
+// coincide, Q = P1).
+int build_dg_table(int p, int Q, double* B) {
+  if (p < 1 || p > kMaxP || Q < 1 || Q > kMaxQ) return 1;
+  const int P1 = p + 1;
+  double g[kMaxP + 1], gw[kMaxP + 1], t[kMaxQ], w[kMaxQ];
+  gauss_points_weights(P1, g, gw);
+  gauss_points_weights(Q, t, w);
+  long double lam[kMaxP + 1];
+  for (int i = 0; i < P1; ++i) {
+    long double d = 1.0L;
+    for (int j = 0; j < P1; ++j)
+      if (j != i) d *= (long double)g[i] - (long double)g[j];
+    lam[i] = 1.0L / d;
+  }
+  for (int k = 0; k < Q; ++k) {
+    int hit = -1;
+    for (int i = 0; i < P1; ++i)
+      if (t[k] == g[i]) hit = i;
+    long double den = 0.0L, li[kMaxP + 1];
+    for (int i = 0; i < P1; ++i) {
+      li[i] = hit >= 0 ? (i == hit ? 1.0L : 0.0L) : lam[i] / ((long double)t[k] - (long double)g[i]);
+      den += li[i];
+    }
+    for (int i = 0; i < P1; ++i) B[k * P1 + i] = (double)(li[i] / den);
+  }
+  return 0;
+}
+
 }  // namespace hofem

@@ -58,6 +58,12 @@ class FusedInfo(ctypes.Structure):
                 ("direct_points", ctypes.c_longlong), ("fixup_points", ctypes.c_longlong)]
 
 
+class DGInfo(ctypes.Structure):
+    _fields_ = [("n_local", ctypes.c_longlong), ("n_global", ctypes.c_longlong),
+                ("elems_local", ctypes.c_longlong), ("p", ctypes.c_int), ("Q", ctypes.c_int),
+                ("dofs_per_elem", ctypes.c_int), ("grid", ctypes.c_int)]
+
+
 class CGStats(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int), ("converged", ctypes.c_int),
                 ("r0_norm", ctypes.c_double), ("final_rel_res", ctypes.c_double)]
@@ -83,6 +89,11 @@ SIGNATURES = {
     "hofem_rhs_manufactured": (_I, [_V, _V, _V]),
     "hofem_fill_random": (_I, [_V, ctypes.c_ulonglong, _V, _V]),
     "hofem_op_destroy": (None, [_V]),
+    "hofem_dg_create": (_I, [_V, _I, _V, _PV]),
+    "hofem_dg_info_get": (_I, [_V, ctypes.POINTER(DGInfo)]),
+    "hofem_dg_apply": (_I, [_V, _V, _V, _V]),
+    "hofem_dg_fill_random": (_I, [_V, ctypes.c_ulonglong, _V, _V]),
+    "hofem_dg_destroy": (None, [_V]),
     "hofem_cg": (_I, [_V, _V, _V, _D, _I, _I, _I, _V, ctypes.POINTER(CGStats), _V]),
     "hofem_dot": (_I, [_V, _V, _V, ctypes.POINTER(_D), _V]),
     "hofem_op_apply_dot": (_I, [_V, _V, _V, ctypes.POINTER(_D), _V]),
@@ -305,6 +316,41 @@ class Operator:
     def close(self):
         if self.handle:
             lib().hofem_op_destroy(self.handle)
+            self.handle = None
+
+
+class DGMass:
+    """Matrix-free DG (L2) mass operator on a Mesh (hofem_dg_*; §8(f) f4).
+    Vectors are element-major E-vectors of n_local doubles."""
+
+    def __init__(self, mesh: Mesh, q_override=0, stream=None):
+        h = ctypes.c_void_p()
+        _check(lib().hofem_dg_create(mesh.handle, q_override, _stream(stream), ctypes.byref(h)))
+        self.handle = h
+        self.mesh = mesh
+        self.info = self.get_info()
+        self.n_local = self.info.n_local
+
+    def get_info(self) -> DGInfo:
+        s = DGInfo()
+        _check(lib().hofem_dg_info_get(self.handle, ctypes.byref(s)))
+        return s
+
+    def random(self, seed: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        out = torch.empty(self.n_local, dtype=torch.float64, device="cuda") if out is None else out
+        _check(lib().hofem_dg_fill_random(self.handle, ctypes.c_ulonglong(seed),
+                                          _ptr(out, self.n_local), _stream(stream)))
+        return out
+
+    def apply(self, x: torch.Tensor, y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        y = torch.empty_like(x) if y is None else y
+        _check(lib().hofem_dg_apply(self.handle, _ptr(x, self.n_local), _ptr(y, self.n_local),
+                                    _stream(stream)))
+        return y
+
+    def close(self):
+        if self.handle:
+            lib().hofem_dg_destroy(self.handle)
             self.handle = None
 
 

@@ -71,3 +71,14 @@ def test_dg_symmetric_positive_definite_and_block_apply():
     y = O.dg_apply(m, Me, x)
     ref = np.concatenate([Me[e] @ x[e * nd:(e + 1) * nd] for e in range(m.n_elems)])
     assert np.abs(y - ref).max() <= 1e-14 * np.abs(ref).max()
+
+
+def test_dg_sample_matches_full_apply():
+    m = O.Mesh(3, 2, 2, 3, alpha=0.1)
+    Me = O.dg_mass_matrices(m)
+    x = np.random.default_rng(1).standard_normal(m.n_elems * 64)
+    y = O.dg_apply(m, Me, x)
+    elems = np.array([0, 5, 11, 7])
+    ye = O.dg_apply_sample(m, x, elems)
+    for k, e in enumerate(elems):
+        assert np.abs(ye[k] - y[e * 64:(e + 1) * 64]).max() <= 1e-15 * np.abs(y).max() * 10

@@ -62,6 +62,18 @@ def bp3_sweep_n(p: int) -> int:
     return int(round(311.0 / p))
 
 
+def dg_sweep_n(p: int) -> int:
+    """f4 DG mass: ~30M DG dofs, E (p+1)^3 with n = round(311/(p+1)) per axis."""
+    return int(round(311.0 / (p + 1)))
+
+
+def config5(n_gpus: int = 1):
+    """Config 5: BP3 p=5, 200 x 200 x 25R elements (~125.5M
+    dofs per GPU), weak scaling over R GPUs."""
+    return dict(name=f"bp3_p5_200x200x{25 * n_gpus}", nx=200, ny=200, nz=25 * n_gpus, p=5,
+                alpha=ALPHA)
+
+
 CONFIG1 = dict(name="bp3_2x2x2_p2", nx=2, ny=2, nz=2, p=2, alpha=ALPHA)
 
 
