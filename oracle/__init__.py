@@ -75,6 +75,11 @@ def lib():
             "orc_l2_error": (d, [M, P, i]),
             "orc_cg": (i, [M, P, i, P, ll, P, P, d, i, i, P, P, P]),
             "orc_num_threads": (i, []),
+            "orc_diagonal": (i, [M, P, i, P]),
+            "orc_prolong": (i, [M, M, P, P]),
+            "orc_restrict": (i, [M, M, P, P]),
+            "orc_power_lmax": (d, [M, P, i, P, P, i]),
+            "orc_cheb": (i, [M, P, i, P, d, d, i, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)

@@ -846,6 +846,158 @@ int orc_cg(const orc_mesh *m, const double *Ae, int bc, const double *Adense, lo
   return status;
 }
 
+/* ------------------------------------------------------------------------- */
+/* p-multigrid preconditioned CG pieces, SURVEY.md §8(f) f2 (*/
+/* §2.1: "p-multigrid ... restriction and prolongation operators ... smoothers */
+/* based only on the diagonal of the matrix ... Chebyshev acceleration";       */
+/* PAPER.md:156 BPS3).  Readings R17-R18.                       */
+/* ------------------------------------------------------------------------- */
+
+/* diag(A) = sum_e R_e^T diag(A_e) (ascending e); Dirichlet rows of the
+ * identity-row convention (reading R6) get 1. */
+int orc_diagonal(const orc_mesh *m, const double *Ae, int bc, double *d) {
+  long long E = orc_num_elems(m), N = orc_num_dofs(m);
+  int P1 = m->p + 1, nd = P1 * P1 * P1;
+  memset(d, 0, sizeof(double) * N);
+  for (long long e = 0; e < E; ++e)
+    for (int c = 0; c < P1; ++c)
+      for (int b = 0; b < P1; ++b)
+        for (int a = 0; a < P1; ++a) {
+          int al = a + P1 * (b + P1 * c);
+          d[l_index(m, e, a, b, c)] += Ae[e * (long long)nd * nd + (long long)al * nd + al];
+        }
+  if (bc) {
+    uint8_t *mask = (uint8_t *)malloc(N);
+    orc_boundary_mask(m, mask);
+    for (long long l = 0; l < N; ++l) if (mask[l]) d[l] = 1.0;
+    free(mask);
+  }
+  return 0;
+}
+
+/* Owner element of a lattice index along one axis (lowest element containing it)
+ * and the local node index there. */
+static void owner_axis(long long I, int p, int n, long long *e, int *a) {
+  long long q = I / p;
+  if (q > n - 1) q = n - 1;
+  *e = q;
+  *a = (int)(I - (long long)p * q);
+}
+
+/* Coarse-to-fine interpolation weights of fine lattice point (I,J,K): its owner
+ * element e and the values phi^c_alpha(xi) of the coarse element basis at the
+ * fine node's reference coordinate (GLL nodes of both orders, product formula). */
+static long long transfer_weights(const orc_mesh *mf, const orc_mesh *mc, long long I, long long J,
+                                  long long K, double *w) {
+  double xf[ORC_MAXP1], xc[ORC_MAXP1], wt[ORC_MAXP1];
+  orc_gll(mf->p, xf, wt);
+  orc_gll(mc->p, xc, wt);
+  long long ex, ey, ez;
+  int a, b, c;
+  owner_axis(I, mf->p, mf->nx, &ex, &a);
+  owner_axis(J, mf->p, mf->ny, &ey, &b);
+  owner_axis(K, mf->p, mf->nzl, &ez, &c);
+  int P1c = mc->p + 1;
+  for (int gc = 0; gc < P1c; ++gc)
+    for (int gb = 0; gb < P1c; ++gb)
+      for (int ga = 0; ga < P1c; ++ga)
+        w[ga + P1c * (gb + P1c * gc)] = lagrange(mc->p, xc, ga, xf[a]) *
+                                        lagrange(mc->p, xc, gb, xf[b]) *
+                                        lagrange(mc->p, xc, gc, xf[c]);
+  return ex + (long long)mf->nx * (ey + (long long)mf->ny * ez);
+}
+
+/* Prolongation P (order mc->p -> mf->p, same elements): the fine nodal value is
+ * the coarse finite-element function evaluated at the fine node (the natural
+ * injection of the nested spaces). */
+int orc_prolong(const orc_mesh *mf, const orc_mesh *mc, const double *xc, double *xf) {
+  long long Nx, Ny, Nz;
+  local_dims(mf, &Nx, &Ny, &Nz);
+  int P1c = mc->p + 1;
+  double w[ORC_MAXP1 * ORC_MAXP1 * ORC_MAXP1];
+  for (long long K = 0; K < Nz; ++K)
+    for (long long J = 0; J < Ny; ++J)
+      for (long long I = 0; I < Nx; ++I) {
+        long long e = transfer_weights(mf, mc, I, J, K, w);
+        double s = 0.0;
+        for (int gc = 0; gc < P1c; ++gc)
+          for (int gb = 0; gb < P1c; ++gb)
+            for (int ga = 0; ga < P1c; ++ga)
+              s += w[ga + P1c * (gb + P1c * gc)] * xc[l_index(mc, e, ga, gb, gc)];
+        xf[I + Nx * (J + Ny * K)] = s;
+      }
+  return 0;
+}
+
+/* Restriction R = P^T: rc[j] = sum_i P_ij rf[i], looping over fine points i with
+ * the same owner element and weights as orc_prolong (so R is exactly P^T). */
+int orc_restrict(const orc_mesh *mf, const orc_mesh *mc, const double *rf, double *rc) {
+  long long Nx, Ny, Nz;
+  local_dims(mf, &Nx, &Ny, &Nz);
+  int P1c = mc->p + 1;
+  memset(rc, 0, sizeof(double) * orc_num_dofs(mc));
+  double w[ORC_MAXP1 * ORC_MAXP1 * ORC_MAXP1];
+  for (long long K = 0; K < Nz; ++K)
+    for (long long J = 0; J < Ny; ++J)
+      for (long long I = 0; I < Nx; ++I) {
+        long long e = transfer_weights(mf, mc, I, J, K, w);
+        double v = rf[I + Nx * (J + Ny * K)];
+        for (int gc = 0; gc < P1c; ++gc)
+          for (int gb = 0; gb < P1c; ++gb)
+            for (int ga = 0; ga < P1c; ++ga)
+              rc[l_index(mc, e, ga, gb, gc)] += w[ga + P1c * (gb + P1c * gc)] * v;
+      }
+  return 0;
+}
+
+/* Largest eigenvalue estimate of D^{-1}A by power iteration (reading R17):
+ * v = v0/|v0|; iters times: w = D^{-1} A v, lambda = |w|, v = w/lambda. */
+double orc_power_lmax(const orc_mesh *m, const double *Ae, int bc, const double *dinv,
+                      const double *v0, int iters) {
+  long long N = orc_num_dofs(m);
+  double *v = (double *)malloc(sizeof(double) * N), *w = (double *)malloc(sizeof(double) * N);
+  double nv = sqrt(dot(N, v0, v0)), lam = 0.0;
+  for (long long i = 0; i < N; ++i) v[i] = v0[i] / nv;
+  for (int k = 0; k < iters; ++k) {
+    orc_apply_ea(m, Ae, bc, v, w);
+    for (long long i = 0; i < N; ++i) w[i] *= dinv[i];
+    lam = sqrt(dot(N, w, w));
+    for (long long i = 0; i < N; ++i) v[i] = w[i] / lam;
+  }
+  free(v); free(w);
+  return lam;
+}
+
+/* Chebyshev acceleration of Jacobi (Saad, "Iterative Methods for Sparse Linear
+ * Systems", Algorithm 12.1, preconditioner D = diag(A)), `degree` >= 1 steps on
+ * the interval [lmin, lmax] of D^{-1}A, starting from x (updated in place):
+ *   r = b - A x; theta = (lmax+lmin)/2; delta = (lmax-lmin)/2; sigma = theta/delta
+ *   rho = 1/sigma; d = D^{-1} r / theta
+ *   for k = 1..degree: x += d; if k < degree: r -= A d;
+ *       rho' = 1/(2 sigma - rho); d = rho' rho d + (2 rho'/delta) D^{-1} r; rho = rho' */
+int orc_cheb(const orc_mesh *m, const double *Ae, int bc, const double *dinv, double lmin,
+             double lmax, int degree, const double *b, double *x) {
+  long long N = orc_num_dofs(m);
+  double *r = (double *)malloc(sizeof(double) * N), *d = (double *)malloc(sizeof(double) * N);
+  double *Ad = (double *)malloc(sizeof(double) * N);
+  orc_apply_ea(m, Ae, bc, x, Ad);
+  for (long long i = 0; i < N; ++i) r[i] = b[i] - Ad[i];
+  double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin), sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  for (long long i = 0; i < N; ++i) d[i] = dinv[i] * r[i] / theta;
+  for (int k = 1; k <= degree; ++k) {
+    for (long long i = 0; i < N; ++i) x[i] += d[i];
+    if (k == degree) break;
+    orc_apply_ea(m, Ae, bc, d, Ad);
+    for (long long i = 0; i < N; ++i) r[i] -= Ad[i];
+    double rn = 1.0 / (2.0 * sigma - rho);
+    for (long long i = 0; i < N; ++i) d[i] = rn * rho * d[i] + (2.0 * rn / delta) * dinv[i] * r[i];
+    rho = rn;
+  }
+  free(r); free(d); free(Ad);
+  return 0;
+}
+
 int orc_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

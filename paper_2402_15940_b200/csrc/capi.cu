@@ -90,6 +90,51 @@ inline bool aligned(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15
   } while (0)
 
 }  // namespace
+
+void op_free(Op* op) { free_op(op); }
+
+// Build a partially assembled operator (hofem_op_create without the handle
+// checks); also used for the DG operator's geometry and the p-multigrid levels.
+hofem_status op_new(Mesh* m, int kind, int rule, int q_override, int bc, cudaStream_t stream,
+                    Op** op_out) {
+  if ((kind != HOFEM_MASS && kind != HOFEM_DIFFUSION) || (rule != HOFEM_GAUSS && rule != HOFEM_GLL) ||
+      (bc != HOFEM_BC_NONE && bc != HOFEM_BC_DIRICHLET) || q_override < 0 || q_override > kMaxQ) {
+    set_error("hofem_op_create: bad kind/rule/bc/q_override");
+    return HOFEM_ERR_ARG;
+  }
+  const int Q = q_override ? q_override : (rule == HOFEM_GAUSS ? m->p + 2 : m->p + 1);
+  if (rule == HOFEM_GLL && Q < 2) { set_error("hofem_op_create: GLL needs Q>=2"); return HOFEM_ERR_ARG; }
+  auto* op = new Op();
+  op->mesh = m; op->kind = kind; op->rule = rule; op->Q = Q; op->bc = bc;
+  op->nc = kind == HOFEM_MASS ? 1 : 6;
+  if (build_tables(m->p, Q, rule, &op->tab)) {
+    delete op;
+    set_error("hofem_op_create: 1D tables failed");
+    return HOFEM_ERR_ARG;
+  }
+  hofem_status st = HOFEM_OK;
+#define CK(x) do { st = (x); if (st != HOFEM_OK) { free_op(op); return st; } } while (0)
+  const int P1 = m->P1;
+  op->qcount = m->elems * op->nc * (long long)Q * Q * Q;
+  CK(dalloc(&op->d_B, Q * P1, "op tables"));
+  CK(dalloc(&op->d_G, Q * P1, "op tables"));
+  CK(dalloc(&op->d_qdata, op->qcount + 2, "qdata"));  // +16 B: widened L2 prefetch
+  CK(cuda_status(cudaMemcpyAsync(op->d_B, op->tab.B, sizeof(double) * Q * P1,
+                                 cudaMemcpyHostToDevice, stream), "upload B"));
+  CK(cuda_status(cudaMemcpyAsync(op->d_G, op->tab.G, sizeof(double) * Q * P1,
+                                 cudaMemcpyHostToDevice, stream), "upload G"));
+  int bad = 0;
+  CK(build_qdata(op, stream, &bad));
+  if (bad) {
+    free_op(op);
+    set_error("hofem_op_create: detJ <= 0 at some quadrature point (invalid mesh)");
+    return HOFEM_ERR_MESH;
+  }
+#undef CK
+  *op_out = op;
+  return HOFEM_OK;
+}
+
 }  // namespace hofem
 
 using namespace hofem;
@@ -219,40 +264,8 @@ hofem_status hofem_op_create(void* mesh, hofem_kind kind, hofem_rule rule, int q
                              hofem_bc bc, void* stream, void** op_out) {
   Mesh* m = static_cast<Mesh*>(mesh);
   if (!m || !op_out) { set_error("hofem_op_create: NULL"); return HOFEM_ERR_ARG; }
-  if ((kind != HOFEM_MASS && kind != HOFEM_DIFFUSION) || (rule != HOFEM_GAUSS && rule != HOFEM_GLL) ||
-      (bc != HOFEM_BC_NONE && bc != HOFEM_BC_DIRICHLET) || q_override < 0 || q_override > kMaxQ) {
-    set_error("hofem_op_create: bad kind/rule/bc/q_override");
-    return HOFEM_ERR_ARG;
-  }
-  const int Q = q_override ? q_override : (rule == HOFEM_GAUSS ? m->p + 2 : m->p + 1);
-  if (rule == HOFEM_GLL && Q < 2) { set_error("hofem_op_create: GLL needs Q>=2"); return HOFEM_ERR_ARG; }
-  auto* op = new Op();
-  op->mesh = m; op->kind = kind; op->rule = rule; op->Q = Q; op->bc = bc;
-  op->nc = kind == HOFEM_MASS ? 1 : 6;
-  if (build_tables(m->p, Q, rule, &op->tab)) {
-    delete op;
-    set_error("hofem_op_create: 1D tables failed");
-    return HOFEM_ERR_ARG;
-  }
-  hofem_status st = HOFEM_OK;
-#define CK(x) do { st = (x); if (st != HOFEM_OK) { free_op(op); return st; } } while (0)
-  const int P1 = m->P1;
-  op->qcount = m->elems * op->nc * (long long)Q * Q * Q;
-  CK(dalloc(&op->d_B, Q * P1, "op tables"));
-  CK(dalloc(&op->d_G, Q * P1, "op tables"));
-  CK(dalloc(&op->d_qdata, op->qcount + 2, "qdata"));  // +16 B: widened L2 prefetch
-  CK(cuda_status(cudaMemcpyAsync(op->d_B, op->tab.B, sizeof(double) * Q * P1,
-                                 cudaMemcpyHostToDevice, S(stream)), "upload B"));
-  CK(cuda_status(cudaMemcpyAsync(op->d_G, op->tab.G, sizeof(double) * Q * P1,
-                                 cudaMemcpyHostToDevice, S(stream)), "upload G"));
-  int bad = 0;
-  CK(build_qdata(op, S(stream), &bad));
-  if (bad) {
-    free_op(op);
-    set_error("hofem_op_create: detJ <= 0 at some quadrature point (invalid mesh)");
-    return HOFEM_ERR_MESH;
-  }
-#undef CK
+  Op* op = nullptr;
+  HOFEM_TRY(op_new(m, kind, rule, q_override, bc, S(stream), &op));
   *op_out = op;
   return HOFEM_OK;
 }

@@ -32,36 +32,9 @@ hofem_status dg_create(Mesh* m, int q_override, cudaStream_t s, DGOp** out) {
     return HOFEM_ERR_ARG;
   }
   // the geometry of the DG operator: W*detJ at the Gauss points, exactly the BP1 qdata
-  auto* geo = new Op();
-  geo->mesh = m;
-  geo->kind = HOFEM_MASS;
-  geo->rule = HOFEM_GAUSS;
-  geo->Q = Q;
-  geo->nc = 1;
-  geo->bc = 0;
-  if (build_tables(m->p, Q, HOFEM_GAUSS, &geo->tab)) {
-    delete geo;
-    delete dg;
-    set_error("hofem_dg_create: 1D tables failed");
-    return HOFEM_ERR_ARG;
-  }
-  geo->qcount = m->elems * (long long)Q * Q * Q;
-  if (cudaMalloc(&geo->d_qdata, sizeof(double) * (geo->qcount + 2)) != cudaSuccess) {
-    cudaGetLastError();
-    delete geo;
-    delete dg;
-    set_error("hofem_dg_create: out of device memory for qdata");
-    return HOFEM_ERR_OOM;
-  }
-  dg->geo = geo;
-  int bad = 0;
-  hofem_status st = build_qdata(geo, s, &bad);
-  if (st == HOFEM_OK && bad) {
-    set_error("hofem_dg_create: detJ <= 0 at some quadrature point (invalid mesh)");
-    st = HOFEM_ERR_MESH;
-  }
+  hofem_status st = op_new(m, HOFEM_MASS, HOFEM_GAUSS, Q, HOFEM_BC_NONE, s, &dg->geo);
   if (st != HOFEM_OK) {
-    dg_destroy(dg);
+    delete dg;
     return st;
   }
   *out = dg;
@@ -70,10 +43,7 @@ hofem_status dg_create(Mesh* m, int q_override, cudaStream_t s, DGOp** out) {
 
 void dg_destroy(DGOp* dg) {
   if (!dg) return;
-  if (dg->geo) {
-    cudaFree(dg->geo->d_qdata);
-    delete dg->geo;
-  }
+  op_free(dg->geo);
   delete dg;
 }
 

@@ -116,6 +116,11 @@ struct Op {
   int cg_cap = 0;
 };
 
+// Operator construction / destruction (capi.cu): qdata, tables; SYNC.
+hofem_status op_new(Mesh* m, int kind, int rule, int q_override, int bc, cudaStream_t s,
+                    Op** out);
+void op_free(Op* op);
+
 // DG (L2) mass operator (dg.cu, dg_impl.cuh; §8(f) f4)
 struct DGOp {
   Mesh* mesh = nullptr;
