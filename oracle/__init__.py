@@ -292,5 +292,138 @@ def cg(b, *, m: Mesh | None = None, Ae=None, bc=0, A=None, x0=None, rel_tol=1e-1
     return x, st, k, rr[: k + 1], (xh[: k + 1] if history else None)
 
 
+# ----------------------------------------------------------------------------- f2
+# p-multigrid preconditioned CG (§2.1;
+# PAPER.md:156 BPS3).  Readings R17 (hierarchy, smoother, eigen estimate) and
+# R18 (PCG) of DESIGN.md §3.  The V-cycle and PCG below follow the algorithm
+# step by step in numpy, calling the C primitives (EA apply, diagonal,
+# transfers, Chebyshev, power iteration) for each step.
+
+def diagonal(m: Mesh, Ae, bc=0):
+    d = np.zeros(m.n_dofs)
+    mc = m.c()
+    lib().orc_diagonal(ctypes.byref(mc), _p(Ae), int(bc), _p(d))
+    return d
+
+
+def prolong(mf: Mesh, mc_: Mesh, xc):
+    xc = np.ascontiguousarray(xc, dtype=np.float64)
+    xf = np.zeros(mf.n_dofs)
+    a, b = mf.c(), mc_.c()
+    lib().orc_prolong(ctypes.byref(a), ctypes.byref(b), _p(xc), _p(xf))
+    return xf
+
+
+def restrict(mf: Mesh, mc_: Mesh, rf):
+    rf = np.ascontiguousarray(rf, dtype=np.float64)
+    rc = np.zeros(mc_.n_dofs)
+    a, b = mf.c(), mc_.c()
+    lib().orc_restrict(ctypes.byref(a), ctypes.byref(b), _p(rf), _p(rc))
+    return rc
+
+
+def power_lmax(m: Mesh, Ae, bc, dinv, v0, iters=10):
+    v0 = np.ascontiguousarray(v0, dtype=np.float64)
+    mc = m.c()
+    return lib().orc_power_lmax(ctypes.byref(mc), _p(Ae), int(bc), _p(dinv), _p(v0), int(iters))
+
+
+def cheb(m: Mesh, Ae, bc, dinv, lmin, lmax, degree, b, x):
+    """Chebyshev-Jacobi smoothing (Saad Alg. 12.1); returns the new x."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.array(x, dtype=np.float64)
+    mc = m.c()
+    lib().orc_cheb(ctypes.byref(mc), _p(Ae), int(bc), _p(dinv), float(lmin), float(lmax),
+                   int(degree), _p(b), _p(x))
+    return x
+
+
+def pmg_orders(p: int):
+    """Reading R17: p_{k-1} = max(1, p_k // 2) down to 1 (fine first)."""
+    out = [p]
+    while out[-1] > 1:
+        out.append(max(1, out[-1] // 2))
+    return out
+
+
+CHEB_HI, CHEB_LO = 1.2, 0.3  # reading R17: [0.3 * 1.2 lam, 1.2 lam]
+
+
+class PMG:
+    """p-multigrid V-cycle on the BP3 (Gauss Q = p_k + 2) Dirichlet operators of
+    the same element grid at orders pmg_orders(p); every level is an EA oracle."""
+
+    def __init__(self, nx, ny, nz, p, alpha=0.1, degree=3, power_iters=10, seed=1,
+                 lmax=None):
+        import workloads as W
+        self.orders = pmg_orders(p)
+        self.degree = degree
+        self.levels = []
+        for k, pk in enumerate(self.orders):
+            m = Mesh(nx, ny, nz, pk, alpha=alpha)
+            Ae = element_matrices(m, DIFFUSION, GAUSS)
+            d = diagonal(m, Ae, bc=1)
+            dinv = 1.0 / d
+            if lmax is not None:
+                lam = lmax[k]
+            else:
+                v0 = W.random_vector(seed, np.arange(m.n_dofs))
+                lam = power_lmax(m, Ae, 1, dinv, v0, power_iters)
+            self.levels.append(dict(m=m, Ae=Ae, dinv=dinv, lam=lam,
+                                    lmax=CHEB_HI * lam, lmin=CHEB_LO * CHEB_HI * lam))
+
+    def smooth(self, k, b, x):
+        L = self.levels[k]
+        return cheb(L["m"], L["Ae"], 1, L["dinv"], L["lmin"], L["lmax"], self.degree, b, x)
+
+    def vcycle(self, b, k=0):
+        """Level k = 0 is the finest (orders[0] = p)."""
+        L = self.levels[k]
+        x = self.smooth(k, b, np.zeros_like(b))
+        if k + 1 < len(self.levels):
+            r = b - apply_ea(L["m"], L["Ae"], x, bc=1)
+            C = self.levels[k + 1]
+            ec = self.vcycle(restrict(L["m"], C["m"], r), k + 1)
+            x = x + prolong(L["m"], C["m"], ec)
+        return self.smooth(k, b, x)
+
+
+def pcg(b, M, *, m: Mesh, Ae, bc=1, rel_tol=1e-10, max_iter=500, history=False):
+    """Preconditioned CG (reading R18): x0 = 0, z = M(r), stop at
+    ||r|| <= rel_tol ||r0||.  Returns (x, status, iters, rr, x_hist)."""
+    x = np.zeros_like(b)
+    r = b.copy()
+    rr = [float(r @ r)]
+    xh = [x.copy()] if history else None
+    z = M(r)
+    p = z.copy()
+    rz = float(r @ z)
+    k = 0
+    st = 7
+    if rr[0] == 0.0:
+        return x, 0, 0, np.array(rr), xh
+    while k < max_iter:
+        Ap = apply_ea(m, Ae, p, bc=bc)
+        pAp = float(p @ Ap)
+        if not pAp > 0:
+            st = 6
+            break
+        a = rz / pAp
+        x = x + a * p
+        r = r - a * Ap
+        k += 1
+        rr.append(float(r @ r))
+        if history:
+            xh.append(x.copy())
+        if np.sqrt(rr[-1]) <= rel_tol * np.sqrt(rr[0]):
+            st = 0
+            break
+        z = M(r)
+        rzn = float(r @ z)
+        p = z + (rzn / rz) * p
+        rz = rzn
+    return x, st, k, np.array(rr), xh
+
+
 def num_threads() -> int:
     return lib().orc_num_threads()
