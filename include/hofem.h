@@ -214,6 +214,56 @@ hofem_status hofem_cg(void* op, const double* b, double* x, double rel_tol, int 
 hofem_status hofem_dot(const void* mesh, const double* a, const double* b, double* out_host,
                        void* stream);
 
+/* ---------------------------------- p-multigrid preconditioned CG (§8(f) f2) */
+/* Matrix-free preconditioning of the BP3 problem, CEED BPS3 (PAPER.md:103-111,
+ * §2.1 "p-multigrid ... Chebyshev acceleration").  Readings R17-R18
+ * (DESIGN.md §3): levels of orders p, p/2, ..., 1 on the same element grid
+ * (each a BP3 Gauss Q = p_k + 2 Dirichlet operator on its own isoparametric mesh
+ * of order p_k), prolongation = nodal interpolation of the coarse function,
+ * restriction = its transpose (coarse Dirichlet rows zeroed), smoother =
+ * Chebyshev acceleration of Jacobi (Saad Alg. 12.1, `degree` steps) on
+ * [0.3 lam_hi, lam_hi], lam_hi = 1.2 x the power-iteration estimate (power_iters
+ * iterations from the R12 random vector `seed`) of lambda_max(D^-1 A); V-cycle
+ * pre-smooth / residual / restrict / recurse / prolong-correct / post-smooth, the
+ * coarsest level smoothed twice (no AMG coarse solve: hypre is out of scope).
+ * Single rank only (HOFEM_ERR_ARG otherwise). */
+
+/* diag(A) of a partially assembled operator by sum factorization over squared
+ * 1D tables (no assembly), interface planes summed across ranks, Dirichlet rows
+ * 1 (identity-row convention R6).  d: n_local doubles. */
+hofem_status hofem_op_diagonal(void* op, double* d, void* stream);
+
+typedef struct {
+  int levels;          /* number of levels (level 0 = the finest, order p) */
+  int orders[8];       /* polynomial order of each level */
+  double lambda[8];    /* power-iteration estimate of lambda_max(D^-1 A) per level */
+  int degree;          /* Chebyshev steps per smoothing pass */
+} hofem_pmg_info;
+/* SYNC.  Builds the hierarchy on `mesh` (borrowed: it must outlive the handle). */
+hofem_status hofem_pmg_create(void* mesh, int degree, int power_iters, unsigned long long seed,
+                              void* stream, void** pmg_out);
+hofem_status hofem_pmg_info_get(const void* pmg, hofem_pmg_info* info_out);
+/* Override level k's eigenvalue estimate (parity testing against the oracle's). */
+hofem_status hofem_pmg_set_lambda(void* pmg, int level, double lambda);
+/* Borrowed handles of level k (its mesh: vector lengths via hofem_mesh_info_get;
+ * its operator: hofem_op_apply etc.).  Owned by the pmg handle. */
+hofem_status hofem_pmg_level(void* pmg, int level, void** mesh_out, void** op_out);
+/* z = V-cycle(r) on level 0 (r, z: level-0 vectors, must not alias). */
+hofem_status hofem_pmg_vcycle(void* pmg, const double* r, double* z, void* stream);
+/* One smoothing pass on level k: x <- x + p(D^-1 A) D^-1 (b - A x). */
+hofem_status hofem_pmg_smooth(void* pmg, int level, const double* b, double* x, void* stream);
+/* Transfers between level k (fine) and k+1 (coarse): dir = 0 prolongation
+ * (fine += P coarse: `in` is coarse, `out` fine, accumulated), dir = 1
+ * restriction (coarse = R fine, coarse Dirichlet rows 0: `in` fine, `out` coarse). */
+hofem_status hofem_pmg_transfer(void* pmg, int level, int dir, const double* in, double* out,
+                                void* stream);
+/* SYNC.  Preconditioned CG (reading R18) on level 0 with one V-cycle per
+ * iteration: x in x0 / out, stop at ||r|| <= rel_tol ||r0||; rr_history (host,
+ * nullable, length max_iter+1) receives r_k.r_k.  Status as hofem_cg. */
+hofem_status hofem_pmg_pcg(void* pmg, const double* b, double* x, double rel_tol, int max_iter,
+                           double* rr_history, hofem_cg_stats* stats, void* stream);
+void hofem_pmg_destroy(void* pmg);
+
 /* Kernel timing hooks for the bench's roofline figure.  When enabled, the
  * library records CUDA events on the launching stream around every fused brick
  * kernel and every brick fix-up kernel; hofem_profile_read synchronizes on

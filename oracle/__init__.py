@@ -369,7 +369,7 @@ class PMG:
             else:
                 v0 = W.random_vector(seed, np.arange(m.n_dofs))
                 lam = power_lmax(m, Ae, 1, dinv, v0, power_iters)
-            self.levels.append(dict(m=m, Ae=Ae, dinv=dinv, lam=lam,
+            self.levels.append(dict(m=m, Ae=Ae, dinv=dinv, lam=lam, ess=boundary_mask(m),
                                     lmax=CHEB_HI * lam, lmin=CHEB_LO * CHEB_HI * lam))
 
     def smooth(self, k, b, x):
@@ -383,7 +383,9 @@ class PMG:
         if k + 1 < len(self.levels):
             r = b - apply_ea(L["m"], L["Ae"], x, bc=1)
             C = self.levels[k + 1]
-            ec = self.vcycle(restrict(L["m"], C["m"], r), k + 1)
+            rc = restrict(L["m"], C["m"], r)
+            rc[C["ess"]] = 0.0  # coarse Dirichlet rows of the restricted residual (R17)
+            ec = self.vcycle(rc, k + 1)
             x = x + prolong(L["m"], C["m"], ec)
         return self.smooth(k, b, x)
 

@@ -92,6 +92,58 @@ inline bool aligned(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15
 }  // namespace
 
 void op_free(Op* op) { free_op(op); }
+void mesh_free(Mesh* m) { free_mesh(m); }
+
+// Build a mesh (hofem_mesh_create without the handle checks); SYNC.  Also used
+// for the p-multigrid levels.
+hofem_status mesh_new(const hofem_mesh_desc* d, Comm* c, cudaStream_t stream, Mesh** mesh_out) {
+  if (d->p < 1 || d->p > kMaxP || d->nx < 1 || d->ny < 1 || d->nz_global < 1 ||
+      !(d->extent[0] > 0) || !(d->extent[1] > 0) || !(d->extent[2] > 0)) {
+    set_error("hofem_mesh_create: need 1<=p<=%d, n>=1, extents>0", kMaxP);
+    return HOFEM_ERR_ARG;
+  }
+  const int R = c ? c->nranks : 1, r = c ? c->rank : 0;
+  if (d->nz_global % R != 0) {
+    set_error("hofem_mesh_create: nranks=%d must divide nz_global=%d", R, d->nz_global);
+    return HOFEM_ERR_ARG;
+  }
+  int dev = 0;
+  HOFEM_CUDA(cudaGetDevice(&dev));
+  auto* m = new Mesh();
+  m->desc = *d;
+  m->comm = c;
+  m->rank = r; m->nranks = R;
+  m->p = d->p; m->P1 = d->p + 1;
+  m->nx = d->nx; m->ny = d->ny; m->nzl = d->nz_global / R; m->z0 = r * m->nzl;
+  m->Nx = (long long)d->p * d->nx + 1;
+  m->Ny = (long long)d->p * d->ny + 1;
+  m->Nzl = (long long)d->p * m->nzl + 1;
+  m->NzG = (long long)d->p * d->nz_global + 1;
+  m->plane = m->Nx * m->Ny;
+  m->n_local = m->plane * m->Nzl;
+  m->n_owned = (r == R - 1) ? m->n_local : m->n_local - m->plane;
+  m->n_global = m->plane * m->NzG;
+  m->elems = (long long)d->nx * d->ny * m->nzl;
+  double xi[kMaxP + 1], w[kMaxP + 1];
+  gll_nodes_weights(d->p, xi, w);
+  hofem_status st = HOFEM_OK;
+#define CK(x) do { st = (x); if (st != HOFEM_OK) { free_mesh(m); return st; } } while (0)
+  CK(dalloc(&m->d_xi, m->P1, "mesh"));
+  CK(dalloc(&m->d_coords, 3 * m->n_local, "mesh coords"));
+  CK(dalloc(&m->d_partials, 4 * kNumSMs + 64, "mesh"));
+  CK(dalloc(&m->d_counter, 4, "mesh"));
+  CK(dalloc(&m->d_scalars, 16, "mesh"));
+  if (R > 1) CK(dalloc(&m->d_recv, 2 * m->plane, "mesh planes"));
+  CK(cuda_status(cudaMemcpyAsync(m->d_xi, xi, sizeof(double) * m->P1, cudaMemcpyHostToDevice,
+                                 stream), "mesh upload"));
+  CK(cuda_status(cudaMemsetAsync(m->d_counter, 0, 4 * sizeof(unsigned), stream), "memset"));
+  CK(mesh_build_coords(m, stream));
+  CK(cuda_status(cudaStreamSynchronize(stream), "mesh_create sync"));
+#undef CK
+  *mesh_out = m;
+  return HOFEM_OK;
+}
+
 
 // Build a partially assembled operator (hofem_op_create without the handle
 // checks); also used for the DG operator's geometry and the p-multigrid levels.
@@ -193,50 +245,8 @@ void hofem_launch_count_reset(void) { g_launches.store(0); }
 hofem_status hofem_mesh_create(const hofem_mesh_desc* d, void* comm, void* stream,
                                void** mesh_out) {
   if (!d || !mesh_out) { set_error("hofem_mesh_create: NULL argument"); return HOFEM_ERR_ARG; }
-  if (d->p < 1 || d->p > kMaxP || d->nx < 1 || d->ny < 1 || d->nz_global < 1 ||
-      !(d->extent[0] > 0) || !(d->extent[1] > 0) || !(d->extent[2] > 0)) {
-    set_error("hofem_mesh_create: need 1<=p<=%d, n>=1, extents>0", kMaxP);
-    return HOFEM_ERR_ARG;
-  }
-  Comm* c = static_cast<Comm*>(comm);
-  const int R = c ? c->nranks : 1, r = c ? c->rank : 0;
-  if (d->nz_global % R != 0) {
-    set_error("hofem_mesh_create: nranks=%d must divide nz_global=%d", R, d->nz_global);
-    return HOFEM_ERR_ARG;
-  }
-  int dev = 0;
-  HOFEM_CUDA(cudaGetDevice(&dev));
-  auto* m = new Mesh();
-  m->desc = *d;
-  m->comm = c;
-  m->rank = r; m->nranks = R;
-  m->p = d->p; m->P1 = d->p + 1;
-  m->nx = d->nx; m->ny = d->ny; m->nzl = d->nz_global / R; m->z0 = r * m->nzl;
-  m->Nx = (long long)d->p * d->nx + 1;
-  m->Ny = (long long)d->p * d->ny + 1;
-  m->Nzl = (long long)d->p * m->nzl + 1;
-  m->NzG = (long long)d->p * d->nz_global + 1;
-  m->plane = m->Nx * m->Ny;
-  m->n_local = m->plane * m->Nzl;
-  m->n_owned = (r == R - 1) ? m->n_local : m->n_local - m->plane;
-  m->n_global = m->plane * m->NzG;
-  m->elems = (long long)d->nx * d->ny * m->nzl;
-  double xi[kMaxP + 1], w[kMaxP + 1];
-  gll_nodes_weights(d->p, xi, w);
-  hofem_status st = HOFEM_OK;
-#define CK(x) do { st = (x); if (st != HOFEM_OK) { free_mesh(m); return st; } } while (0)
-  CK(dalloc(&m->d_xi, m->P1, "mesh"));
-  CK(dalloc(&m->d_coords, 3 * m->n_local, "mesh coords"));
-  CK(dalloc(&m->d_partials, 4 * kNumSMs + 64, "mesh"));
-  CK(dalloc(&m->d_counter, 4, "mesh"));
-  CK(dalloc(&m->d_scalars, 16, "mesh"));
-  if (R > 1) CK(dalloc(&m->d_recv, 2 * m->plane, "mesh planes"));
-  CK(cuda_status(cudaMemcpyAsync(m->d_xi, xi, sizeof(double) * m->P1, cudaMemcpyHostToDevice,
-                                 S(stream)), "mesh upload"));
-  CK(cuda_status(cudaMemsetAsync(m->d_counter, 0, 4 * sizeof(unsigned), S(stream)), "memset"));
-  CK(mesh_build_coords(m, S(stream)));
-  CK(cuda_status(cudaStreamSynchronize(S(stream)), "mesh_create sync"));
-#undef CK
+  Mesh* m = nullptr;
+  HOFEM_TRY(mesh_new(d, static_cast<Comm*>(comm), S(stream), &m));
   *mesh_out = m;
   return HOFEM_OK;
 }
@@ -385,6 +395,94 @@ hofem_status hofem_dg_fill_random(const void* dg_, unsigned long long seed, doub
 }
 
 void hofem_dg_destroy(void* dg) { dg_destroy(static_cast<DGOp*>(dg)); }
+
+hofem_status hofem_op_diagonal(void* op_, double* d, void* stream) {
+  Op* op = static_cast<Op*>(op_);
+  if (!op || !d) { set_error("hofem_op_diagonal: NULL"); return HOFEM_ERR_ARG; }
+  HOFEM_ALIGNED("hofem_op_diagonal", d);
+  return op_diagonal(op, d, S(stream));
+}
+
+hofem_status hofem_pmg_create(void* mesh, int degree, int power_iters, unsigned long long seed,
+                              void* stream, void** pmg_out) {
+  Mesh* m = static_cast<Mesh*>(mesh);
+  if (!m || !pmg_out) { set_error("hofem_pmg_create: NULL"); return HOFEM_ERR_ARG; }
+  PMG* P = nullptr;
+  HOFEM_TRY(pmg_create(m, degree, power_iters, seed, S(stream), &P));
+  *pmg_out = P;
+  return HOFEM_OK;
+}
+
+hofem_status hofem_pmg_info_get(const void* pmg, hofem_pmg_info* info) {
+  const PMG* P = static_cast<const PMG*>(pmg);
+  if (!P || !info) { set_error("hofem_pmg_info_get: NULL"); return HOFEM_ERR_ARG; }
+  memset(info, 0, sizeof(*info));
+  info->levels = pmg_levels(P);
+  for (int k = 0; k < info->levels && k < 8; ++k) {
+    info->orders[k] = pmg_level_mesh(const_cast<PMG*>(P), k)->p;
+    info->lambda[k] = pmg_level_lambda(P, k);
+  }
+  info->degree = pmg_degree(P);
+  return HOFEM_OK;
+}
+
+hofem_status hofem_pmg_set_lambda(void* pmg, int level, double lambda) {
+  PMG* P = static_cast<PMG*>(pmg);
+  if (!P || level < 0 || level >= pmg_levels(P) || !(lambda > 0)) {
+    set_error("hofem_pmg_set_lambda: bad level or lambda");
+    return HOFEM_ERR_ARG;
+  }
+  pmg_set_lambda(P, level, lambda);
+  return HOFEM_OK;
+}
+
+hofem_status hofem_pmg_level(void* pmg, int level, void** mesh_out, void** op_out) {
+  PMG* P = static_cast<PMG*>(pmg);
+  if (!P || level < 0 || level >= pmg_levels(P)) { set_error("hofem_pmg_level: bad level"); return HOFEM_ERR_ARG; }
+  if (mesh_out) *mesh_out = pmg_level_mesh(P, level);
+  if (op_out) *op_out = pmg_level_op(P, level);
+  return HOFEM_OK;
+}
+
+hofem_status hofem_pmg_vcycle(void* pmg, const double* r, double* z, void* stream) {
+  PMG* P = static_cast<PMG*>(pmg);
+  if (!P || !r || !z || r == z) { set_error("hofem_pmg_vcycle: NULL or aliased"); return HOFEM_ERR_ARG; }
+  HOFEM_ALIGNED("hofem_pmg_vcycle", r, z);
+  return pmg_vcycle_level(P, 0, r, z, S(stream));
+}
+
+hofem_status hofem_pmg_smooth(void* pmg, int level, const double* b, double* x, void* stream) {
+  PMG* P = static_cast<PMG*>(pmg);
+  if (!P || !b || !x || b == x || level < 0 || level >= pmg_levels(P)) {
+    set_error("hofem_pmg_smooth: bad arguments");
+    return HOFEM_ERR_ARG;
+  }
+  HOFEM_ALIGNED("hofem_pmg_smooth", b, x);
+  return pmg_smooth(P, level, b, x, false, S(stream));
+}
+
+hofem_status hofem_pmg_transfer(void* pmg, int level, int dir, const double* in, double* out,
+                                void* stream) {
+  PMG* P = static_cast<PMG*>(pmg);
+  if (!P || !in || !out || in == out || level < 0 || level + 1 >= pmg_levels(P) ||
+      (dir != 0 && dir != 1)) {
+    set_error("hofem_pmg_transfer: bad arguments");
+    return HOFEM_ERR_ARG;
+  }
+  HOFEM_ALIGNED("hofem_pmg_transfer", in, out);
+  return dir == 0 ? pmg_prolong_add(P, level, in, out, S(stream))
+                  : pmg_restrict(P, level, in, out, S(stream));
+}
+
+hofem_status hofem_pmg_pcg(void* pmg, const double* b, double* x, double rel_tol, int max_iter,
+                           double* rr_history, hofem_cg_stats* stats, void* stream) {
+  PMG* P = static_cast<PMG*>(pmg);
+  if (!P || !b || !x || b == x || max_iter < 0) { set_error("hofem_pmg_pcg: bad arguments"); return HOFEM_ERR_ARG; }
+  HOFEM_ALIGNED("hofem_pmg_pcg", b, x);
+  return pmg_pcg(P, b, x, rel_tol, max_iter, rr_history, stats, S(stream));
+}
+
+void hofem_pmg_destroy(void* pmg) { pmg_destroy(static_cast<PMG*>(pmg)); }
 
 hofem_status hofem_dot(const void* mesh, const double* a, const double* b, double* out_host,
                        void* stream) {

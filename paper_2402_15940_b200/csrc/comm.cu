@@ -21,7 +21,7 @@ __global__ void add_plane_kernel(long long plane, long long Nx, long long Ny, lo
   if (bcmode) {
     long long I = t % Nx, J = t / Nx;
     if (I == 0 || I == Nx - 1 || J == 0 || J == Ny - 1 || Kg == 0 || Kg == NzG - 1)
-      v = bcmode == 1 ? xbc[t] : 0.0;
+      v = bcmode == 1 ? xbc[t] : (bcmode == 3 ? 1.0 : 0.0);
   }
   y[t] = v;
 }
@@ -35,6 +35,11 @@ hofem_status nccl_status(ncclResult_t r, const char* what) {
 }  // namespace
 
 hofem_status exchange_planes(Op* op, const double* x, double* y, cudaStream_t s) {
+  return exchange_planes_bc(op, x, y, op->bc ? (x ? 1 : 2) : 0, s);
+}
+
+// bcmode on the summed planes' Dirichlet points: 0 none, 1 y = x, 2 y = 0, 3 y = 1
+hofem_status exchange_planes_bc(Op* op, const double* x, double* y, int bcmode, cudaStream_t s) {
   Mesh* m = op->mesh;
   if (m->nranks <= 1) return HOFEM_OK;
   const long long plane = m->plane;
@@ -52,7 +57,6 @@ hofem_status exchange_planes(Op* op, const double* x, double* y, cudaStream_t s)
                           "ncclRecv hi"));
   }
   HOFEM_TRY(nccl_status(ncclGroupEnd(), "ncclGroupEnd"));
-  const int bcmode = op->bc ? (x ? 1 : 2) : 0;
   const unsigned g = (unsigned)((plane + 255) / 256);
   const long long K0 = (long long)m->p * m->z0;
   if (r > 0) {

@@ -250,17 +250,29 @@ __global__ void __launch_bounds__(NT) dg_mass_simt(const __grid_constant__ Tab<P
   }
 }
 
-// Per-P1 batch shapes (elements per batch, threads): stage-3 items NE*Q^2 ~ NT.
+// Per-P1 batch shapes (elements per batch, threads): stage-3 items NE*Q^2 <= NT,
+// shared memory small enough for several CTAs per SM (bytes in flight and
+// barrier-latency hiding).  -DHOFEM_DG_NE=.. -DHOFEM_DG_NT=.. overrides the
+// shape of the P1 being compiled (tuning builds, scripts/build_pvariant.py).
 template <int P1>
-struct ShapeDG;
-template <> struct ShapeDG<2> { static constexpr int NE = 28, NT = 256; };
-template <> struct ShapeDG<3> { static constexpr int NE = 16, NT = 256; };
-template <> struct ShapeDG<4> { static constexpr int NE = 10, NT = 256; };
-template <> struct ShapeDG<5> { static constexpr int NE = 8, NT = 288; };
-template <> struct ShapeDG<6> { static constexpr int NE = 6, NT = 288; };
-template <> struct ShapeDG<7> { static constexpr int NE = 4, NT = 256; };
-template <> struct ShapeDG<8> { static constexpr int NE = 4, NT = 320; };
-template <> struct ShapeDG<9> { static constexpr int NE = 2, NT = 224; };
+struct ShapeDGD;
+template <> struct ShapeDGD<2> { static constexpr int NE = 16, NT = 160; };
+template <> struct ShapeDGD<3> { static constexpr int NE = 8, NT = 128; };
+template <> struct ShapeDGD<4> { static constexpr int NE = 4, NT = 128; };
+template <> struct ShapeDGD<5> { static constexpr int NE = 4, NT = 160; };
+template <> struct ShapeDGD<6> { static constexpr int NE = 2, NT = 128; };
+template <> struct ShapeDGD<7> { static constexpr int NE = 2, NT = 128; };
+template <> struct ShapeDGD<8> { static constexpr int NE = 2, NT = 192; };
+template <> struct ShapeDGD<9> { static constexpr int NE = 2, NT = 224; };
+#if defined(HOFEM_DG_NE) && defined(HOFEM_DG_NT)
+template <int P1>
+struct ShapeDG {
+  static constexpr int NE = HOFEM_DG_NE, NT = HOFEM_DG_NT;
+};
+#else
+template <int P1>
+struct ShapeDG : ShapeDGD<P1> {};
+#endif
 
 // Defined per P1 in dg_p.cu (Q = P1 + 1, the Gauss rule of reading R2).
 template <int P1>

@@ -1746,6 +1746,8 @@ __global__ void __maxnreg__(MAXR)
   unsigned qphase = 0;
   const long long st = (long long)gridDim.x * NT;
   const long long t0 = (long long)blockIdx.x * NT + threadIdx.x;
+  constexpr int CGU = 4;           // 16-byte pairs in flight per thread (vector phases)
+  const long long np = G.n >> 1;  // vectors are 16-byte aligned (hofem.h)
   if (G.zero_ap)
     for (long long i = t0; i < G.n; i += st) G.Ap[i] = 0.0;
   grid_barrier(A.bar);
@@ -1768,21 +1770,74 @@ __global__ void __maxnreg__(MAXR)
       break;
     }
     const double alpha = rr / pAp;
+    // r -= alpha Ap, r.r terms: 16-byte pairs, CGU pairs in flight per thread
     double s = 0.0;
-    for (long long i = t0; i < G.n; i += st) {
-      const double v = fma(-alpha, __ldcg(G.Ap + i), G.r[i]);
-      G.r[i] = v;
-      s = fma(v, v, s);
+    {
+      const double2* A2 = reinterpret_cast<const double2*>(G.Ap);
+      double2* r2 = reinterpret_cast<double2*>(G.r);
+      for (long long i0 = t0; i0 < np; i0 += (long long)CGU * st) {
+        double2 a[CGU], v[CGU];
+#pragma unroll
+        for (int u = 0; u < CGU; ++u) {
+          const long long i = i0 + u * st;
+          if (i < np) { a[u] = __ldcg(A2 + i); v[u] = r2[i]; }
+        }
+#pragma unroll
+        for (int u = 0; u < CGU; ++u) {
+          const long long i = i0 + u * st;
+          if (i < np) {
+            v[u].x = fma(-alpha, a[u].x, v[u].x);
+            v[u].y = fma(-alpha, a[u].y, v[u].y);
+            r2[i] = v[u];
+            s = fma(v[u].x, v[u].x, s);
+            s = fma(v[u].y, v[u].y, s);
+          }
+        }
+      }
+      if ((G.n & 1) && t0 == 0) {
+        const double v = fma(-alpha, __ldcg(G.Ap + G.n - 1), G.r[G.n - 1]);
+        G.r[G.n - 1] = v;
+        s = fma(v, v, s);
+      }
     }
     block_sum_store(s, G.parts2 + blockIdx.x, smem);
     grid_barrier(A.bar);
     const double rn = grid_sum<NT>(G.parts2, smem);
     const double beta = rr > 0.0 ? rn / rr : 0.0;
-    for (long long i = t0; i < G.n; i += st) {
-      const double pv = G.p[i];
-      G.x[i] = fma(alpha, pv, G.x[i]);
-      G.p[i] = fma(beta, pv, G.r[i]);
-      if (G.zero_ap) G.Ap[i] = 0.0;
+    {
+      // x += alpha p; p = r + beta p; Ap = 0 for the next pass
+      double2* x2 = reinterpret_cast<double2*>(G.x);
+      double2* p2 = reinterpret_cast<double2*>(G.p);
+      const double2* r2 = reinterpret_cast<const double2*>(G.r);
+      double2* A2 = reinterpret_cast<double2*>(G.Ap);
+      for (long long i0 = t0; i0 < np; i0 += (long long)CGU * st) {
+        double2 pv[CGU], xv[CGU], rv[CGU];
+#pragma unroll
+        for (int u = 0; u < CGU; ++u) {
+          const long long i = i0 + u * st;
+          if (i < np) { pv[u] = p2[i]; xv[u] = x2[i]; rv[u] = r2[i]; }
+        }
+#pragma unroll
+        for (int u = 0; u < CGU; ++u) {
+          const long long i = i0 + u * st;
+          if (i < np) {
+            xv[u].x = fma(alpha, pv[u].x, xv[u].x);
+            xv[u].y = fma(alpha, pv[u].y, xv[u].y);
+            x2[i] = xv[u];
+            rv[u].x = fma(beta, pv[u].x, rv[u].x);
+            rv[u].y = fma(beta, pv[u].y, rv[u].y);
+            p2[i] = rv[u];
+            if (G.zero_ap) A2[i] = make_double2(0.0, 0.0);
+          }
+        }
+      }
+      if ((G.n & 1) && t0 == 0) {
+        const long long i = G.n - 1;
+        const double pv = G.p[i];
+        G.x[i] = fma(alpha, pv, G.x[i]);
+        G.p[i] = fma(beta, pv, G.r[i]);
+        if (G.zero_ap) G.Ap[i] = 0.0;
+      }
     }
     ++k;
     rr = rn;

@@ -116,10 +116,35 @@ struct Op {
   int cg_cap = 0;
 };
 
+// p-multigrid (pmg.cu; §8(f) f2)
+struct PMG;
+hofem_status op_diagonal(Op* op, double* d, cudaStream_t s);
+hofem_status pmg_create(Mesh* fine, int degree, int power_iters, unsigned long long seed,
+                        cudaStream_t s, PMG** out);
+void pmg_destroy(PMG* P);
+hofem_status pmg_vcycle_level(PMG* P, int k, const double* b, double* z, cudaStream_t s);
+hofem_status pmg_smooth(PMG* P, int k, const double* b, double* x, bool x_zero, cudaStream_t s);
+hofem_status pmg_prolong_add(PMG* P, int k, const double* xc, double* xf, cudaStream_t s);
+hofem_status pmg_restrict(PMG* P, int k, const double* rf, double* rc, cudaStream_t s);
+hofem_status pmg_pcg(PMG* P, const double* b, double* x, double rel_tol, int max_iter,
+                     double* rr_history, hofem_cg_stats* stats, cudaStream_t s);
+int pmg_levels(const PMG* P);
+Mesh* pmg_level_mesh(PMG* P, int k);
+Op* pmg_level_op(PMG* P, int k);
+double pmg_level_lambda(const PMG* P, int k);
+void pmg_set_lambda(PMG* P, int k, double lam);
+int pmg_degree(const PMG* P);
+
 // Operator construction / destruction (capi.cu): qdata, tables; SYNC.
 hofem_status op_new(Mesh* m, int kind, int rule, int q_override, int bc, cudaStream_t s,
                     Op** out);
 void op_free(Op* op);
+hofem_status mesh_new(const hofem_mesh_desc* d, Comm* comm, cudaStream_t s, Mesh** out);
+void mesh_free(Mesh* m);
+// E-vector -> L-vector deterministic scatter through the transposed offsets
+// (unfused.cu).  bcmode: 0 none, 1 y[ess] = xbc[ess], 2 y[ess] = 0, 3 y[ess] = 1.
+hofem_status scatter_evector_bc(Op* op, const double* ein, double* y, int bcmode,
+                                const double* xbc, cudaStream_t s);
 
 // DG (L2) mass operator (dg.cu, dg_impl.cuh; §8(f) f4)
 struct DGOp {
@@ -171,6 +196,7 @@ bool fused_supported(const Op* op);
 
 // ---- comm (comm.cu): sum duplicated interface planes, fix BC there
 hofem_status exchange_planes(Op* op, const double* x, double* y, cudaStream_t s);
+hofem_status exchange_planes_bc(Op* op, const double* x, double* y, int bcmode, cudaStream_t s);
 hofem_status allreduce_sum(Mesh* m, double* d_val, int count, cudaStream_t s);
 
 // ---- vector kernels (cg.cu)

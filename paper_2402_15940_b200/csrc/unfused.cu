@@ -29,7 +29,7 @@ __global__ void gather_kernel(long long ent, const int* __restrict__ l2e,
   ein[t] = (bc && ess_at(es, l)) ? 0.0 : x[l];
 }
 
-// bcmode: 0 none, 1 y[ess] = xbc[ess], 2 y[ess] = 0
+// bcmode: 0 none, 1 y[ess] = xbc[ess], 2 y[ess] = 0, 3 y[ess] = 1
 __global__ void scatter_kernel(long long n, const long long* __restrict__ toff,
                                const int* __restrict__ tidx, const double* __restrict__ eout,
                                int bcmode, const double* __restrict__ xbc, EssInfo es,
@@ -38,7 +38,7 @@ __global__ void scatter_kernel(long long n, const long long* __restrict__ toff,
   if (l >= n) return;
   double s = 0.0;
   for (long long k = toff[l]; k < toff[l + 1]; ++k) s += eout[tidx[k]];
-  if (bcmode && ess_at(es, l)) s = (bcmode == 1) ? xbc[l] : 0.0;
+  if (bcmode && ess_at(es, l)) s = (bcmode == 1) ? xbc[l] : (bcmode == 3 ? 1.0 : 0.0);
   y[l] = s;
 }
 

@@ -14,7 +14,9 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libhofem.so")
+# HOFEM_LIB_PATH: load a tuning build (scripts/build_pvariant.py) instead of the
+# in-tree library; the default is the in-tree libhofem.so.
+LIB_PATH = os.environ.get("HOFEM_LIB_PATH") or os.path.join(_PKG, "libhofem.so")
 
 MASS, DIFFUSION = 1, 2
 GAUSS, GLL = 1, 2
@@ -64,6 +66,11 @@ class DGInfo(ctypes.Structure):
                 ("dofs_per_elem", ctypes.c_int), ("grid", ctypes.c_int)]
 
 
+class PMGInfo(ctypes.Structure):
+    _fields_ = [("levels", ctypes.c_int), ("orders", ctypes.c_int * 8),
+                ("lambda_", ctypes.c_double * 8), ("degree", ctypes.c_int)]
+
+
 class CGStats(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int), ("converged", ctypes.c_int),
                 ("r0_norm", ctypes.c_double), ("final_rel_res", ctypes.c_double)]
@@ -94,6 +101,16 @@ SIGNATURES = {
     "hofem_dg_apply": (_I, [_V, _V, _V, _V]),
     "hofem_dg_fill_random": (_I, [_V, ctypes.c_ulonglong, _V, _V]),
     "hofem_dg_destroy": (None, [_V]),
+    "hofem_op_diagonal": (_I, [_V, _V, _V]),
+    "hofem_pmg_create": (_I, [_V, _I, _I, ctypes.c_ulonglong, _V, _PV]),
+    "hofem_pmg_info_get": (_I, [_V, ctypes.POINTER(PMGInfo)]),
+    "hofem_pmg_set_lambda": (_I, [_V, _I, _D]),
+    "hofem_pmg_level": (_I, [_V, _I, _PV, _PV]),
+    "hofem_pmg_vcycle": (_I, [_V, _V, _V, _V]),
+    "hofem_pmg_smooth": (_I, [_V, _I, _V, _V, _V]),
+    "hofem_pmg_transfer": (_I, [_V, _I, _I, _V, _V, _V]),
+    "hofem_pmg_pcg": (_I, [_V, _V, _V, _D, _I, _V, ctypes.POINTER(CGStats), _V]),
+    "hofem_pmg_destroy": (None, [_V]),
     "hofem_cg": (_I, [_V, _V, _V, _D, _I, _I, _I, _V, ctypes.POINTER(CGStats), _V]),
     "hofem_dot": (_I, [_V, _V, _V, ctypes.POINTER(_D), _V]),
     "hofem_op_apply_dot": (_I, [_V, _V, _V, ctypes.POINTER(_D), _V]),
@@ -313,9 +330,103 @@ class Operator:
         rr = list(hist[: stats.iterations + 1]) if history else None
         return st, stats, rr
 
+    def diagonal(self, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """diag(A) by sum factorization (hofem_op_diagonal); Dirichlet rows 1."""
+        out = torch.empty(self.mesh.n_local, dtype=torch.float64, device="cuda") if out is None else out
+        _check(lib().hofem_op_diagonal(self.handle, _ptr(out, self.mesh.n_local), _stream(stream)))
+        return out
+
     def close(self):
         if self.handle:
             lib().hofem_op_destroy(self.handle)
+            self.handle = None
+
+
+class _Borrowed:
+    """A level's mesh / operator owned by a PMG handle (never destroyed here)."""
+
+
+class PMG:
+    """p-multigrid V-cycle and preconditioned CG on a fine BP3 mesh (hofem_pmg_*;
+    §8(f) f2).  Level 0 is the finest; level k vectors have levels[k].n_local."""
+
+    def __init__(self, mesh: Mesh, degree=3, power_iters=10, seed=1, stream=None):
+        h = ctypes.c_void_p()
+        _check(lib().hofem_pmg_create(mesh.handle, degree, power_iters, ctypes.c_ulonglong(seed),
+                                      _stream(stream), ctypes.byref(h)))
+        self.handle = h
+        self.mesh = mesh
+        info = self.info()
+        self.orders = list(info.orders[: info.levels])
+        self.levels = []
+        for k in range(info.levels):
+            mh, oh = ctypes.c_void_p(), ctypes.c_void_p()
+            _check(lib().hofem_pmg_level(h, k, ctypes.byref(mh), ctypes.byref(oh)))
+            mi = MeshInfo()
+            _check(lib().hofem_mesh_info_get(mh, ctypes.byref(mi)))
+            lv = _Borrowed()
+            lv.mesh_handle, lv.op_handle, lv.n_local, lv.p = mh, oh, mi.n_local, self.orders[k]
+            self.levels.append(lv)
+
+    def info(self) -> PMGInfo:
+        s = PMGInfo()
+        _check(lib().hofem_pmg_info_get(self.handle, ctypes.byref(s)))
+        return s
+
+    def lambdas(self):
+        i = self.info()
+        return list(i.lambda_[: i.levels])
+
+    def set_lambda(self, level: int, lam: float):
+        _check(lib().hofem_pmg_set_lambda(self.handle, level, float(lam)))
+
+    def vec(self, level: int) -> torch.Tensor:
+        return torch.zeros(self.levels[level].n_local, dtype=torch.float64, device="cuda")
+
+    def apply(self, level: int, x: torch.Tensor, y: torch.Tensor | None = None, stream=None):
+        y = torch.empty_like(x) if y is None else y
+        n = self.levels[level].n_local
+        _check(lib().hofem_op_apply(self.levels[level].op_handle, _ptr(x, n), _ptr(y, n),
+                                    _stream(stream)))
+        return y
+
+    def vcycle(self, r: torch.Tensor, z: torch.Tensor | None = None, stream=None):
+        z = torch.empty_like(r) if z is None else z
+        n = self.levels[0].n_local
+        _check(lib().hofem_pmg_vcycle(self.handle, _ptr(r, n), _ptr(z, n), _stream(stream)))
+        return z
+
+    def smooth(self, level: int, b: torch.Tensor, x: torch.Tensor, stream=None):
+        n = self.levels[level].n_local
+        _check(lib().hofem_pmg_smooth(self.handle, level, _ptr(b, n), _ptr(x, n), _stream(stream)))
+        return x
+
+    def prolong_add(self, level: int, xc: torch.Tensor, xf: torch.Tensor, stream=None):
+        _check(lib().hofem_pmg_transfer(self.handle, level, 0, _ptr(xc, self.levels[level + 1].n_local),
+                                        _ptr(xf, self.levels[level].n_local), _stream(stream)))
+        return xf
+
+    def restrict(self, level: int, rf: torch.Tensor, rc: torch.Tensor | None = None, stream=None):
+        rc = self.vec(level + 1) if rc is None else rc
+        _check(lib().hofem_pmg_transfer(self.handle, level, 1, _ptr(rf, self.levels[level].n_local),
+                                        _ptr(rc, self.levels[level + 1].n_local), _stream(stream)))
+        return rc
+
+    def pcg(self, b: torch.Tensor, x: torch.Tensor, rel_tol=1e-10, max_iter=500, history=False,
+            stream=None):
+        stats = CGStats()
+        hist = (ctypes.c_double * (max_iter + 1))() if history else None
+        n = self.levels[0].n_local
+        st = lib().hofem_pmg_pcg(self.handle, _ptr(b, n), _ptr(x, n), rel_tol, max_iter, hist,
+                                 ctypes.byref(stats), _stream(stream))
+        if st not in (OK, NOT_CONVERGED):
+            _check(st)
+        rr = list(hist[: stats.iterations + 1]) if history else None
+        return st, stats, rr
+
+    def close(self):
+        if self.handle:
+            lib().hofem_pmg_destroy(self.handle)
             self.handle = None
 
 

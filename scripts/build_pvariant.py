@@ -1,7 +1,9 @@
-"""Fast kernel-tuning variant: recompile only fused_p.cu for one P1 with extra
--D flags and relink against the in-tree objects (run the normal build first).
+"""Fast kernel-tuning variant: recompile only one per-P1 unit (fused_p.cu, or
+dg_p.cu with --src dg_p) for one P1 with extra -D flags and relink against the
+in-tree objects (run the normal build first).
 
-    python scripts/build_pvariant.py NAME P1 -DFLAG=... [...]   ->  scratch/libhofem_NAME.so
+    python scripts/build_pvariant.py [--src dg_p] NAME P1 -DFLAG=... [...]
+        ->  scratch/libhofem_NAME.so   (load it with HOFEM_LIB_PATH=...)
 """
 import os
 import subprocess
@@ -10,16 +12,20 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2402_15940_b200 import build as B  # noqa: E402
 
-name, p1, flags = sys.argv[1], int(sys.argv[2]), sys.argv[3:]
+args = sys.argv[1:]
+unit = "fused_p"
+if args and args[0] == "--src":
+    unit, args = args[1], args[2:]
+name, p1, flags = args[0], int(args[1]), args[2:]
 B.build()
 os.makedirs("scratch/obj", exist_ok=True)
-src = os.path.join(B.CSRC, "fused_p.cu")
-obj = os.path.abspath(f"scratch/obj/fused_p{p1}_{name}.o")
+src = os.path.join(B.CSRC, f"{unit}.cu")
+obj = os.path.abspath(f"scratch/obj/{unit}{p1}_{name}.o")
 cmd = [B.NVCC] + B._common_flags() + [f"-DHOFEM_P1={p1}"] + flags + ["-c", src, "-o", obj]
 r = subprocess.run(cmd, capture_output=True, text=True)
 if r.returncode:
     sys.exit(r.stderr)
-objs = [obj if os.path.basename(j[1]) == f"fused_p{p1}.o" else j[1] for j in B._jobs()]
+objs = [obj if os.path.basename(j[1]) == f"{unit}{p1}.o" else j[1] for j in B._jobs()]
 nccl = B._nccl_dir()
 out = os.path.abspath(f"scratch/libhofem_{name}.so")
 cmd = [B.NVCC] + B.ARCH + ["-shared", "-o", out] + objs + [
