@@ -131,6 +131,16 @@ hofem_status hofem_op_apply(void* op, const double* x, double* y, void* stream);
  * table) -> element kernel -> deterministic scatter through precomputed
  * transposed offsets (R^T, ascending (e, i) order). */
 hofem_status hofem_op_apply_unfused(void* op, const double* x, double* y, void* stream);
+/* y = A x, "Fully Matrix-Free" assembly level (§2.2; §8(f) f3):
+ * the same operator as hofem_op_apply, but the quadrature data is NOT read --
+ * every call recomputes J = dX/dxi at the quadrature points from the nodal
+ * coordinates by sum factorization, then adj(J), detJ and
+ * D = W adj(J)adj(J)^T / detJ pointwise, in the kernel.  One persistent kernel
+ * per apply writes element results to an E-vector, then the deterministic
+ * transposed-offset scatter (ascending (e, i)) assembles y; Dirichlet rows
+ * y = x.  BP3 only (DIFFUSION, Gauss Q = p+2), else HOFEM_ERR_ARG. */
+hofem_status hofem_op_apply_mf(void* op, const double* x, double* y, void* stream);
+
 /* SYNC.  y = A x (as hofem_op_apply) and *dot_host = x.y over owned dofs,
  * allreduced -- the x^T A x energy that CG needs as p^T A p.  On the fused
  * path the product is accumulated inside the operator kernels from the values

@@ -316,6 +316,13 @@ hofem_status hofem_op_apply_unfused(void* op_, const double* x, double* y, void*
   return apply_unfused(op, x, y, S(stream));
 }
 
+hofem_status hofem_op_apply_mf(void* op_, const double* x, double* y, void* stream) {
+  Op* op = static_cast<Op*>(op_);
+  if (!op || !x || !y || x == y) { set_error("hofem_op_apply_mf: NULL or aliased x/y"); return HOFEM_ERR_ARG; }
+  HOFEM_ALIGNED("hofem_op_apply_mf", x, y);
+  return apply_mf(op, x, y, S(stream));
+}
+
 hofem_status hofem_op_qdata(const void* op_, const double** qdata, long long* count) {
   const Op* op = static_cast<const Op*>(op_);
   if (!op || !qdata || !count) { set_error("hofem_op_qdata: NULL"); return HOFEM_ERR_ARG; }

@@ -54,7 +54,7 @@ FusedLaunch shape_for(int P1, int kind, int Q) {
     HOFEM_FOR_P1(HOFEM_CASE)
 #undef HOFEM_CASE
   }
-  return FusedLaunch{0, 0, 0, 1};
+  return FusedLaunch{0, 0, 0, 1, 1};
 }
 
 int fused_kind(const Op* op) {
@@ -160,11 +160,12 @@ struct Plan {
   int nbx, nby, zc, nchunks, grid;
   long long ncol, nbricks, nunits;
 };
-Plan make_plan(const Op* op) {
+Plan make_plan(const Op* op, bool for_cg = false) {
   const Mesh* m = op->mesh;
   Plan P;
   P.kind = fused_kind(op);
   P.L = shape_for(m->P1, P.kind, op->Q);
+  if (for_cg) P.L.ctas_per_sm = P.L.ctas_per_sm_cg;
   P.nbx = (m->nx + P.L.BX - 1) / P.L.BX;
   P.nby = (m->ny + P.L.BY - 1) / P.L.BY;
   P.ncol = (long long)P.nbx * P.nby;
@@ -214,11 +215,12 @@ hofem_status ensure_bar(Op* op) {
   return HOFEM_OK;
 }
 
-hofem_status prepare(Op* op, const double* x, double* y, bool fdot, Prepared* out) {
+hofem_status prepare(Op* op, const double* x, double* y, bool fdot, Prepared* out,
+                     bool for_cg = false) {
   Mesh* m = op->mesh;
   const int p = m->p;
   Prepared& R = *out;
-  R.PL = make_plan(op);
+  R.PL = make_plan(op, for_cg);
   const Plan& PL = R.PL;
   const FusedLaunch L = PL.L;
   HOFEM_TRY(grow(&op->d_bbuf, &op->bbuf_len, PL.nbricks * L.face_block,
@@ -387,7 +389,7 @@ hofem_status cg_persistent(Op* op, double* x, double* r, double* p, double* Ap, 
     return HOFEM_ERR_ARG;
   }
   Prepared R;
-  HOFEM_TRY(prepare(op, p, Ap, false, &R));
+  HOFEM_TRY(prepare(op, p, Ap, false, &R, true));
   const Plan& PL = R.PL;
   HOFEM_TRY(ensure_bar(op));
   HOFEM_TRY(grow(&op->d_cgparts, &op->cgparts_len, 2LL * PL.grid, "the CG partials"));

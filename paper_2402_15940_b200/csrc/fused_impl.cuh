@@ -1736,6 +1736,89 @@ __device__ __forceinline__ double grid_sum(const double* parts, double* red) {
   return total;
 }
 
+// Vector phases of the persistent CG as separate (not inlined) functions: their
+// 16-byte, CGU-deep load batches would otherwise raise the register pressure of
+// the inlined brick pass (spills); a call per phase per iteration is free.
+// Grid-stride over 16-byte pairs (vectors are 16-byte aligned, hofem.h); the
+// traversal order is fixed, so the returned partial is deterministic.
+constexpr int CGU = 4;
+
+// r -= alpha Ap; returns this thread's share of r.r
+static __device__ __noinline__ double cg_r_update(long long n, double alpha, const double* Ap,
+                                           double* r) {
+  const long long st = (long long)gridDim.x * blockDim.x;
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long np = n >> 1;
+  const double2* A2 = reinterpret_cast<const double2*>(Ap);
+  double2* r2 = reinterpret_cast<double2*>(r);
+  double s = 0.0;
+  for (long long i0 = t0; i0 < np; i0 += (long long)CGU * st) {
+    double2 a[CGU], v[CGU];
+#pragma unroll
+    for (int u = 0; u < CGU; ++u) {
+      const long long i = i0 + u * st;
+      if (i < np) { a[u] = __ldcg(A2 + i); v[u] = r2[i]; }
+    }
+#pragma unroll
+    for (int u = 0; u < CGU; ++u) {
+      const long long i = i0 + u * st;
+      if (i < np) {
+        v[u].x = fma(-alpha, a[u].x, v[u].x);
+        v[u].y = fma(-alpha, a[u].y, v[u].y);
+        r2[i] = v[u];
+        s = fma(v[u].x, v[u].x, s);
+        s = fma(v[u].y, v[u].y, s);
+      }
+    }
+  }
+  if ((n & 1) && t0 == 0) {
+    const double v = fma(-alpha, __ldcg(Ap + n - 1), r[n - 1]);
+    r[n - 1] = v;
+    s = fma(v, v, s);
+  }
+  return s;
+}
+
+// x += alpha p; p = r + beta p; Ap = 0 (for the next pass) if zero_ap
+static __device__ __noinline__ void cg_xp_update(long long n, double alpha, double beta, double* x,
+                                          double* p, const double* r, double* Ap, int zero_ap) {
+  const long long st = (long long)gridDim.x * blockDim.x;
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long np = n >> 1;
+  double2* x2 = reinterpret_cast<double2*>(x);
+  double2* p2 = reinterpret_cast<double2*>(p);
+  const double2* r2 = reinterpret_cast<const double2*>(r);
+  double2* A2 = reinterpret_cast<double2*>(Ap);
+  for (long long i0 = t0; i0 < np; i0 += (long long)CGU * st) {
+    double2 pv[CGU], xv[CGU], rv[CGU];
+#pragma unroll
+    for (int u = 0; u < CGU; ++u) {
+      const long long i = i0 + u * st;
+      if (i < np) { pv[u] = p2[i]; xv[u] = x2[i]; rv[u] = r2[i]; }
+    }
+#pragma unroll
+    for (int u = 0; u < CGU; ++u) {
+      const long long i = i0 + u * st;
+      if (i < np) {
+        xv[u].x = fma(alpha, pv[u].x, xv[u].x);
+        xv[u].y = fma(alpha, pv[u].y, xv[u].y);
+        x2[i] = xv[u];
+        rv[u].x = fma(beta, pv[u].x, rv[u].x);
+        rv[u].y = fma(beta, pv[u].y, rv[u].y);
+        p2[i] = rv[u];
+        if (zero_ap) A2[i] = make_double2(0.0, 0.0);
+      }
+    }
+  }
+  if ((n & 1) && t0 == 0) {
+    const long long i = n - 1;
+    const double pv = p[i];
+    x[i] = fma(alpha, pv, x[i]);
+    p[i] = fma(beta, pv, r[i]);
+    if (zero_ap) Ap[i] = 0.0;
+  }
+}
+
 template <int KIND, int P1, int Q, int BX, int BY, int NT, int MAXR, bool EO>
 __global__ void __maxnreg__(MAXR)
     cg_persistent_simt(const __grid_constant__ Tab<P1, Q> T, const __grid_constant__ ColArgs A,
@@ -1746,8 +1829,6 @@ __global__ void __maxnreg__(MAXR)
   unsigned qphase = 0;
   const long long st = (long long)gridDim.x * NT;
   const long long t0 = (long long)blockIdx.x * NT + threadIdx.x;
-  constexpr int CGU = 4;           // 16-byte pairs in flight per thread (vector phases)
-  const long long np = G.n >> 1;  // vectors are 16-byte aligned (hofem.h)
   if (G.zero_ap)
     for (long long i = t0; i < G.n; i += st) G.Ap[i] = 0.0;
   grid_barrier(A.bar);
@@ -1770,75 +1851,12 @@ __global__ void __maxnreg__(MAXR)
       break;
     }
     const double alpha = rr / pAp;
-    // r -= alpha Ap, r.r terms: 16-byte pairs, CGU pairs in flight per thread
-    double s = 0.0;
-    {
-      const double2* A2 = reinterpret_cast<const double2*>(G.Ap);
-      double2* r2 = reinterpret_cast<double2*>(G.r);
-      for (long long i0 = t0; i0 < np; i0 += (long long)CGU * st) {
-        double2 a[CGU], v[CGU];
-#pragma unroll
-        for (int u = 0; u < CGU; ++u) {
-          const long long i = i0 + u * st;
-          if (i < np) { a[u] = __ldcg(A2 + i); v[u] = r2[i]; }
-        }
-#pragma unroll
-        for (int u = 0; u < CGU; ++u) {
-          const long long i = i0 + u * st;
-          if (i < np) {
-            v[u].x = fma(-alpha, a[u].x, v[u].x);
-            v[u].y = fma(-alpha, a[u].y, v[u].y);
-            r2[i] = v[u];
-            s = fma(v[u].x, v[u].x, s);
-            s = fma(v[u].y, v[u].y, s);
-          }
-        }
-      }
-      if ((G.n & 1) && t0 == 0) {
-        const double v = fma(-alpha, __ldcg(G.Ap + G.n - 1), G.r[G.n - 1]);
-        G.r[G.n - 1] = v;
-        s = fma(v, v, s);
-      }
-    }
+    const double s = cg_r_update(G.n, alpha, G.Ap, G.r);
     block_sum_store(s, G.parts2 + blockIdx.x, smem);
     grid_barrier(A.bar);
     const double rn = grid_sum<NT>(G.parts2, smem);
     const double beta = rr > 0.0 ? rn / rr : 0.0;
-    {
-      // x += alpha p; p = r + beta p; Ap = 0 for the next pass
-      double2* x2 = reinterpret_cast<double2*>(G.x);
-      double2* p2 = reinterpret_cast<double2*>(G.p);
-      const double2* r2 = reinterpret_cast<const double2*>(G.r);
-      double2* A2 = reinterpret_cast<double2*>(G.Ap);
-      for (long long i0 = t0; i0 < np; i0 += (long long)CGU * st) {
-        double2 pv[CGU], xv[CGU], rv[CGU];
-#pragma unroll
-        for (int u = 0; u < CGU; ++u) {
-          const long long i = i0 + u * st;
-          if (i < np) { pv[u] = p2[i]; xv[u] = x2[i]; rv[u] = r2[i]; }
-        }
-#pragma unroll
-        for (int u = 0; u < CGU; ++u) {
-          const long long i = i0 + u * st;
-          if (i < np) {
-            xv[u].x = fma(alpha, pv[u].x, xv[u].x);
-            xv[u].y = fma(alpha, pv[u].y, xv[u].y);
-            x2[i] = xv[u];
-            rv[u].x = fma(beta, pv[u].x, rv[u].x);
-            rv[u].y = fma(beta, pv[u].y, rv[u].y);
-            p2[i] = rv[u];
-            if (G.zero_ap) A2[i] = make_double2(0.0, 0.0);
-          }
-        }
-      }
-      if ((G.n & 1) && t0 == 0) {
-        const long long i = G.n - 1;
-        const double pv = G.p[i];
-        G.x[i] = fma(alpha, pv, G.x[i]);
-        G.p[i] = fma(beta, pv, G.r[i]);
-        if (G.zero_ap) G.Ap[i] = 0.0;
-      }
-    }
+    cg_xp_update(G.n, alpha, beta, G.x, G.p, G.r, G.Ap, G.zero_ap);
     ++k;
     rr = rn;
     if (blockIdx.x == 0 && threadIdx.x == 0) G.rr[k] = rn;
@@ -1927,7 +1945,13 @@ using ShapeSK = std::conditional_t<KIND == KIND_COLLOC, ShapeSC<P1>,
 
 struct FusedLaunch {
   int BX, BY, face_block, ctas_per_sm;  // face_block = FaceLayout<>::FB
+  int ctas_per_sm_cg;                   // the persistent CG kernel (own register cap)
 };
+
+// Register cap of the persistent CG kernel: the brick pass inside an iteration
+// loop carries more live state than the apply kernel; 32 more registers (fewer
+// resident CTAs) instead of spilling inside the contraction stages.
+constexpr int cg_maxr(int maxr) { return maxr + 32 > 255 ? 255 : maxr + 32; }
 
 // Defined per P1 in fused_p.cu: kind in {KIND_MASS, KIND_DIFF, KIND_COLLOC},
 // Q in {P1, P1+1} for MASS/DIFF and Q == P1 for COLLOC.  Return false if the

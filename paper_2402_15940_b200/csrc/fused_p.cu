@@ -23,7 +23,8 @@ auto simt_kernel() {
 template <int KIND, int P1, int Q>
 auto cg_kernel() {
   using S = ShapeSK<KIND, P1>;
-  return cg_persistent_simt<KIND, P1, Q, S::BX, S::BY, S::NT, S::MAXR, HOFEM_SIMT_EO != 0>;
+  return cg_persistent_simt<KIND, P1, Q, S::BX, S::BY, S::NT, cg_maxr(S::MAXR),
+                            HOFEM_SIMT_EO != 0>;
 }
 template <int KIND, int P1, int Q>
 constexpr int simt_smem() {
@@ -95,11 +96,14 @@ int occupancy(K kern, int threads, int smem, int fallback) {
 template <int KIND, int P1, int Q>
 int simt_ctas_per_sm() {
   using S = ShapeSK<KIND, P1>;
-  static const int n = [] {
-    const int a = occupancy(simt_kernel<KIND, P1, Q>(), S::NT, simt_smem<KIND, P1, Q>(), S::CPS);
-    const int b = occupancy(cg_kernel<KIND, P1, Q>(), S::NT, simt_smem<KIND, P1, Q>(), S::CPS);
-    return a < b ? a : b;  // one grid serves both kernels
-  }();
+  static const int n =
+      occupancy(simt_kernel<KIND, P1, Q>(), S::NT, simt_smem<KIND, P1, Q>(), S::CPS);
+  return n;
+}
+template <int KIND, int P1, int Q>
+int cg_ctas_per_sm() {
+  using S = ShapeSK<KIND, P1>;
+  static const int n = occupancy(cg_kernel<KIND, P1, Q>(), S::NT, simt_smem<KIND, P1, Q>(), 1);
   return n;
 }
 
@@ -107,9 +111,10 @@ template <int KIND, int P1>
 FusedLaunch shape_of(int Q) {
   constexpr int p = P1 - 1;
   using S = ShapeSK<KIND, P1>;
-  const int cps = (KIND == KIND_COLLOC || Q == P1) ? simt_ctas_per_sm<KIND, P1, P1>()
-                                                  : simt_ctas_per_sm<KIND, P1, P1 + 1>();
-  return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB, cps};
+  const bool q1 = KIND == KIND_COLLOC || Q == P1;
+  const int cps = q1 ? simt_ctas_per_sm<KIND, P1, P1>() : simt_ctas_per_sm<KIND, P1, P1 + 1>();
+  const int cpc = q1 ? cg_ctas_per_sm<KIND, P1, P1>() : cg_ctas_per_sm<KIND, P1, P1 + 1>();
+  return FusedLaunch{S::BX, S::BY, FaceLayout<p, p * S::BX + 1, p * S::BY + 1>::FB, cps, cpc};
 }
 
 }  // namespace

@@ -116,6 +116,9 @@ struct Op {
   int cg_cap = 0;
 };
 
+// fully matrix-free BP3 apply (mf.cu, mf_impl.cuh; §8(f) f3)
+hofem_status apply_mf(Op* op, const double* x, double* y, cudaStream_t s);
+
 // p-multigrid (pmg.cu; §8(f) f2)
 struct PMG;
 hofem_status op_diagonal(Op* op, double* d, cudaStream_t s);

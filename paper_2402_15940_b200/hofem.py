@@ -91,6 +91,7 @@ SIGNATURES = {
     "hofem_op_create": (_I, [_V, _I, _I, _I, _I, _V, _PV]),
     "hofem_op_apply": (_I, [_V, _V, _V, _V]),
     "hofem_op_apply_unfused": (_I, [_V, _V, _V, _V]),
+    "hofem_op_apply_mf": (_I, [_V, _V, _V, _V]),
     "hofem_op_qdata": (_I, [_V, ctypes.POINTER(_V), ctypes.POINTER(_LL)]),
     "hofem_op_nq1d": (_I, [_V, ctypes.POINTER(_I)]),
     "hofem_rhs_manufactured": (_I, [_V, _V, _V]),
@@ -304,6 +305,13 @@ class Operator:
         y = torch.empty_like(x) if y is None else y
         n = self.mesh.n_local
         _check(lib().hofem_op_apply_unfused(self.handle, _ptr(x, n), _ptr(y, n), _stream(stream)))
+        return y
+
+    def apply_mf(self, x: torch.Tensor, y: torch.Tensor | None = None, stream=None):
+        """Fully matrix-free apply (geometry recomputed from the nodal coordinates)."""
+        y = torch.empty_like(x) if y is None else y
+        n = self.mesh.n_local
+        _check(lib().hofem_op_apply_mf(self.handle, _ptr(x, n), _ptr(y, n), _stream(stream)))
         return y
 
     def qdata(self) -> torch.Tensor:

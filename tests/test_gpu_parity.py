@@ -316,10 +316,16 @@ def test_cg_iterates_small(hf, bench, p, n, mode):
     kmax = min(kwin, 200)
     _, _, _, _, xh = O.cg(bo, m=om, Ae=Ae, bc=bc, max_iter=kmax, fixed_iters=True,
                           history=True)
+    # the oracle's own rounding sensitivity: the same CG on b perturbed at the
+    # 1e-15 level (two correct runs differ by about this much; reading R14)
+    pert = 1.0 + 1e-15 * W.random_vector(99, np.arange(len(bo)))
+    _, _, _, _, xp = O.cg(bo * pert, m=om, Ae=Ae, bc=bc, max_iter=kmax, fixed_iters=True,
+                          history=True)
     for k in sorted({1, 2, 5, kmax // 2, kmax}):
         x = torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
         op.cg(b, x, max_iter=k, fixed_iters=True)
-        assert rel(host(x), xh[k]) <= 1e-10, (k, rel(host(x), xh[k]))
+        tol = max(1e-10, 100.0 * rel(xp[k], xh[k]))
+        assert rel(host(x), xh[k]) <= tol, (k, rel(host(x), xh[k]), tol)
     # converged solutions (both to rel-res 1e-13) agree to 1e-11
     x = torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
     st, stats, _ = op.cg(b, x, rel_tol=1e-13, max_iter=800)
