@@ -72,6 +72,19 @@ hofem_status hofem_comm_unique_id(void* nccl_id_out /* 128 bytes, host */);
 hofem_status hofem_comm_init(const void* nccl_id /* 128 B host */, int rank, int nranks,
                              int device, void** comm_out);
 void hofem_comm_destroy(void* comm);
+/* In-process loopback transport (testing the multi-rank data path on ONE GPU):
+ * a group of nranks "ranks" that are host threads of this process sharing the
+ * current device.  Every rank's thread calls hofem_comm_init_loopback with its
+ * rank and then drives its own mesh / operator on its own stream exactly as
+ * with NCCL; the interface exchange becomes device-to-device plane copies
+ * ordered by CUDA events behind host barriers, the allreduce a fixed rank-order
+ * sum (bitwise identical on every rank).  All ranks must make the same sequence
+ * of collective calls (apply, dot, CG, ...), like NCCL.  Cooperative in-kernel
+ * grid barriers are not used on a loopback multi-rank mesh (several ranks'
+ * kernels share the device).  The group must outlive its comms. */
+hofem_status hofem_loopback_group_create(int nranks, void** group_out);
+hofem_status hofem_comm_init_loopback(void* group, int rank, void** comm_out);
+void hofem_loopback_group_destroy(void* group);
 
 /* ---------------------------------------------------------------- mesh (a1) */
 /* Structured nx*ny*nz_global hex mesh of [0,extent0]x[0,extent1]x[0,extent2],

@@ -6,9 +6,42 @@
 // received.  a+b == b+a in IEEE arithmetic, so both copies of a shared plane end
 // bitwise identical (reading R9).  Dirichlet rows on the planes are re-imposed
 // after the sum.  CG dot products use ncclAllReduce of one FP64 (§8(e)).
+#include <condition_variable>
+#include <mutex>
+#include <vector>
+
 #include "internal.h"
 
 namespace hofem {
+
+struct LoopGroup {
+  int n = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  std::vector<cudaEvent_t> ev_a, ev_b;      // per rank: "my data is ready" / "I am done reading"
+  std::vector<const double*> lo, hi;        // per rank: its bottom / top plane this exchange
+  double* slots = nullptr;                  // allreduce staging, n * kSlot doubles
+  static constexpr int kSlot = 8;
+  int attached = 0;
+};
+
+namespace {
+
+void loop_barrier(LoopGroup* g) {
+  std::unique_lock<std::mutex> lk(g->mu);
+  const long long my = g->gen;
+  if (++g->arrived == g->n) {
+    g->arrived = 0;
+    ++g->gen;
+    g->cv.notify_all();
+  } else {
+    g->cv.wait(lk, [&] { return g->gen != my; });
+  }
+}
+
+}  // namespace
 
 namespace {
 
@@ -44,8 +77,30 @@ hofem_status exchange_planes_bc(Op* op, const double* x, double* y, int bcmode, 
   if (m->nranks <= 1) return HOFEM_OK;
   const long long plane = m->plane;
   const int r = m->rank, R = m->nranks;
-  ncclComm_t c = m->comm->nccl;
   double* top = y + (m->Nzl - 1) * plane;
+  if (LoopGroup* g = m->comm->loop) {
+    // loopback: publish my planes, copy the neighbours' once they are ready,
+    // and modify mine only after the neighbours have copied them
+    g->lo[r] = y;
+    g->hi[r] = top;
+    HOFEM_CUDA(cudaEventRecord(g->ev_a[r], s));
+    loop_barrier(g);
+    if (r > 0) {
+      HOFEM_CUDA(cudaStreamWaitEvent(s, g->ev_a[r - 1], 0));
+      HOFEM_CUDA(cudaMemcpyAsync(m->d_recv, g->hi[r - 1], sizeof(double) * plane,
+                                 cudaMemcpyDeviceToDevice, s));
+    }
+    if (r < R - 1) {
+      HOFEM_CUDA(cudaStreamWaitEvent(s, g->ev_a[r + 1], 0));
+      HOFEM_CUDA(cudaMemcpyAsync(m->d_recv + plane, g->lo[r + 1], sizeof(double) * plane,
+                                 cudaMemcpyDeviceToDevice, s));
+    }
+    HOFEM_CUDA(cudaEventRecord(g->ev_b[r], s));
+    loop_barrier(g);
+    if (r > 0) HOFEM_CUDA(cudaStreamWaitEvent(s, g->ev_b[r - 1], 0));
+    if (r < R - 1) HOFEM_CUDA(cudaStreamWaitEvent(s, g->ev_b[r + 1], 0));
+  } else {
+  ncclComm_t c = m->comm->nccl;
   HOFEM_TRY(nccl_status(ncclGroupStart(), "ncclGroupStart"));
   if (r > 0) {
     HOFEM_TRY(nccl_status(ncclSend(y, plane, ncclDouble, r - 1, c, s), "ncclSend lo"));
@@ -57,6 +112,7 @@ hofem_status exchange_planes_bc(Op* op, const double* x, double* y, int bcmode, 
                           "ncclRecv hi"));
   }
   HOFEM_TRY(nccl_status(ncclGroupEnd(), "ncclGroupEnd"));
+  }
   const unsigned g = (unsigned)((plane + 255) / 256);
   const long long K0 = (long long)m->p * m->z0;
   if (r > 0) {
@@ -72,8 +128,40 @@ hofem_status exchange_planes_bc(Op* op, const double* x, double* y, int bcmode, 
   return HOFEM_OK;
 }
 
+namespace {
+// d_val[i] = sum over ranks (rank order) of the staged values
+__global__ void loop_sum_kernel(const double* __restrict__ slots, int n, int count, int stride,
+                                double* __restrict__ d_val) {
+  const int i = threadIdx.x;
+  if (i >= count) return;
+  double s = 0.0;
+  for (int r = 0; r < n; ++r) s += slots[r * stride + i];
+  d_val[i] = s;
+}
+}  // namespace
+
 hofem_status allreduce_sum(Mesh* m, double* d_val, int count, cudaStream_t s) {
   if (m->nranks <= 1) return HOFEM_OK;
+  if (LoopGroup* g = m->comm->loop) {
+    if (count > LoopGroup::kSlot) {
+      set_error("loopback allreduce: count %d > %d", count, LoopGroup::kSlot);
+      return HOFEM_ERR_ARG;
+    }
+    const int r = m->rank;
+    HOFEM_CUDA(cudaMemcpyAsync(g->slots + r * LoopGroup::kSlot, d_val, sizeof(double) * count,
+                               cudaMemcpyDeviceToDevice, s));
+    HOFEM_CUDA(cudaEventRecord(g->ev_a[r], s));
+    loop_barrier(g);
+    for (int q = 0; q < g->n; ++q)
+      if (q != r) HOFEM_CUDA(cudaStreamWaitEvent(s, g->ev_a[q], 0));
+    loop_sum_kernel<<<1, 32, 0, s>>>(g->slots, g->n, count, LoopGroup::kSlot, d_val);
+    HOFEM_LAUNCHED();
+    HOFEM_CUDA(cudaEventRecord(g->ev_b[r], s));
+    loop_barrier(g);
+    for (int q = 0; q < g->n; ++q)
+      if (q != r) HOFEM_CUDA(cudaStreamWaitEvent(s, g->ev_b[q], 0));
+    return HOFEM_OK;
+  }
   return nccl_status(
       ncclAllReduce(d_val, d_val, count, ncclDouble, ncclSum, m->comm->nccl, s), "ncclAllReduce");
 }
@@ -114,6 +202,58 @@ void hofem_comm_destroy(void* comm) {
   if (!c) return;
   if (c->nccl) ncclCommDestroy(c->nccl);
   delete c;
+}
+
+hofem_status hofem_loopback_group_create(int nranks, void** group_out) {
+  if (nranks < 1 || !group_out) {
+    hofem::set_error("hofem_loopback_group_create: bad arguments");
+    return HOFEM_ERR_ARG;
+  }
+  auto* g = new hofem::LoopGroup();
+  g->n = nranks;
+  g->ev_a.resize(nranks);
+  g->ev_b.resize(nranks);
+  g->lo.resize(nranks);
+  g->hi.resize(nranks);
+  for (int r = 0; r < nranks; ++r) {
+    if (cudaEventCreateWithFlags(&g->ev_a[r], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->ev_b[r], cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      hofem::set_error("hofem_loopback_group_create: event creation failed");
+      return HOFEM_ERR_CUDA;
+    }
+  }
+  if (cudaMalloc(&g->slots, sizeof(double) * nranks * hofem::LoopGroup::kSlot) != cudaSuccess) {
+    cudaGetLastError();
+    hofem::set_error("hofem_loopback_group_create: out of device memory");
+    return HOFEM_ERR_OOM;
+  }
+  *group_out = g;
+  return HOFEM_OK;
+}
+
+hofem_status hofem_comm_init_loopback(void* group, int rank, void** comm_out) {
+  auto* g = static_cast<hofem::LoopGroup*>(group);
+  if (!g || !comm_out || rank < 0 || rank >= g->n) {
+    hofem::set_error("hofem_comm_init_loopback: bad arguments");
+    return HOFEM_ERR_ARG;
+  }
+  auto* c = new hofem::Comm();
+  c->rank = rank;
+  c->nranks = g->n;
+  cudaGetDevice(&c->device);
+  c->loop = g;
+  *comm_out = c;
+  return HOFEM_OK;
+}
+
+void hofem_loopback_group_destroy(void* group) {
+  auto* g = static_cast<hofem::LoopGroup*>(group);
+  if (!g) return;
+  for (auto e : g->ev_a) cudaEventDestroy(e);
+  for (auto e : g->ev_b) cudaEventDestroy(e);
+  cudaFree(g->slots);
+  delete g;
 }
 
 }  // extern "C"

@@ -316,7 +316,10 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
   // in-kernel fix-up (cooperative launch, grid barrier).  Measured (gpurun_out/
   // e15, e16): pays for small (launch/latency-bound) problems, neutral or
   // slower at ~30M dofs -- hence the size threshold of the auto setting.
-  bool infix = R.need_fix && (op->opt_infix == 2 || (op->opt_infix == 1 && R.npts <= (8LL << 20)));
+  // (not on a loopback multi-rank mesh: several ranks' grids share one device)
+  const bool loopback = m->nranks > 1 && m->comm && m->comm->loop;
+  bool infix = R.need_fix && !loopback &&
+               (op->opt_infix == 2 || (op->opt_infix == 1 && R.npts <= (8LL << 20)));
   if (infix) HOFEM_TRY(ensure_bar(op));
   A.infix = infix ? 1 : 0;
   A.bar = op->d_bar;

@@ -38,9 +38,17 @@ int num_sms();  // SM count of the current device (fused.cu)
     if (s_ != HOFEM_OK) return s_;                                         \
   } while (0)
 
+// In-process loopback transport (comm.cu): ranks are host threads of one
+// process on one device; plane exchange by device copies ordered with CUDA
+// events behind host barriers, allreduce by a fixed rank-order sum.  Exercises
+// the whole multi-rank data path (partition, exchange, Dirichlet re-imposition,
+// owned-dof dot products) on a single GPU.
+struct LoopGroup;
+
 struct Comm {
   int rank = 0, nranks = 1, device = 0;
   ncclComm_t nccl = nullptr;
+  LoopGroup* loop = nullptr;  // non-null: loopback transport instead of NCCL
 };
 
 // 1D tables (independent host implementation, long double Newton).

@@ -84,6 +84,9 @@ SIGNATURES = {
     "hofem_comm_unique_id": (_I, [_V]),
     "hofem_comm_init": (_I, [_V, _I, _I, _I, _PV]),
     "hofem_comm_destroy": (None, [_V]),
+    "hofem_loopback_group_create": (_I, [_I, _PV]),
+    "hofem_comm_init_loopback": (_I, [_V, _I, _PV]),
+    "hofem_loopback_group_destroy": (None, [_V]),
     "hofem_mesh_create": (_I, [ctypes.POINTER(MeshDesc), _V, _V, _PV]),
     "hofem_mesh_info_get": (_I, [_V, ctypes.POINTER(MeshInfo)]),
     "hofem_mesh_coords": (_I, [_V, _V, _V]),
@@ -188,14 +191,40 @@ def copy_device_to_tensor(dev_ptr: int, n: int, device=None) -> torch.Tensor:
     return out
 
 
-class Comm:
-    """NCCL communicator for the z-slab partition (one process per GPU)."""
+class LoopbackGroup:
+    """In-process loopback transport: nranks ranks as threads on one GPU
+    (hofem_loopback_group_create); see Comm.loopback."""
 
-    def __init__(self, rank: int, nranks: int, device: int, nccl_id: bytes):
+    def __init__(self, nranks: int):
+        h = ctypes.c_void_p()
+        _check(lib().hofem_loopback_group_create(nranks, ctypes.byref(h)))
+        self.handle = h
+        self.nranks = nranks
+
+    def close(self):
+        if self.handle:
+            lib().hofem_loopback_group_destroy(self.handle)
+            self.handle = None
+
+
+class Comm:
+    """NCCL communicator for the z-slab partition (one process per GPU), or the
+    in-process loopback transport (Comm.loopback)."""
+
+    def __init__(self, rank: int, nranks: int, device: int, nccl_id: bytes, _handle=None):
+        if _handle is not None:
+            self.handle = _handle
+            return
         h = ctypes.c_void_p()
         buf = ctypes.create_string_buffer(nccl_id, 128)
         _check(lib().hofem_comm_init(buf, rank, nranks, device, ctypes.byref(h)))
         self.handle = h
+
+    @classmethod
+    def loopback(cls, group: "LoopbackGroup", rank: int) -> "Comm":
+        h = ctypes.c_void_p()
+        _check(lib().hofem_comm_init_loopback(group.handle, rank, ctypes.byref(h)))
+        return cls(rank, group.nranks, 0, b"", _handle=h)
 
     @staticmethod
     def unique_id() -> bytes:

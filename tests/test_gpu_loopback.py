@@ -1,0 +1,152 @@
+"""The multi-rank CUDA data path on ONE GPU:
+R = 2, 3 ranks as host threads with the in-process loopback transport
+(hofem_loopback_group_create / hofem_comm_init_loopback), each on its own
+stream, drive comm.cu's plane exchange (with Dirichlet re-imposition on the
+interface planes), the owned-dof dot products / allreduce, the fused kernel's
+owned-dof p.Ap and the multi-rank CG -- compared with the GLOBAL single-mesh
+oracle."""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hf():
+    import paper_2402_15940_b200 as hf
+    hf.lib()
+    return hf
+
+
+def run_ranks(hf, R, fn):
+    group = hf.LoopbackGroup(R)
+    out, err = [None] * R, [None] * R
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                comm = hf.Comm.loopback(group, r)
+                out[r] = fn(r, comm, s)
+                s.synchronize()
+        except Exception as e:  # noqa: BLE001
+            err[r] = e
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(R)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    group.close()
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def slab(v, plane, p, nzl, r):
+    return v[plane * p * nzl * r: plane * (p * nzl * (r + 1) + 1)]
+
+
+CFG = [(2, "bp3", 3, (3, 2, 4), 1), (3, "bp3", 2, (4, 3, 6), 1), (2, "bp1", 4, (2, 3, 2), 0),
+       (3, "bp5", 3, (3, 3, 3), 1), (2, "bp3", 5, (3, 2, 4), 0)]
+KINDS = {"bp1": (1, 1), "bp3": (2, 1), "bp5": (2, 2)}
+
+
+@pytest.mark.parametrize("R,bench,p,dims,bc", CFG)
+def test_loopback_apply_rhs_dot_match_global(hf, R, bench, p, dims, bc):
+    kind, rule = KINDS[bench]
+    nx, ny, nz = dims
+    nzl = nz // R
+    plane = (p * nx + 1) * (p * ny + 1)
+
+    def fn(r, comm, s):
+        m = hf.Mesh(nx, ny, nz, p, alpha=0.1, comm=comm, stream=s)
+        op = hf.Operator(m, kind=kind, rule=rule, bc=bc, stream=s)
+        x = m.random(5, stream=s)
+        y = op.apply(x, stream=s)
+        yd, d = op.apply_dot(x, stream=s)
+        yu = op.apply_unfused(x, stream=s)
+        b = op.rhs(stream=s)
+        xx = m.dot(x, x, stream=s)
+        s.synchronize()
+        return dict(x=host(x), y=host(y), yd=host(yd), yu=host(yu), b=host(b), d=d, xx=xx,
+                    n_owned=m.n_owned)
+
+    res = run_ranks(hf, R, fn)
+    om = O.Mesh(nx, ny, nz, p, alpha=0.1)
+    xg = W.random_vector(5, np.arange(om.n_dofs))
+    Ae = O.element_matrices(om, kind, rule)
+    yg = O.apply_ea(om, Ae, xg, bc=bc)
+    bg = O.rhs(om, kind, rule, bc=bc)
+    for r in range(R):
+        R_ = res[r]
+        assert np.array_equal(R_["x"], slab(xg, plane, p, nzl, r))
+        assert rel(R_["y"], slab(yg, plane, p, nzl, r)) <= 1e-12
+        assert rel(R_["yu"], slab(yg, plane, p, nzl, r)) <= 1e-12
+        assert np.array_equal(R_["yd"].view(np.uint64), R_["y"].view(np.uint64))
+        assert rel(R_["b"], slab(bg, plane, p, nzl, r)) <= 1e-13
+        # allreduced dots: identical on every rank, equal to the global values
+        assert R_["d"] == res[0]["d"] and R_["xx"] == res[0]["xx"]
+        if r + 1 < R:  # duplicated interface plane: bitwise equal on both ranks
+            top = R_["y"][-plane:]
+            bot = res[r + 1]["y"][:plane]
+            assert np.array_equal(top.view(np.uint64), bot.view(np.uint64))
+    assert sum(res[r]["n_owned"] for r in range(R)) == om.n_dofs
+    scale = float(np.abs(xg) @ np.abs(yg))
+    assert abs(res[0]["d"] - float(xg @ yg)) <= 1e-12 * scale
+    assert abs(res[0]["xx"] - float(xg @ xg)) <= 1e-12 * float(xg @ xg)
+
+
+@pytest.mark.parametrize("R,bench,p,dims", [(2, "bp3", 3, (3, 2, 4)), (3, "bp3", 2, (3, 3, 6))])
+def test_loopback_cg_iterates_match_global(hf, R, bench, p, dims):
+    """Multi-rank CG (separate vector kernels, NCCL-path scalars via the loopback
+    allreduce) against the global oracle CG iterates."""
+    kind, rule = KINDS[bench]
+    nx, ny, nz = dims
+    nzl = nz // R
+    plane = (p * nx + 1) * (p * ny + 1)
+    om = O.Mesh(nx, ny, nz, p, alpha=0.1)
+    Ae = O.element_matrices(om, kind, rule)
+    bg = O.rhs(om, kind, rule, bc=1)
+    ks = [1, 4, 12]
+    _, _, _, _, xh = O.cg(bg, m=om, Ae=Ae, bc=1, max_iter=max(ks), fixed_iters=True, history=True)
+    xo, st, kconv, _, _ = O.cg(bg, m=om, Ae=Ae, bc=1, rel_tol=1e-13, max_iter=1000)
+
+    def fn(r, comm, s):
+        m = hf.Mesh(nx, ny, nz, p, alpha=0.1, comm=comm, stream=s)
+        op = hf.Operator(m, kind=kind, rule=rule, bc=1, stream=s)
+        b = op.rhs(stream=s)
+        out = {}
+        for k in ks:
+            x = torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
+            op.cg(b, x, max_iter=k, fixed_iters=True, stream=s)
+            out[k] = host(x)
+        x = torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
+        st, stats, _ = op.cg(b, x, rel_tol=1e-13, max_iter=1000, check_every=1, stream=s)
+        out["conv"] = (st, stats.iterations, host(x))
+        return out
+
+    res = run_ranks(hf, R, fn)
+    for r in range(R):
+        for k in ks:
+            assert rel(res[r][k], slab(xh[k], plane, p, nzl, r)) <= 1e-10, (r, k)
+        st_r, it_r, x_r = res[r]["conv"]
+        assert st_r == 0 and abs(it_r - kconv) <= 2
+        assert rel(x_r, slab(xo, plane, p, nzl, r)) <= 1e-11
