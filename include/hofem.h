@@ -327,7 +327,7 @@ hofem_status hofem_op_fused_info(const void* op, hofem_fused_info* out);
  *  CG_PERSISTENT  hofem_cg runs the whole solve in ONE cooperative kernel (brick
  *                 pass, fix-up, p.Ap, updates, r.r, stop test, all behind grid
  *                 barriers; §2.3); single rank only; auto =
- *                 <= 8 Mi dofs.  Convergence is then tested every iteration.
+ *                 <= 256 Ki dofs (measured crossover).  Convergence is then tested every iteration.
  *  L2_PREFETCH    bulk-prefetch the next brick's qdata into L2. */
 typedef enum {
   HOFEM_OPT_INFIX = 1,

@@ -333,11 +333,13 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
 
   const unsigned vgrid = kDotBlocks;
   // Whole solve in one persistent cooperative kernel (§8(f) f1): single rank,
-  // fused operator; auto = local problems up to 8 Mi dofs (the launch- and
-  // latency-bound regime), 2 = always.  Convergence is tested every iteration
-  // on the device (check_every does not apply).
+  // fused operator; 2 = always; auto = local problems up to 256 Ki dofs, where
+  // it measured fastest (gpurun_out/r2e, profiles/ab/r2_cg_modes.txt: BP3 p=5
+  // 8^3 elements 31.4 vs 32.8 us/it); from ~0.5M dofs on, the per-iteration
+  // kernels (fused cooperative update) win.  Convergence is tested every
+  // iteration on the device (check_every does not apply).
   const bool persist = m->nranks == 1 && fused_supported(op) &&
-                       (op->opt_cg_persist == 2 || (op->opt_cg_persist == 1 && n <= (8LL << 20)));
+                       (op->opt_cg_persist == 2 || (op->opt_cg_persist == 1 && n <= (256LL << 10)));
   if (persist && !(rr0 == 0.0 && !fixed_iters)) {
     int* dres = reinterpret_cast<int*>(flag + 1);
     HOFEM_CUDA(cudaMemsetAsync(dres, 0, 2 * sizeof(int), s));

@@ -1948,10 +1948,10 @@ struct FusedLaunch {
   int ctas_per_sm_cg;                   // the persistent CG kernel (own register cap)
 };
 
-// Register cap of the persistent CG kernel: the brick pass inside an iteration
-// loop carries more live state than the apply kernel; 32 more registers (fewer
-// resident CTAs) instead of spilling inside the contraction stages.
-constexpr int cg_maxr(int maxr) { return maxr + 32 > 255 ? 255 : maxr + 32; }
+// Register cap of the persistent CG kernel.  Measured (gpurun_out/r2e vs r2c):
+// 32 more registers than the apply kernel remove most spills but cost resident
+// CTAs and are slower overall; the apply kernel's cap is kept.
+constexpr int cg_maxr(int maxr) { return maxr; }
 
 // Defined per P1 in fused_p.cu: kind in {KIND_MASS, KIND_DIFF, KIND_COLLOC},
 // Q in {P1, P1+1} for MASS/DIFF and Q == P1 for COLLOC.  Return false if the
