@@ -3,13 +3,19 @@
 vs p; CG [DOFs x iters]/s at 1/2/4/8 B200").
 
 One *step* = one CG iteration of the BP3 diffusion operator (SURVEY.md §8(a)
-rows a4-a10: fused apply + dot + fused updates), p = 5, Gauss Q = p+2,
-curvilinear unit cube, homogeneous Dirichlet, manufactured RHS; 62^3 elements
-= 30,080,231 dofs per GPU (configs[2] size; weak scaling stacks one 62^3 slab
-per GPU in z, exchanged over NCCL).  ``value`` = global DOFs x iterations / s
-over all GPUs (G[DOF*it]/s), device-timed with CUDA events, max over ranks.
+rows a4-a10: fused apply + p.Ap + fused updates), p = 5, Gauss Q = p+2,
+curvilinear unit cube, homogeneous Dirichlet, manufactured RHS, on BASELINE
+config 5's slab of 200 x 200 x 25 elements per GPU (125.5M dofs per GPU; weak
+scaling stacks one slab per GPU in z, exchanged over NCCL).  ``value`` = global
+DOFs x iterations / s over all GPUs (G[DOF*it]/s), device-timed with CUDA
+events, max over ranks.  The line also carries the dominant kernel's roofline,
+e2e (host buffers through the public API), the CPU oracle baseline and -- on
+rank 0 at N = 1, time-bounded -- ``sweep``: apply GDOF/s and HBM-roofline
+fraction vs p for configs 2-4 (BP3 fused / unfused / fully matrix-free, BP5,
+BP1 eager / CUDA-graph / L2-flushed + 100-iteration CG), the DG mass operator,
+the DOFs needed to reach 80 % of peak, and BPS3 p-multigrid PCG vs CG.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--p 5] [--sweep]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--p 5] [--no-sweep] [--bp5-cg]
     python bench.py --impl reference ...   # the CPU oracle (rank 0 only)
 
 Prints ONE JSON line on rank 0.
@@ -130,15 +136,27 @@ def oracle_cg_sample(p, n, iters, warmup=0):
     return om.n_dofs * iters / (t3 - t2), t1 - t0, t3 - t2, om.n_dofs, O.num_threads()
 
 
-def arm_config(p, n, world):
-    """The workload both arms report (BASELINE configs[2] size, one n^3 slab per GPU)."""
+def slab_dims(args):
+    """Per-GPU slab (elements): BASELINE config 5: 200 x 200 x 25
+    per GPU, stacked in z for weak scaling; --n gives an n^3 slab instead."""
+    if args.n:
+        return args.n, args.n, args.n
+    return tuple(int(v) for v in args.slab.split(","))
+
+
+def arm_config(p, dims, world):
+    """The workload both arms report."""
+    nx, ny, nzs = dims
     Q = p + 2
-    n_global = (p * n + 1) ** 2 * (p * n * world + 1)
-    return {"workload": f"bp3_p{p}_{n}x{n}x{n}_per_gpu", "p": p, "q": Q,
-            "elements_per_gpu": n ** 3, "dofs_global": n_global,
-            "dofs_per_gpu": (p * n + 1) ** 3, "bc": "dirichlet", "mesh": "curvilinear alpha=0.1",
+    n_global = (p * nx + 1) * (p * ny + 1) * (p * nzs * world + 1)
+    qd_gb = nx * ny * nzs * 6 * Q ** 3 * 8 / 1e9
+    vec_mb = (p * nx + 1) * (p * ny + 1) * (p * nzs + 1) * 8 / 1e6
+    return {"workload": f"bp3_p{p}_{nx}x{ny}x{nzs}_per_gpu (BASELINE config 5, weak scaling)",
+            "p": p, "q": Q, "elements_per_gpu": nx * ny * nzs, "dofs_global": n_global,
+            "dofs_per_gpu_local": (p * nx + 1) * (p * ny + 1) * (p * nzs + 1), "bc": "dirichlet",
+            "mesh": "curvilinear alpha=0.1",
             "parallelism": f"z-slab x{world} (NCCL plane exchange + allreduce)",
-            "l2": "inputs larger than L2 (qdata 3.9 GB/GPU, vectors 240 MB)"}
+            "l2": f"inputs larger than L2 (qdata {qd_gb:.1f} GB/GPU, vectors {vec_mb:.0f} MB), no flush"}
 
 
 def run_reference(args):
@@ -156,7 +174,7 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         # the arm's workload; each step is the bounded oracle sample named in cpu_baseline
-        "config": arm_config(p, args.n or int(round(311.0 / p)), args.gpus),
+        "config": arm_config(p, slab_dims(args), args.gpus),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -183,9 +201,8 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     p = args.p
-    n = args.n or int(round(311.0 / p))
-    nx = ny = n
-    nz = n * world
+    nx, ny, nzs = slab_dims(args)
+    nz = nzs * world
     Q = p + 2
     mesh = hf.Mesh(nx, ny, nz, p, alpha=0.1, comm=comm)
     op = hf.Operator(mesh, kind=hf.DIFFUSION, rule=hf.GAUSS, bc=hf.BC_DIRICHLET)
@@ -246,8 +263,7 @@ def run_ours(args):
     hf.profile_enable(False)
     t_brick = prof.brick_ms / 1e3 / max(prof.brick_launches, 1)
     t_fix = prof.fixup_ms / 1e3 / max(prof.fixup_launches, 1)
-    nzl = n
-    bytes_apply, N_l, E_l = alg_bytes(nx, ny, nzl, p, Q, 6)
+    bytes_apply, N_l, E_l = alg_bytes(nx, ny, nzs, p, Q, 6)
     info = op.fused_info()
     nd = info.direct_points
     bytes_brick = 8 * N_l + 8 * 6 * E_l * Q ** 3 + 8 * nd
@@ -257,7 +273,7 @@ def run_ours(args):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            ent = json.load(open(tpath)).get(f"bp3_p{p}_n{n}")
+            ent = json.load(open(tpath)).get(f"bp3_p{p}_{nx}x{ny}x{nzs}")
             traffic = ent["dram_bytes"] if ent else None
         except Exception:
             traffic = None
@@ -287,8 +303,14 @@ def run_ours(args):
                "step": f"one hofem_cg solve of {it} fixed iterations incl. H2D of b and D2H of x "
                        f"(per rank); {reps} solves timed"}
 
-    # ---- optional sweep (apply GDOF/s per GPU vs p, fused vs unfused, BP1/BP5)
-    sweep = run_sweep(args, hf, torch, stream) if args.sweep else None
+    # ---- sweep (rank 0, N = 1; time-bounded): configs 2-4 and the §8(f) rows
+    sweep = None
+    if rank == 0 and world == 1 and not args.no_sweep:
+        op.close()
+        mesh.close()
+        del b, x
+        torch.cuda.empty_cache()
+        sweep = run_sweep(args, hf, torch, stream)
 
     # ---- CPU baseline: rank 0, N = 1 only
     cpu = None
@@ -306,7 +328,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_cg / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": arm_config(p, n, world),
+            "config": arm_config(p, (nx, ny, nzs), world),
             "apply_gdof_s_per_gpu": N_l / t_apply / 1e9,
             "apply_ms": 1e3 * t_apply,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -330,85 +352,206 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _evt_time(torch, stream, fn, reps, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3 / reps
+
+
+def _graph_time(torch, fn, reps=200, launches=5):
+    """`reps` applies captured in ONE CUDA graph, median
+    of `launches` graph launches (per apply)."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            fn()
+    ts = []
+    for _ in range(launches):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3 / reps)
+    del g
+    return statistics.median(ts)
+
+
 def run_sweep(args, hf, torch, stream):
-    """Apply throughput per GPU vs p (configs 2-4 of BASELINE.json)."""
+    """Configs 2-4 of BASELINE.json and the §8(f) rows, time-bounded: apply
+    throughput per GPU vs p with its HBM-roofline fraction (algorithmic bytes,
+    SURVEY.md §8(d)), fused / unfused / fully matrix-free BP3, BP5, BP1 (eager,
+    CUDA-graph, L2-flushed; 100-iteration CG), DG mass; the DOFs needed to reach
+    80 % of peak; BPS3 p-multigrid PCG vs CG."""
+    import workloads as W
     peak, _ = load_peaks()
-    out = []
-    reps = 20
+    out = {"bp3": [], "bp5": [], "bp1": [], "dg": []}
+    reps = args.sweep_reps
+
+    def rec(name, t, nbytes, ndofs, flops=None):
+        d = {"ms": 1e3 * t, "gdof_s": ndofs / t / 1e9, "alg_gbs": nbytes / t / 1e9,
+             "frac": nbytes / t / 1e9 / peak}
+        if flops:
+            d["fp64_tflops"] = flops / t / 1e12
+        return d
+
     for bench, kind, rule, ps in (("bp3", hf.DIFFUSION, hf.GAUSS, range(1, 9)),
                                   ("bp5", hf.DIFFUSION, hf.GLL, range(4, 9)),
                                   ("bp1", hf.MASS, hf.GAUSS, range(1, 9))):
         for p in ps:
-            n = int(round((99.0 if bench == "bp1" else 311.0) / p))
+            n = W.bp1_sweep_n(p) if bench == "bp1" else W.bp3_sweep_n(p)
             Q = p + 2 if rule == hf.GAUSS else p + 1
             nc = 1 if kind == hf.MASS else 6
             m = hf.Mesh(n, n, n, p, alpha=0.1)
             op = hf.Operator(m, kind=kind, rule=rule)
             x = m.random(3)
             y = torch.empty_like(x)
-            res = {"bench": bench, "p": p, "n": n, "dofs": m.n_local}
-            for name, fn in (("fused", op.apply), ("unfused", op.apply_unfused)):
-                if name == "unfused" and bench == "bp1":
-                    continue
-                for _ in range(3):
-                    fn(x, y)
-                torch.cuda.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                for _ in range(reps):
-                    fn(x, y)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                t = e0.elapsed_time(e1) / 1e3 / reps
-                bts, N, E = alg_bytes(n, n, n, p, Q, nc)
-                res[name] = {"gdof_s": N / t / 1e9, "ms": 1e3 * t,
-                             "alg_gbs": bts / t / 1e9, "frac": bts / t / 1e9 / peak}
-            if bench == "bp1" and getattr(args, "bp5_cg", False):
-                # config 2: 100 fixed CG iterations on the ~1M-dof mass operator (SPEC.md:644)
+            bts, N, E = alg_bytes(n, n, n, p, Q, nc)
+            res = {"p": p, "n": n, "dofs": N}
+            res["fused"] = rec("fused", _evt_time(torch, stream, lambda: op.apply(x, y), reps),
+                               bts, N)
+            if bench == "bp3":
+                res["unfused"] = rec("unfused", _evt_time(torch, stream,
+                                                          lambda: op.apply_unfused(x, y),
+                                                          max(3, reps // 4)), bts, N)
+                # f3: algorithmic bytes 8 (x) + 24 (X, Y, Z) + 8 (y) B/DOF + the
+                # E-vector round trip 16 B per element dof
+                bmf = 40 * N + 16 * E * (p + 1) ** 3
+                res["matrix_free"] = rec("mf", _evt_time(torch, stream,
+                                                         lambda: op.apply_mf(x, y),
+                                                         max(3, reps // 4)), bmf, N)
+            if bench == "bp1":
+                res["graph"] = rec("graph", _graph_time(torch, lambda: op.apply(x, y),
+                                                       reps=200), bts, N)
+                # cold L2: a 2 x L2 memset between applies; its own time subtracted
+                flush = torch.empty(2 * 126 * 2 ** 20 // 8, dtype=torch.float64, device="cuda")
+                t_fl = _evt_time(torch, stream, lambda: flush.zero_(), 10)
+                t_both = _evt_time(torch, stream, lambda: (flush.zero_(), op.apply(x, y)), 10)
+                res["l2_flushed"] = rec("flushed", max(t_both - t_fl, 1e-9), bts, N)
+                del flush
                 b = op.rhs()
                 xs = torch.zeros_like(b)
-                op.cg(b, xs, max_iter=5, fixed_iters=True)
-                xs.zero_()
-                torch.cuda.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                st, stats, _ = op.cg(b, xs, max_iter=100, fixed_iters=True)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                t = e0.elapsed_time(e1) / 1e3
-                res["cg_100"] = {"iterations": stats.iterations, "s": t,
-                                 "gdof_it_s": m.n_local * stats.iterations / t / 1e9}
-            if bench == "bp5" and getattr(args, "bp5_cg", False):
-                # config 4: Dirichlet, manufactured RHS, CG to 1e-10 relative residual
-                opd = hf.Operator(m, kind=kind, rule=rule, bc=hf.BC_DIRICHLET)
-                b = opd.rhs()
-                xs = torch.zeros_like(b)
-                torch.cuda.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                st, stats, _ = opd.cg(b, xs, rel_tol=1e-10, max_iter=20000, check_every=50)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                t = e0.elapsed_time(e1) / 1e3
-                res["cg_1e-10"] = {"iterations": stats.iterations, "converged": bool(stats.converged),
-                                   "rel_res": stats.final_rel_res, "s": t,
-                                   "gdof_it_s": m.n_local * stats.iterations / t / 1e9}
-                opd.close()
+                t_cg = _evt_time(torch, stream,
+                                 lambda: op.cg(b, xs, max_iter=100, fixed_iters=True), 1, warm=1)
+                res["cg_100"] = {"ms": 1e3 * t_cg, "gdof_it_s": N * 100 / t_cg / 1e9,
+                                 "us_per_it": 1e4 * t_cg}
+            out[bench].append(res)
             op.close()
             m.close()
             torch.cuda.empty_cache()
-            out.append(res)
+    # f4: DG (L2) mass, ~30M DG dofs
+    for p in range(1, 9):
+        n = W.dg_sweep_n(p)
+        m = hf.Mesh(n, n, n, p, alpha=0.1)
+        dg = hf.DGMass(m)
+        x = dg.random(1)
+        y = torch.empty_like(x)
+        E = n ** 3
+        bts = 16 * dg.n_local + 8 * E * (p + 2) ** 3
+        r = rec("dg", _evt_time(torch, stream, lambda: dg.apply(x, y), reps), bts, dg.n_local)
+        r.update({"p": p, "n": n, "dofs": dg.n_local})
+        out["dg"].append(r)
+        dg.close()
+        m.close()
+        torch.cuda.empty_cache()
+    # f1 metric (PAPER.md:200): DOFs needed to reach 80 % of peak, BP3 p=5 CG
+    # iterations, fused schedule (in-kernel fix-up + fused update / persistent
+    # kernel, i.e. the defaults) vs the separate-kernel schedule
+    sizes = [4, 6, 8, 12, 16, 24, 32, 44, 62]
+    curves = {"fused": [], "separate": []}
+    for n in sizes:
+        m = hf.Mesh(n, n, n, 5, alpha=0.1)
+        op = hf.Operator(m, kind=hf.DIFFUSION, rule=hf.GAUSS, bc=hf.BC_DIRICHLET)
+        b = op.rhs()
+        xs = torch.zeros_like(b)
+        for name in ("fused", "separate"):
+            v = hf.AUTO if name == "fused" else hf.NEVER
+            for o in (hf.OPT_INFIX, hf.OPT_CG_FUSED_UPDATE, hf.OPT_CG_PERSISTENT):
+                op.set_option(o, v)
+            it = 50
+            t = _evt_time(torch, stream, lambda: op.cg(b, xs, max_iter=it, fixed_iters=True), 1,
+                          warm=1)
+            curves[name].append({"n": n, "dofs": m.n_local, "gdof_it_s": m.n_local * it / t / 1e9})
+        op.close()
+        m.close()
+        torch.cuda.empty_cache()
+    d80 = {}
+    for name, cv in curves.items():
+        top = max(c["gdof_it_s"] for c in cv)
+        d80[name] = next(c["dofs"] for c in cv if c["gdof_it_s"] >= 0.8 * top)
+    out["dofs_to_80pct_of_peak"] = {"bench": "bp3 p=5 CG (Dirichlet), 50 fixed iterations",
+                                    "curves": curves, "dofs_80pct": d80}
+    # f2: BPS3 -- p-multigrid preconditioned CG vs CG to 1e-10 (BP3 p=5, 24^3 elements)
+    m = hf.Mesh(24, 24, 24, 5, alpha=0.1)
+    op = hf.Operator(m, kind=hf.DIFFUSION, rule=hf.GAUSS, bc=hf.BC_DIRICHLET)
+    b = op.rhs()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    P = hf.PMG(m, degree=3)
+    t_setup = time.perf_counter() - t0
+    xs = torch.zeros_like(b)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, pst, _ = P.pcg(b, xs, rel_tol=1e-10, max_iter=500)
+    t_pcg = time.perf_counter() - t0
+    xs.zero_()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, cst, _ = op.cg(b, xs, rel_tol=1e-10, max_iter=20000, check_every=10)
+    t_cgs = time.perf_counter() - t0
+    out["bps3"] = {"mesh": "24^3 elements, p=5, curvilinear, Dirichlet", "dofs": m.n_local,
+                   "orders": P.orders, "chebyshev_degree": 3,
+                   "pmg_pcg": {"iterations": pst.iterations, "s": t_pcg, "setup_s": t_setup,
+                               "rel_res": pst.final_rel_res},
+                   "cg": {"iterations": cst.iterations, "s": t_cgs, "rel_res": cst.final_rel_res}}
+    P.close()
+    op.close()
+    m.close()
+    torch.cuda.empty_cache()
+    if getattr(args, "bp5_cg", False):
+        out["bp5_cg_1e-10"] = []
+        for p in range(4, 9):
+            n = W.bp3_sweep_n(p)
+            m = hf.Mesh(n, n, n, p, alpha=0.1)
+            opd = hf.Operator(m, kind=hf.DIFFUSION, rule=hf.GLL, bc=hf.BC_DIRICHLET)
+            b = opd.rhs()
+            xs = torch.zeros_like(b)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            st, stats, _ = opd.cg(b, xs, rel_tol=1e-10, max_iter=20000, check_every=50)
+            t = time.perf_counter() - t0
+            out["bp5_cg_1e-10"].append({"p": p, "iterations": stats.iterations, "s": t,
+                                        "gdof_it_s": m.n_local * stats.iterations / t / 1e9})
+            opd.close()
+            m.close()
+            torch.cuda.empty_cache()
     return out
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
-    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--p", type=int, default=5)
-    ap.add_argument("--n", type=int, default=0, help="elements per axis per GPU (0: round(311/p))")
+    ap.add_argument("--n", type=int, default=0, help="n^3 elements per GPU instead of --slab")
+    ap.add_argument("--slab", default="200,200,25",
+                    help="elements per GPU nx,ny,nz (BASELINE config 5: 200,200,25)")
     ap.add_argument("--apply-reps", type=int, default=50)
     ap.add_argument("--e2e-iters", type=int, default=100)
     ap.add_argument("--e2e-reps", type=int, default=2)
@@ -416,10 +559,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-n", type=int, default=10, help="oracle sample: elements per axis")
     ap.add_argument("--ref-iters", type=int, default=3000)
-    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the p / size sweeps")
+    ap.add_argument("--sweep-reps", type=int, default=20)
     ap.add_argument("--bp5-cg", action="store_true",
-                    help="with --sweep: BP5 CG solves to 1e-10 (BASELINE config 4) and "
-                         "100 fixed BP1 CG iterations (config 2)")
+                    help="sweep also runs the BP5 CG solves to 1e-10 (BASELINE config 4, ~15 s)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
