@@ -49,12 +49,16 @@ def main(tag):
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units[i], 1)
             b = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
             import re
-            m = re.match(r"(?:fused_bp3p|simt_p|mma_p)(\d+)$", name)
-            if m:
-                p = int(m.group(1))
-                n = int(round(311.0 / p))
-                traffic[f"bp3_p{p}_n{n}"] = {"dram_bytes": b, "kernel": kn[:80],
-                                             "source": f"profiles/{tag}_{name}_raw.csv"}
+            mm = re.match(r"simt_p(\d+)(?:_(\d+)x(\d+)x(\d+))?$", name)
+            if mm:
+                p = int(mm.group(1))
+                if mm.group(2):
+                    key = f"bp3_p{p}_{mm.group(2)}x{mm.group(3)}x{mm.group(4)}"
+                else:
+                    n = int(round(311.0 / p))
+                    key = f"bp3_p{p}_{n}x{n}x{n}"
+                traffic[key] = {"dram_bytes": b, "kernel": kn[:80],
+                                "source": f"profiles/{tag}_{name}_raw.csv"}
     with open(tpath, "w") as f:
         json.dump(traffic, f, indent=1)
     print("wrote", sorted(os.listdir(dst)))
