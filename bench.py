@@ -30,6 +30,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -157,6 +159,51 @@ def arm_config(p, dims, world):
             "mesh": "curvilinear alpha=0.1",
             "parallelism": f"z-slab x{world} (NCCL plane exchange + allreduce)",
             "l2": f"inputs larger than L2 (qdata {qd_gb:.1f} GB/GPU, vectors {vec_mb:.0f} MB), no flush"}
+
+
+def run_oracle_plan(args):
+    """SURVEY.md §8(d) oracle timing plan, on the host cores: EA setup (the
+    "Element Assembly" level), EA apply and 10 fixed CG
+    iterations timed separately (median of 3), with 1 thread and all cores, on
+    the per-config sample sizes; prints one JSON line (rank 0 only)."""
+    import oracle as O
+    import workloads as W
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    ncores = os.cpu_count() or 1
+    plan = [("config1_bp3_2x2x2_p2", O.DIFFUSION, O.GAUSS, 2, (2, 2, 2), 1)]
+    plan += [(f"config2_bp1_p{p}", O.MASS, O.GAUSS, p, (W.bp1_sweep_n(p),) * 3, 0)
+             for p in (1, 2, 3, 4, 5)]
+    plan += [(f"config3_bp3_p{p}_n_over_4", O.DIFFUSION, O.GAUSS, p,
+              (max(1, W.bp3_sweep_n(p) // 4),) * 3, 1) for p in (2, 5)]
+    plan += [("config4_bp5_p5_n8", O.DIFFUSION, O.GLL, 5, (8, 8, 8), 1),
+             ("config5_bp3_p5_16x16x2", O.DIFFUSION, O.GAUSS, 5, (16, 16, 2), 1)]
+    rows = []
+    for name, kind, rule, p, dims, bc in plan:
+        om = O.Mesh(*dims, p, alpha=0.1)
+        x = W.random_vector(1, np.arange(om.n_dofs))
+        b = O.rhs(om, kind, rule, bc=bc)
+        row = {"case": name, "p": p, "elements": dims, "dofs": om.n_dofs}
+        for threads in sorted({1, ncores}):
+            O.set_threads(threads)
+            ts, ta, tc = [], [], []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                Ae = O.element_matrices(om, kind, rule)
+                t1 = time.perf_counter()
+                O.apply_ea(om, Ae, x, bc=bc)
+                t2 = time.perf_counter()
+                O.cg(b, m=om, Ae=Ae, bc=bc, max_iter=10, fixed_iters=True)
+                t3 = time.perf_counter()
+                ts.append(t1 - t0); ta.append(t2 - t1); tc.append(t3 - t2)
+                del Ae
+            sa, aa, ca = (statistics.median(v) for v in (ts, ta, tc))
+            row[f"threads_{threads}"] = {"setup_s": sa, "apply_s": aa, "cg10_s": ca,
+                                         "apply_gdof_s": om.n_dofs / aa / 1e9,
+                                         "cg_gdof_it_s": om.n_dofs * 10 / ca / 1e9}
+        rows.append(row)
+    O.set_threads(ncores)
+    print(json.dumps({"oracle_plan": rows, "cpu": cpu_info(), "cores": ncores}), flush=True)
 
 
 def run_reference(args):
@@ -560,13 +607,17 @@ def main():
     ap.add_argument("--ref-n", type=int, default=10, help="oracle sample: elements per axis")
     ap.add_argument("--ref-iters", type=int, default=3000)
     ap.add_argument("--no-sweep", action="store_true", help="skip the p / size sweeps")
+    ap.add_argument("--oracle-plan", action="store_true",
+                    help="SURVEY §8(d) oracle timing plan on the host cores (no GPU work)")
     ap.add_argument("--sweep-reps", type=int, default=20)
     ap.add_argument("--bp5-cg", action="store_true",
                     help="sweep also runs the BP5 CG solves to 1e-10 (BASELINE config 4, ~15 s)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.oracle_plan:
+        run_oracle_plan(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

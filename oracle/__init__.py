@@ -75,6 +75,7 @@ def lib():
             "orc_l2_error": (d, [M, P, i]),
             "orc_cg": (i, [M, P, i, P, ll, P, P, d, i, i, P, P, P]),
             "orc_num_threads": (i, []),
+            "orc_set_threads": (None, [i]),
             "orc_diagonal": (i, [M, P, i, P]),
             "orc_prolong": (i, [M, M, P, P]),
             "orc_restrict": (i, [M, M, P, P]),
@@ -425,6 +426,10 @@ def pcg(b, M, *, m: Mesh, Ae, bc=1, rel_tol=1e-10, max_iter=500, history=False):
         p = z + (rzn / rz) * p
         rz = rzn
     return x, st, k, np.array(rr), xh
+
+
+def set_threads(n: int):
+    lib().orc_set_threads(int(n))
 
 
 def num_threads() -> int:

@@ -998,6 +998,14 @@ int orc_cheb(const orc_mesh *m, const double *Ae, int bc, const double *dinv, do
   return 0;
 }
 
+void orc_set_threads(int n) {
+#ifdef _OPENMP
+  omp_set_num_threads(n > 0 ? n : 1);
+#else
+  (void)n;
+#endif
+}
+
 int orc_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();
