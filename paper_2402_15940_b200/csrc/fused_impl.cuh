@@ -34,6 +34,7 @@
 #include <type_traits>
 
 #include "internal.h"
+#include "simt_layout.h"
 
 #ifndef HOFEM_SIMT_DSMEM
 #define HOFEM_SIMT_DSMEM -1  // SIMT: D staged in smem (1), from L2 in registers (0), per p (-1)
@@ -65,6 +66,12 @@
 #endif
 #ifndef HOFEM_L2PF_POL
 #define HOFEM_L2PF_POL 0  // 1: the qdata L2 prefetch marks its lines evict_last
+#endif
+#ifndef HOFEM_SIMT_T2QX
+#define HOFEM_SIMT_T2QX 1  // SIMT: T2 [m][qy][c][qx] with qx-fastest stage-2 items (simt_layout.h)
+#endif
+#ifndef HOFEM_LAT_KF
+#define HOFEM_LAT_KF 1  // lattice copies / epilogue rows with k (z) fastest across lanes
 #endif
 #ifndef HOFEM_SIMT_ENDBAR
 #define HOFEM_SIMT_ENDBAR -1  // SIMT: 1 = barrier at the end of every brick, 0 = folded (see
@@ -385,7 +392,8 @@ __device__ __forceinline__ void issue_lattice(const ColArgs& A, double* L, long 
   const bool interior = I0 > 0 && I0 + LX < A.Nx && J0 > 0 && J0 + LY < A.Ny &&
                         (!A.bc || (Kg0 > 0 && Kg0 + LZ < A.NzG));
   FOR_ITEMS(it, LY * LZ * BX, NT, vtid()) {
-    const int sx = it % BX, r = it / BX, j = r % LY, k = r / LY;
+    const int sx = it % BX, r = it / BX;
+    const int j = HOFEM_LAT_KF ? r / LZ : r % LY, k = HOFEM_LAT_KF ? r % LZ : r / LY;
     const long long J = J0 + j, K = K0l + k;
     double* dst = L + C::lat(p * sx, j, k);
     if (interior) {
@@ -585,7 +593,8 @@ __device__ __forceinline__ void brick_epilogue(const ColArgs& A, const double* R
   // multiple of 32 so every warp runs a single compile-time segment SX
   constexpr int ROWS = LY * P1, RPS = (ROWS + 31) / 32 * 32;
   FOR_ITEMS(it, RPS * BX, NT, threadIdx.x) {
-    const int sx = it / RPS, r = it % RPS, j = r % LY, k = r / LY;
+    const int sx = it / RPS, r = it % RPS;
+    const int j = HOFEM_LAT_KF ? r / P1 : r % LY, k = HOFEM_LAT_KF ? r % P1 : r / LY;
     if (r >= ROWS) continue;
     const long long J = J0 + j, K = K0l + k, Kg = K + A.K0;
     if (J >= A.Ny) continue;
@@ -830,14 +839,30 @@ struct CfgS {
   static constexpr int NA = (KIND == KIND_MASS) ? 1 : 2;
   static constexpr int NB = (KIND == KIND_MASS) ? 1 : 3;
   static constexpr int NC = (KIND == KIND_MASS) ? 1 : 6;
-  static constexpr int S1 = P * P + (((P - P * P) % 16) + 16) % 16;
-  static constexpr int T1M = Q * S1, T1SZ = NA * T1M;
-  static constexpr int SP = (P % 2) ? P : P + 1;
-  static constexpr int T2M = Q * Q * SP;
   static constexpr int SA = ((P * P) % 2 == 0) ? P * P + 1 : P * P;
   static constexpr int YEN = SA * P;
+#if HOFEM_SIMT_T2QX
+  // T1 [m][qx][b*P+c] (qx stride S1), T2 [m][qy][c][qx] (qy stride TY, c stride
+  // TC = Q), stage-2 items qx fastest: strides from the generated conflict
+  // search (simt_layout.h); every kind uses the diffusion block's residue mod 16
+  using LYT = LayoutS<P1, Q, NE>;
+  static constexpr bool QXF = true;
+  static constexpr int S1 = LYT::S1, SP = P, TY = LYT::RS, TX = 1, TC = Q;
+  static constexpr int T1M = Q * S1, T1SZ = NA * T1M;
+  static constexpr int T2M = Q * TY;
+  static constexpr int EB0 = T1SZ + cmax(NB * T2M, YEN);
+  static constexpr int EBD = 2 * Q * S1 + cmax(3 * T2M, YEN) + LYT::EBPAD;
+  static constexpr int EB = EB0 + ((EBD - EB0) % 16 + 16) % 16;
+#else
+  // T2 [m][qy][qx][c], odd point stride SP, stage-2 items c fastest
+  static constexpr bool QXF = false;
+  static constexpr int S1 = P * P + (((P - P * P) % 16) + 16) % 16;
+  static constexpr int SP = (P % 2) ? P : P + 1, TY = Q * SP, TX = SP, TC = 1;
+  static constexpr int T1M = Q * S1, T1SZ = NA * T1M;
+  static constexpr int T2M = Q * Q * SP;
   static constexpr int EB0 = T1SZ + cmax(NB * T2M, YEN);
   static constexpr int EB = EB0 + ((7 - EB0) % 16 + 16) % 16;  // == 7 (mod 16)
+#endif
   static constexpr int CARRY = LX * LY;
   static constexpr int PR = P + (P & 1);  // table row stride
   static constexpr int TOFF0 = NE * EB + 2 * LAT + 2 * CARRY;
@@ -1030,7 +1055,8 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
   // folded end-of-brick barrier: +1-2 % for BP1/BP3, -1.5 % for BP5
   constexpr bool ENDBAR = HOFEM_SIMT_ENDBAR >= 0 ? HOFEM_SIMT_ENDBAR != 0 : COL;
   constexpr int EB = C::EB, S1 = C::S1, T1M = C::T1M, T1SZ = C::T1SZ, SP = C::SP,
-                T2M = C::T2M, PR = C::PR;
+                T2M = C::T2M, PR = C::PR, TY = C::TY, TX = C::TX, TC = C::TC;
+  (void)SP;
   extern __shared__ __align__(16) double smem[];
   double* LB = smem + NE * EB;
   double* CY = LB + 2 * C::LAT;
@@ -1164,7 +1190,8 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
     }
     // ---- S2: contract y.  item (el, qx, c), c fastest.
     FOR_ITEMS(it, NE * Q * P, NT, tid) {
-      const int el = it / (Q * P), r = it % (Q * P), qx = r / P, c = r % P;
+      const int el = it / (Q * P), r = it % (Q * P);
+      const int qx = C::QXF ? r % Q : r / P, c = C::QXF ? r / Q : r % P;
       const double* t1 = smem + el * EB + qx * S1 + c;
       double vb[P], vg[P];
 #pragma unroll
@@ -1172,18 +1199,18 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
         vb[b] = t1[b * P];
         vg[b] = DIFF ? t1[T1M + b * P] : 0.0;
       }
-      double* t2 = smem + el * EB + T1SZ + qx * SP + c;
+      double* t2 = smem + el * EB + T1SZ + qx * TX + c * TC;
       if constexpr (EO) {
         double eb[H], ob[PH], eg[H], og[PH];
         eo_split<P>(vb, eb, ob);
         if (DIFF && !COL) eo_split<P>(vg, eg, og);
         auto put = [&](int qy, double bb, double gb, double bg) {
           if (DIFF) {
-            t2[qy * Q * SP] = gb;            // G_x B_y  (-> u_x)
-            t2[T2M + qy * Q * SP] = bg;      // B_x G_y  (-> u_y)
-            t2[2 * T2M + qy * Q * SP] = bb;  // B_x B_y  (-> u_z)
+            t2[qy * TY] = gb;            // G_x B_y  (-> u_x)
+            t2[T2M + qy * TY] = bg;      // B_x G_y  (-> u_y)
+            t2[2 * T2M + qy * TY] = bb;  // B_x B_y  (-> u_z)
           } else {
-            t2[qy * Q * SP] = bb;
+            t2[qy * TY] = bb;
           }
         };
 #pragma unroll
@@ -1231,11 +1258,11 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
           gb = vg[qy];
         }
         if (DIFF) {
-          t2[qy * Q * SP] = gb;            // G_x B_y  (-> u_x)
-          t2[T2M + qy * Q * SP] = bg;      // B_x G_y  (-> u_y)
-          t2[2 * T2M + qy * Q * SP] = bb;  // B_x B_y  (-> u_z)
+          t2[qy * TY] = gb;            // G_x B_y  (-> u_x)
+          t2[T2M + qy * TY] = bg;      // B_x G_y  (-> u_y)
+          t2[2 * T2M + qy * TY] = bb;  // B_x B_y  (-> u_z)
         } else {
-          t2[qy * Q * SP] = bb;
+          t2[qy * TY] = bb;
         }
       }
       }
@@ -1257,7 +1284,7 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
           C::DSM ? QS + el * C::QSLOT + stage_off<C>(A, ex, ey, ez) + pt
                  : A.qd + (ex + (long long)A.nx * (ey + (long long)A.ny * ez)) *
                               (long long)(C::NC * Q3) + pt;
-      double* t2 = smem + el * EB + T1SZ + pt * SP;
+      double* t2 = smem + el * EB + T1SZ + (pt / Q) * TY + (pt % Q) * TX;
       if constexpr (EO) {
         // pairs (qz = t, Q-1-t), then the middle point (odd Q); the next pair's
         // D values are loaded while this pair computes
@@ -1278,9 +1305,9 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
           double g0[P], g1[P], g2[P];
 #pragma unroll
           for (int c = 0; c < P; ++c) {
-            g0[c] = t2[c];
-            g1[c] = t2[T2M + c];
-            g2[c] = t2[2 * T2M + c];
+            g0[c] = t2[c * TC];
+            g1[c] = t2[T2M + c * TC];
+            g2[c] = t2[2 * T2M + c * TC];
           }
           double e0[H], o0[PH], e1[H], o1[PH], e2[H], o2[PH];
           if (!COL) {
@@ -1320,8 +1347,8 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
             const double w2l = dl[2] * u0l + dl[4] * u1l + dl[5] * u2l;
             if (mid) {
               if (COL) {
-                t2[t] = w0l;  // written after all loads of g0 (registers)
-                t2[T2M + t] = w1l;
+                t2[t * TC] = w0l;  // written after all loads of g0 (registers)
+                t2[T2M + t * TC] = w1l;
               } else {
                 eo_acc_mid<1, P>(T.BE, T.BO, t, zo, w0l, SE0, SO0);
                 eo_acc_mid<1, P>(T.BE, T.BO, t, zo, w1l, SE1, SO1);
@@ -1332,8 +1359,8 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
               const double w1h = dh[1] * u0h + dh[3] * u1h + dh[4] * u2h;
               const double w2h = dh[2] * u0h + dh[4] * u1h + dh[5] * u2h;
               if (COL) {
-                t2[t] = w0l; t2[Q - 1 - t] = w0h;
-                t2[T2M + t] = w1l; t2[T2M + Q - 1 - t] = w1h;
+                t2[t * TC] = w0l; t2[(Q - 1 - t) * TC] = w0h;
+                t2[T2M + t * TC] = w1l; t2[T2M + (Q - 1 - t) * TC] = w1h;
               } else {
                 eo_acc<1, P>(T.BE, T.BO, t, zo, w0l, w0h, SE0, SO0);
                 eo_acc<1, P>(T.BE, T.BO, t, zo, w1l, w1h, SE1, SO1);
@@ -1345,18 +1372,18 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
           if (!COL) {
             eo_join<P>(SE0, SO0, s);
 #pragma unroll
-            for (int c = 0; c < P; ++c) t2[c] = s[c];
+            for (int c = 0; c < P; ++c) t2[c * TC] = s[c];
             eo_join<P>(SE1, SO1, s);
 #pragma unroll
-            for (int c = 0; c < P; ++c) t2[T2M + c] = s[c];
+            for (int c = 0; c < P; ++c) t2[T2M + c * TC] = s[c];
           }
           eo_join<P>(SE2, SO2, s);
 #pragma unroll
-          for (int c = 0; c < P; ++c) t2[2 * T2M + c] = s[c];
+          for (int c = 0; c < P; ++c) t2[2 * T2M + c * TC] = s[c];
         } else {
           double g[P];
 #pragma unroll
-          for (int c = 0; c < P; ++c) g[c] = t2[c];
+          for (int c = 0; c < P; ++c) g[c] = t2[c * TC];
           double e[H], o[PH], SE[H], SO[PH];
           eo_split<P>(g, e, o);
           zero(SE); zero(SO);
@@ -1377,7 +1404,7 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
           double s[P];
           eo_join<P>(SE, SO, s);
 #pragma unroll
-          for (int c = 0; c < P; ++c) t2[c] = s[c];
+          for (int c = 0; c < P; ++c) t2[c * TC] = s[c];
         }
       } else {
       if (DIFF) {
@@ -1393,9 +1420,9 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
         double g0[P], g1[P], g2[P], s0[P], s1[P], s2[P];
 #pragma unroll
         for (int c = 0; c < P; ++c) {
-          g0[c] = t2[c];
-          g1[c] = t2[T2M + c];
-          g2[c] = t2[2 * T2M + c];
+          g0[c] = t2[c * TC];
+          g1[c] = t2[T2M + c * TC];
+          g2[c] = t2[2 * T2M + c * TC];
           s0[c] = s1[c] = s2[c] = 0.0;
         }
 #pragma unroll
@@ -1441,14 +1468,14 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
         }
 #pragma unroll
         for (int c = 0; c < P; ++c) {
-          t2[c] = s0[c];
-          t2[T2M + c] = s1[c];
-          t2[2 * T2M + c] = s2[c];
+          t2[c * TC] = s0[c];
+          t2[T2M + c * TC] = s1[c];
+          t2[2 * T2M + c * TC] = s2[c];
         }
       } else {
         double g[P], s[P];
 #pragma unroll
-        for (int c = 0; c < P; ++c) { g[c] = t2[c]; s[c] = 0.0; }
+        for (int c = 0; c < P; ++c) { g[c] = t2[c * TC]; s[c] = 0.0; }
         double dn = ld_d<C::DSM>(qde);
 #pragma unroll
         for (int qz = 0; qz < Q; ++qz) {
@@ -1464,7 +1491,7 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
           for (int c = 0; c < P; ++c) s[c] = fma(br[c], v, s[c]);
         }
 #pragma unroll
-        for (int c = 0; c < P; ++c) t2[c] = s[c];
+        for (int c = 0; c < P; ++c) t2[c * TC] = s[c];
       }
       }
     }
@@ -1473,15 +1500,16 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
 
     // ---- S2T: contract qy.  item (el, qx, c), c fastest.
     FOR_ITEMS(it, NE * Q * P, NT, tid) {
-      const int el = it / (Q * P), r = it % (Q * P), qx = r / P, c = r % P;
-      const double* t2 = smem + el * EB + T1SZ + qx * SP + c;
+      const int el = it / (Q * P), r = it % (Q * P);
+      const int qx = C::QXF ? r % Q : r / P, c = C::QXF ? r / Q : r % P;
+      const double* t2 = smem + el * EB + T1SZ + qx * TX + c * TC;
       double* t1 = smem + el * EB + qx * S1 + c;
       if constexpr (EO) {
         // rg = B_y^T v0 (x part), rb = G_y^T v1 + B_y^T v2 (y, z parts); mass: rb = B_y^T v0
         double SEg[H], SOg[PH], SEb[H], SOb[PH];
         zero(SEg); zero(SOg); zero(SEb); zero(SOb);
         double rg[P] = {}, rb[P];
-        constexpr int QS = Q * SP;
+        constexpr int QS = TY;
 #pragma unroll
         for (int t = 0; t < (Q + 1) / 2; ++t) {
           const int th = Q - 1 - t;
@@ -1539,16 +1567,16 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
         if (!COL) TROW(B, qy, br);
         if (COL) {
           TROW(G, qy, gr);
-          const double v0 = t2[qy * Q * SP], v1 = t2[T2M + qy * Q * SP],
-                       v2 = t2[2 * T2M + qy * Q * SP];
+          const double v0 = t2[qy * TY], v1 = t2[T2M + qy * TY],
+                       v2 = t2[2 * T2M + qy * TY];
           rg[qy] = v0;
 #pragma unroll
           for (int b = 0; b < P; ++b) rb[b] = fma(gr[b], v1, rb[b]);
           rb[qy] += v2;
         } else if (DIFF) {
           TROW(G, qy, gr);
-          const double v0 = t2[qy * Q * SP], v1 = t2[T2M + qy * Q * SP],
-                       v2 = t2[2 * T2M + qy * Q * SP];
+          const double v0 = t2[qy * TY], v1 = t2[T2M + qy * TY],
+                       v2 = t2[2 * T2M + qy * TY];
 #pragma unroll
           for (int b = 0; b < P; ++b) {
             rg[b] = fma(br[b], v0, rg[b]);
@@ -1556,7 +1584,7 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
             rb[b] = fma(br[b], v2, rb[b]);
           }
         } else {
-          const double v = t2[qy * Q * SP];
+          const double v = t2[qy * TY];
 #pragma unroll
           for (int b = 0; b < P; ++b) rb[b] = fma(br[b], v, rb[b]);
         }
