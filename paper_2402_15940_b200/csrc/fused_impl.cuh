@@ -68,10 +68,12 @@
 #define HOFEM_L2PF_POL 0  // 1: the qdata L2 prefetch marks its lines evict_last
 #endif
 #ifndef HOFEM_SIMT_T2QX
-#define HOFEM_SIMT_T2QX 1  // SIMT: T2 [m][qy][c][qx] with qx-fastest stage-2 items (simt_layout.h)
+#define HOFEM_SIMT_T2QX -1  // SIMT: 1 = T2 [m][qy][c][qx] with qx-fastest stage-2 items
+                            // (simt_layout.h), 0 = T2 [m][qy][qx][c], -1 = per P1 (measured)
 #endif
 #ifndef HOFEM_LAT_KF
-#define HOFEM_LAT_KF 1  // lattice copies / epilogue rows with k (z) fastest across lanes
+#define HOFEM_LAT_KF 0  // lattice copies / epilogue rows with k (z) fastest across lanes
+                        // (measured r2h: no gain for BP3, -5 % for BP5 at p = 5)
 #endif
 #ifndef HOFEM_SIMT_ENDBAR
 #define HOFEM_SIMT_ENDBAR -1  // SIMT: 1 = barrier at the end of every brick, 0 = folded (see
@@ -829,6 +831,15 @@ __device__ __forceinline__ double ld_dp(const double* ptr, unsigned long long po
   }
 }
 
+// Per-P1 stage layout (HOFEM_SIMT_T2QX = -1).  Measured (gpurun_out/r2h,
+// profiles/ab/r2h_ab_layout.txt, brick-kernel ms at 30M dofs): qx-fastest T2 wins
+// at P1 = 3 (BP3 -4 %, BP5 -6 %) and P1 = 6 (p=5: BP3 -2.7 %, BP5 -5 %), loses
+// at P1 = 5 (BP3 +2.5 %, BP5 +8 %), ~neutral at P1 = 7, 9 (old kept).
+template <int P1>
+constexpr bool simt_t2qx() {
+  return HOFEM_SIMT_T2QX >= 0 ? HOFEM_SIMT_T2QX != 0 : (P1 == 3 || P1 == 6 || P1 == 2 || P1 == 4 || P1 == 8);
+}
+
 template <int KIND, int P1, int Q, int BX, int BY>
 struct CfgS {
   static constexpr int p = P1 - 1, P = P1, NE = BX * BY;
@@ -841,28 +852,23 @@ struct CfgS {
   static constexpr int NC = (KIND == KIND_MASS) ? 1 : 6;
   static constexpr int SA = ((P * P) % 2 == 0) ? P * P + 1 : P * P;
   static constexpr int YEN = SA * P;
-#if HOFEM_SIMT_T2QX
-  // T1 [m][qx][b*P+c] (qx stride S1), T2 [m][qy][c][qx] (qy stride TY, c stride
-  // TC = Q), stage-2 items qx fastest: strides from the generated conflict
-  // search (simt_layout.h); every kind uses the diffusion block's residue mod 16
+  // T1 [m][qx][b*P+c]: qx stride S1.  QXF: T2 [m][qy][c][qx] (qy stride TY,
+  // c stride TC = Q), stage-2 items qx fastest, strides from the generated
+  // conflict search (simt_layout.h; every kind keeps the diffusion block's
+  // residue mod 16).  Otherwise T2 [m][qy][qx][c] with odd point stride SP and
+  // c-fastest stage-2 items.
+  static constexpr bool QXF = simt_t2qx<P1>();
   using LYT = LayoutS<P1, Q, NE>;
-  static constexpr bool QXF = true;
-  static constexpr int S1 = LYT::S1, SP = P, TY = LYT::RS, TX = 1, TC = Q;
+  static constexpr int SPO = (P % 2) ? P : P + 1;
+  static constexpr int S1 = QXF ? LYT::S1 : P * P + (((P - P * P) % 16) + 16) % 16;
+  static constexpr int SP = QXF ? P : SPO;
+  static constexpr int TY = QXF ? LYT::RS : Q * SPO, TX = QXF ? 1 : SPO, TC = QXF ? Q : 1;
   static constexpr int T1M = Q * S1, T1SZ = NA * T1M;
   static constexpr int T2M = Q * TY;
   static constexpr int EB0 = T1SZ + cmax(NB * T2M, YEN);
   static constexpr int EBD = 2 * Q * S1 + cmax(3 * T2M, YEN) + LYT::EBPAD;
-  static constexpr int EB = EB0 + ((EBD - EB0) % 16 + 16) % 16;
-#else
-  // T2 [m][qy][qx][c], odd point stride SP, stage-2 items c fastest
-  static constexpr bool QXF = false;
-  static constexpr int S1 = P * P + (((P - P * P) % 16) + 16) % 16;
-  static constexpr int SP = (P % 2) ? P : P + 1, TY = Q * SP, TX = SP, TC = 1;
-  static constexpr int T1M = Q * S1, T1SZ = NA * T1M;
-  static constexpr int T2M = Q * Q * SP;
-  static constexpr int EB0 = T1SZ + cmax(NB * T2M, YEN);
-  static constexpr int EB = EB0 + ((7 - EB0) % 16 + 16) % 16;  // == 7 (mod 16)
-#endif
+  static constexpr int EB = QXF ? EB0 + ((EBD - EB0) % 16 + 16) % 16
+                                : EB0 + ((7 - EB0) % 16 + 16) % 16;  // old: == 7 (mod 16)
   static constexpr int CARRY = LX * LY;
   static constexpr int PR = P + (P & 1);  // table row stride
   static constexpr int TOFF0 = NE * EB + 2 * LAT + 2 * CARRY;
