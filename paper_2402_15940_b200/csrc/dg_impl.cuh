@@ -8,17 +8,18 @@
 // D_e = W detJ at the Q^3 Gauss points (the BP1 qdata) and B the 1D basis table
 // applied dimension by dimension -- no gather, no scatter, no fix-up.
 //
-// Persistent kernel, one CTA per (SM x occupancy), batches of NE elements:
-//   - x of the NEXT batch arrives by asynchronous 8-byte copies (coalesced global
-//     reads) into a padded, a-slowest shared-memory stage (odd strides: bank-
-//     conflict-free stage-1 reads), double-buffered;
-//   - D of the next batch (contiguous NE*Q^3 doubles) by ONE bulk copy
-//     (cp.async.bulk, the TMA engine) into a second double-buffered stage,
-//     completion on an mbarrier;
-//   - the five thread-per-line stages of the SIMT brick kernel (even-odd
-//     contractions, tables from the kernel-parameter constant bank): x, y, z+D+z^T,
-//     y^T, x^T;
-//   - y written back with coalesced stores.
+// Persistent kernel, one CTA per (SM x occupancy), batches of NE elements.
+// x and y stay in their natural element-contiguous layout end to end:
+//   - x and D of the NEXT batch arrive by two bulk copies (cp.async.bulk, the
+//     TMA engine) into a double-buffered stage, completing on one mbarrier;
+//   - the five thread-per-line stages contract z first (lines along the slowest
+//     index, so lanes run over contiguous (a, b) and read the dense x without
+//     bank conflicts), then y, then x with the pointwise D, and back (x^T, y^T,
+//     z^T) -- even-odd contractions, tables from the kernel-parameter constant
+//     bank, padded strides from a bank-conflict search (dg_layout below);
+//   - z^T writes y densely into the batch's x stage, which ONE bulk store
+//     (cp.async.bulk global <- shared) sends to HBM.
+// No per-dof index arithmetic is left outside the contraction stages.
 // Bound: HBM (16 + 8 Q^3/P1^3 B/DOF; flop/B < 3.1 even at p = 8).
 #pragma once
 
@@ -29,58 +30,65 @@ namespace hofem {
 struct DGArgs {
   const double* x;
   double* y;
-  const double* qd;  // [E][Q^3] W*detJ
+  const double* qd;  // [E][Q^3] W*detJ (allocated with 2 doubles of slack)
   long long E;       // local elements
   long long nbatch;  // ceil(E / NE)
 };
 
+// Work-area strides per element: T1 [qz][b][a] (qz stride R1), T2 [qz][qy][a]
+// (qz stride R2, qy stride PP), element block EB = Q R1 + Q R2 + PAD.
+template <int P1, int NE>
+struct LayoutDG {  // generic fallback (odd row strides)
+  static constexpr int Q = P1 + 1;
+  static constexpr int R1 = P1 * P1, PP = (P1 % 2) ? P1 : P1 + 1, R2 = Q * PP, PAD = 0;
+};
+
 template <int P1, int Q, int NE>
 struct CfgDG {
+  using L = LayoutDG<P1, NE>;
   static constexpr int P = P1, P2 = P1 * P1, P3 = P2 * P1, Q2 = Q * Q, Q3 = Q2 * Q;
-  static constexpr int XS = (P2 % 2) ? P2 : P2 + 1;  // a-stride of x / y staging (odd)
-  static constexpr int XE = P * XS;                  // doubles per element
-  static constexpr int S1 = P2 + (((P - P2) % 16) + 16) % 16;
-  static constexpr int T1M = Q * S1;
-  static constexpr int SP = (P % 2) ? P : P + 1;
-  static constexpr int T2M = Q2 * SP;
-  static constexpr int EB0 = T1M + (T2M > XE ? T2M : XE);
-  static constexpr int EB = EB0 + ((7 - EB0) % 16 + 16) % 16;  // == 7 (mod 16)
-  static constexpr int XB = NE * XE;                             // one x stage
-  static constexpr int QSL = ((NE * Q3 + 2) + 1) / 2 * 2;        // one D stage (even)
+  static constexpr int R1 = L::R1, PP = L::PP, R2 = L::R2;
+  static constexpr int T2OFF = Q * R1;
+  static constexpr int EB = Q * R1 + Q * R2 + L::PAD;
+  static constexpr int XB = ((NE * P3) + 1) / 2 * 2;             // x in / y out stage (even)
+  static constexpr int QSL = ((NE * Q3 + 2) + 1) / 2 * 2;        // D stage (even)
   static constexpr int OFF_X = 0;
-  static constexpr int OFF_Q = ((2 * XB) + 1) / 2 * 2;           // 16-byte aligned
+  static constexpr int OFF_Q = 2 * XB;
   static constexpr int OFF_W = OFF_Q + 2 * QSL;
   static constexpr int SMEM_DOUBLES = OFF_W + NE * EB;
   static constexpr int SMEM_BYTES = SMEM_DOUBLES * 8;
-  static_assert(T2M >= XE, "y staging aliases T2");
 };
 
-template <int P1, int Q, int NE, int NT>
-__device__ __forceinline__ void dg_issue_x(const DGArgs& A, double* xs, long long bk) {
-  using C = CfgDG<P1, Q, NE>;
-  constexpr int P = P1;
-  const long long e0 = bk * NE;
-  for (int i = threadIdx.x; i < NE * C::P3; i += NT) {
-    const int el = i / C::P3, g = i - el * C::P3;
-    const int a = g % P, b = (g / P) % P, c = g / C::P2;
-    const bool valid = e0 + el < A.E;
-    cp_async8(xs + el * C::XE + a * C::XS + b * P + c, valid ? A.x + (e0 * C::P3 + i) : A.x,
-              valid);
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Thread 0: x and D of batch bk into stage (xs, qs), completing on `bar`.  An
+// odd-length x tail (last batch only) loads its final double directly (the
+// bulk size must be a multiple of 16 B and x has no slack); D has 16 B of slack.
 template <int P1, int Q, int NE>
-__device__ __forceinline__ void dg_issue_q(const DGArgs& A, double* qs, unsigned long long* bar,
-                                           long long bk) {
+__device__ __forceinline__ void dg_issue(const DGArgs& A, double* xs, double* qs,
+                                         unsigned long long* bar, long long bk) {
   using C = CfgDG<P1, Q, NE>;
-  if (threadIdx.x != 0) return;
   const long long e0 = bk * NE;
   const long long cnt = A.E - e0 < NE ? A.E - e0 : NE;
-  const unsigned bytes = (unsigned)((cnt * C::Q3 * 8 + 15) & ~15LL);  // qdata has 16 B of slack
+  const long long nx = cnt * C::P3;
+  const unsigned xbytes = (unsigned)((nx & ~1LL) * 8);
+  const unsigned qbytes = (unsigned)((cnt * C::Q3 * 8 + 15) & ~15LL);
+  if (nx & 1) xs[nx - 1] = A.x[e0 * C::P3 + nx - 1];
   fence_proxy_async();
-  mbar_expect_tx(bar, bytes);
-  bulk_g2s(qs, A.qd + e0 * C::Q3, bytes, bar);
+  mbar_expect_tx(bar, xbytes + qbytes);
+  if (xbytes) bulk_g2s(xs, A.x + e0 * C::P3, xbytes, bar);
+  bulk_g2s(qs, A.qd + e0 * C::Q3, qbytes, bar);
 }
 
 template <int P1, int Q, int NE, int NT>
@@ -88,7 +96,8 @@ __global__ void __launch_bounds__(NT) dg_mass_simt(const __grid_constant__ Tab<P
                                                    const __grid_constant__ DGArgs A) {
   using C = CfgDG<P1, Q, NE>;
   constexpr int P = P1, H = (P + 1) / 2, PH = P / 2, QH = Q / 2, HQ = (Q + 1) / 2;
-  constexpr int Q2 = C::Q2, S1 = C::S1, T1M = C::T1M, SP = C::SP, EB = C::EB, XS = C::XS;
+  constexpr int P2 = C::P2, P3 = C::P3, Q2 = C::Q2, Q3 = C::Q3, R1 = C::R1, R2 = C::R2,
+                PP = C::PP, EB = C::EB, T2O = C::T2OFF;
   (void)H; (void)PH;
   extern __shared__ __align__(16) double smem[];
   double* XS0 = smem + C::OFF_X;
@@ -103,151 +112,143 @@ __global__ void __launch_bounds__(NT) dg_mass_simt(const __grid_constant__ Tab<P
   __syncthreads();
   long long bk = blockIdx.x;
   if (bk >= A.nbatch) return;
-  dg_issue_x<P1, Q, NE, NT>(A, XS0, bk);
-  dg_issue_q<P1, Q, NE>(A, QS0, &qbar[0], bk);
+  if (threadIdx.x == 0) dg_issue<P1, Q, NE>(A, XS0, QS0, &qbar[0], bk);
   unsigned phase = 0;  // bit j: parity of qbar[j]
   for (int k = 0; bk < A.nbatch; ++k, bk += gridDim.x) {
     const int buf = k & 1;
     const long long nb = bk + gridDim.x;
     const int tid = vtid();
     const int zo = (int)(bk >> 40);  // == 0, loop-variant (see cb_row in fused_impl.cuh)
-    if (nb < A.nbatch) {
-      dg_issue_x<P1, Q, NE, NT>(A, XS0 + (buf ^ 1) * C::XB, nb);
-      dg_issue_q<P1, Q, NE>(A, QS0 + (buf ^ 1) * C::QSL, &qbar[buf ^ 1], nb);
-    } else {
-      asm volatile("cp.async.commit_group;" ::: "memory");
+    double* X = XS0 + buf * C::XB;
+    const double* QD = QS0 + buf * C::QSL;
+    if (threadIdx.x == 0 && nb < A.nbatch) {
+      bulk_wait_read();  // the previous batch's y store has read stage buf^1
+      dg_issue<P1, Q, NE>(A, XS0 + (buf ^ 1) * C::XB, QS0 + (buf ^ 1) * C::QSL, &qbar[buf ^ 1],
+                          nb);
     }
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-    cta_sync();
-    const double* X = XS0 + buf * C::XB;
+    mbar_wait(&qbar[buf], (phase >> buf) & 1u);
+    phase ^= 1u << buf;
+    cta_sync();  // (the odd tail double of x is a generic store by thread 0)
 
-    // ---- S1: x lines (items (b, c), c fastest) -> T1[qx][b][c]
-    FOR_ITEMS(it, NE * P * P, NT, tid) {
-      const int el = it / (P * P), r = it % (P * P);
-      const double* xl = X + el * C::XE + r;
-      double xa[P];
+    // ---- S1: z lines (items (b, a), a fastest) -> T1[qz][b][a]
+    FOR_ITEMS(it, NE * P2, NT, tid) {
+      const int el = it / P2, r = it % P2;
+      const double* xl = X + el * P3 + r;
+      double v[P];
 #pragma unroll
-      for (int a = 0; a < P; ++a) xa[a] = xl[XS * a];
+      for (int c = 0; c < P; ++c) v[c] = xl[c * P2];
       double e[H], o[PH];
-      eo_split<P>(xa, e, o);
+      eo_split<P>(v, e, o);
       double* t1 = W + el * EB + r;
 #pragma unroll
       for (int t = 0; t < QH; ++t) {
         double lo, hi;
         eo_fwd<1, P>(T.BE, T.BO, t, zo, e, o, lo, hi);
-        t1[t * S1] = lo;
-        t1[(Q - 1 - t) * S1] = hi;
+        t1[t * R1] = lo;
+        t1[(Q - 1 - t) * R1] = hi;
       }
-      if (Q & 1) t1[QH * S1] = eo_fwd_mid<1, P>(T.BE, T.BO, QH, zo, e, o);
+      if (Q & 1) t1[QH * R1] = eo_fwd_mid<1, P>(T.BE, T.BO, QH, zo, e, o);
     }
     cta_sync();
-    // ---- S2: y lines (items (qx, c), c fastest) -> T2[qy][qx][c]
+    // ---- S2: y lines (items (qz, a), a fastest) -> T2[qz][qy][a]
     FOR_ITEMS(it, NE * Q * P, NT, tid) {
-      const int el = it / (Q * P), r = it % (Q * P), qx = r / P, c = r % P;
-      const double* t1 = W + el * EB + qx * S1 + c;
-      double vb[P];
+      const int el = it / (Q * P), r = it % (Q * P), qz = r / P, a = r % P;
+      const double* t1 = W + el * EB + qz * R1 + a;
+      double v[P];
 #pragma unroll
-      for (int b = 0; b < P; ++b) vb[b] = t1[b * P];
-      double eb[H], ob[PH];
-      eo_split<P>(vb, eb, ob);
-      double* t2 = W + el * EB + T1M + qx * SP + c;
+      for (int b = 0; b < P; ++b) v[b] = t1[b * P];
+      double e[H], o[PH];
+      eo_split<P>(v, e, o);
+      double* t2 = W + el * EB + T2O + qz * R2 + a;
 #pragma unroll
       for (int t = 0; t < QH; ++t) {
         double lo, hi;
-        eo_fwd<1, P>(T.BE, T.BO, t, zo, eb, ob, lo, hi);
-        t2[t * Q * SP] = lo;
-        t2[(Q - 1 - t) * Q * SP] = hi;
+        eo_fwd<1, P>(T.BE, T.BO, t, zo, e, o, lo, hi);
+        t2[t * PP] = lo;
+        t2[(Q - 1 - t) * PP] = hi;
       }
-      if (Q & 1) t2[QH * Q * SP] = eo_fwd_mid<1, P>(T.BE, T.BO, QH, zo, eb, ob);
+      if (Q & 1) t2[QH * PP] = eo_fwd_mid<1, P>(T.BE, T.BO, QH, zo, e, o);
     }
     cta_sync();
-    // ---- S3: z lines (items (qx, qy)): z contraction, D, z back-contraction
-    mbar_wait(&qbar[buf], (phase >> buf) & 1u);
-    phase ^= 1u << buf;
-    {
-      const double* QD = QS0 + buf * C::QSL;
-      FOR_ITEMS(it, NE * Q2, NT, tid) {
-        const int el = it / Q2, pt = it % Q2;
-        const double* qde = QD + el * C::Q3 + pt;
-        double* t2 = W + el * EB + T1M + pt * SP;
-        double g[P];
+    // ---- S3: x lines (items (qz, qy), qy fastest): x contraction, D, x back
+    FOR_ITEMS(it, NE * Q2, NT, tid) {
+      const int el = it / Q2, r = it % Q2, qz = r / Q, qy = r % Q;
+      double* t2 = W + el * EB + T2O + qz * R2 + qy * PP;
+      const double* qde = QD + el * Q3 + qz * Q2 + qy * Q;
+      double g[P];
 #pragma unroll
-        for (int c = 0; c < P; ++c) g[c] = t2[c];
-        double e[H], o[PH], SE[H], SO[PH];
-        eo_split<P>(g, e, o);
-        zero(SE);
-        zero(SO);
+      for (int a = 0; a < P; ++a) g[a] = t2[a];
+      double e[H], o[PH], SE[H], SO[PH];
+      eo_split<P>(g, e, o);
+      zero(SE);
+      zero(SO);
 #pragma unroll
-        for (int t = 0; t < HQ; ++t) {
-          if ((Q & 1) && t == QH) {
-            const double u = eo_fwd_mid<1, P>(T.BE, T.BO, t, zo, e, o);
-            eo_acc_mid<1, P>(T.BE, T.BO, t, zo, qde[t * Q2] * u, SE, SO);
-          } else {
-            double ul, uh;
-            eo_fwd<1, P>(T.BE, T.BO, t, zo, e, o, ul, uh);
-            eo_acc<1, P>(T.BE, T.BO, t, zo, qde[t * Q2] * ul, qde[(Q - 1 - t) * Q2] * uh, SE,
-                         SO);
-          }
+      for (int t = 0; t < HQ; ++t) {
+        if ((Q & 1) && t == QH) {
+          const double u = eo_fwd_mid<1, P>(T.BE, T.BO, t, zo, e, o);
+          eo_acc_mid<1, P>(T.BE, T.BO, t, zo, qde[t] * u, SE, SO);
+        } else {
+          double ul, uh;
+          eo_fwd<1, P>(T.BE, T.BO, t, zo, e, o, ul, uh);
+          eo_acc<1, P>(T.BE, T.BO, t, zo, qde[t] * ul, qde[Q - 1 - t] * uh, SE, SO);
         }
-        double s[P];
-        eo_join<P>(SE, SO, s);
-#pragma unroll
-        for (int c = 0; c < P; ++c) t2[c] = s[c];
       }
+      double s[P];
+      eo_join<P>(SE, SO, s);
+#pragma unroll
+      for (int a = 0; a < P; ++a) t2[a] = s[a];
     }
     cta_sync();
-    // ---- S2T: y back (items (qx, c)) -> T1[qx][b][c]
+    // ---- S2T: y back (items (qz, a)) -> T1[qz][b][a]
     FOR_ITEMS(it, NE * Q * P, NT, tid) {
-      const int el = it / (Q * P), r = it % (Q * P), qx = r / P, c = r % P;
-      const double* t2 = W + el * EB + T1M + qx * SP + c;
-      double* t1 = W + el * EB + qx * S1 + c;
+      const int el = it / (Q * P), r = it % (Q * P), qz = r / P, a = r % P;
+      const double* t2 = W + el * EB + T2O + qz * R2 + a;
+      double* t1 = W + el * EB + qz * R1 + a;
       double SE[H], SO[PH], rb[P];
       zero(SE);
       zero(SO);
-      constexpr int QS = Q * SP;
 #pragma unroll
       for (int t = 0; t < HQ; ++t) {
         if ((Q & 1) && t == QH)
-          eo_acc_mid<1, P>(T.BE, T.BO, t, zo, t2[t * QS], SE, SO);
+          eo_acc_mid<1, P>(T.BE, T.BO, t, zo, t2[t * PP], SE, SO);
         else
-          eo_acc<1, P>(T.BE, T.BO, t, zo, t2[t * QS], t2[(Q - 1 - t) * QS], SE, SO);
+          eo_acc<1, P>(T.BE, T.BO, t, zo, t2[t * PP], t2[(Q - 1 - t) * PP], SE, SO);
       }
       eo_join<P>(SE, SO, rb);
 #pragma unroll
       for (int b = 0; b < P; ++b) t1[b * P] = rb[b];
     }
     cta_sync();
-    // ---- S1T: x back (items (b, c)) -> y staging [a][b][c] (aliases T2)
-    FOR_ITEMS(it, NE * P * P, NT, tid) {
-      const int el = it / (P * P), r = it % (P * P);
+    // ---- S1T: z back (items (b, a)) -> y[c][b][a] into the x stage (dense)
+    FOR_ITEMS(it, NE * P2, NT, tid) {
+      const int el = it / P2, r = it % P2;
       const double* t1 = W + el * EB + r;
-      double SE[H], SO[PH], ye[P];
+      double SE[H], SO[PH], y[P];
       zero(SE);
       zero(SO);
 #pragma unroll
       for (int t = 0; t < HQ; ++t) {
         if ((Q & 1) && t == QH)
-          eo_acc_mid<1, P>(T.BE, T.BO, t, zo, t1[t * S1], SE, SO);
+          eo_acc_mid<1, P>(T.BE, T.BO, t, zo, t1[t * R1], SE, SO);
         else
-          eo_acc<1, P>(T.BE, T.BO, t, zo, t1[t * S1], t1[(Q - 1 - t) * S1], SE, SO);
+          eo_acc<1, P>(T.BE, T.BO, t, zo, t1[t * R1], t1[(Q - 1 - t) * R1], SE, SO);
       }
-      eo_join<P>(SE, SO, ye);
-      double* yo = W + el * EB + T1M + r;
+      eo_join<P>(SE, SO, y);
+      double* yo = X + el * P3 + r;
 #pragma unroll
-      for (int a = 0; a < P; ++a) yo[XS * a] = ye[a];
+      for (int c = 0; c < P; ++c) yo[c * P2] = y[c];
     }
     cta_sync();
-    // ---- y: coalesced stores of the batch's contiguous E-vector range
-    {
+    // ---- y: one bulk store of the batch's contiguous E-vector range
+    if (threadIdx.x == 0) {
       const long long e0 = bk * NE;
-      const long long lim = (A.E - e0 < NE ? A.E - e0 : NE) * C::P3;
-      for (int i = tid; i < lim; i += NT) {
-        const int el = i / C::P3, g = i - el * C::P3;
-        const int a = g % P, b = (g / P) % P, c = g / C::P2;
-        A.y[e0 * C::P3 + i] = W[el * EB + T1M + a * XS + b * P + c];
-      }
+      const long long ny = (A.E - e0 < NE ? A.E - e0 : NE) * P3;
+      if (ny & 1) A.y[e0 * P3 + ny - 1] = X[ny - 1];
+      fence_proxy_async();
+      if (ny > 1) bulk_s2g(A.y + e0 * P3, X, (unsigned)((ny & ~1LL) * 8));
     }
   }
+  if (threadIdx.x == 0) bulk_wait_all();
 }
 
 // Per-P1 batch shapes (elements per batch, threads): stage-3 items NE*Q^2 <= NT,

@@ -831,10 +831,11 @@ __device__ __forceinline__ double ld_dp(const double* ptr, unsigned long long po
   }
 }
 
-// Per-P1 stage layout (HOFEM_SIMT_T2QX = -1).  Measured (gpurun_out/r2h,
-// profiles/ab/r2h_ab_layout.txt, brick-kernel ms at 30M dofs): qx-fastest T2 wins
-// at P1 = 3 (BP3 -4 %, BP5 -6 %) and P1 = 6 (p=5: BP3 -2.7 %, BP5 -5 %), loses
-// at P1 = 5 (BP3 +2.5 %, BP5 +8 %), ~neutral at P1 = 7, 9 (old kept).
+// Per-P1 stage layout (HOFEM_SIMT_T2QX = -1).  Measured (gpurun_out/r2h, r2i;
+// profiles/ab/r2h_ab_layout.txt, r2i_ab_layout2.txt; brick-kernel ms at 30M
+// dofs): qx-fastest T2 wins at P1 = 2 (BP3 -2.7 %), 3 (BP3 -4 %, BP5 -6 %),
+// 4 (BP3 -5 %), 6 (p=5: BP3 -2.7 %, BP5 -5 %) and 8 (p=7: BP3 -12 %, BP5 -6 %);
+// loses at P1 = 5 (BP3 +2.5 %, BP5 +8 %); ~neutral at P1 = 7, 9 (old kept).
 template <int P1>
 constexpr bool simt_t2qx() {
   return HOFEM_SIMT_T2QX >= 0 ? HOFEM_SIMT_T2QX != 0 : (P1 == 3 || P1 == 6 || P1 == 2 || P1 == 4 || P1 == 8);
