@@ -43,6 +43,17 @@ struct LayoutDG {  // generic fallback (odd row strides)
   static constexpr int R1 = P1 * P1, PP = (P1 % 2) ? P1 : P1 + 1, R2 = Q * PP, PAD = 0;
 };
 
+// Searched (fewest 64-bit shared-memory bank conflicts over the stage access
+// patterns, 16-lane phases; at most 2-way) for the default batch sizes:
+template <> struct LayoutDG<2, 16> { static constexpr int Q = 3, R1 = 10, PP = 3, R2 = 10, PAD = 2; };
+template <> struct LayoutDG<3, 8> { static constexpr int Q = 4, R1 = 19, PP = 4, R2 = 19, PAD = 4; };
+template <> struct LayoutDG<4, 4> { static constexpr int Q = 5, R1 = 28, PP = 5, R2 = 28, PAD = 4; };
+template <> struct LayoutDG<5, 4> { static constexpr int Q = 6, R1 = 37, PP = 6, R2 = 37, PAD = 2; };
+template <> struct LayoutDG<6, 2> { static constexpr int Q = 7, R1 = 38, PP = 7, R2 = 54, PAD = 6; };
+template <> struct LayoutDG<7, 2> { static constexpr int Q = 8, R1 = 55, PP = 10, R2 = 87, PAD = 8; };
+template <> struct LayoutDG<8, 2> { static constexpr int Q = 9, R1 = 72, PP = 9, R2 = 88, PAD = 8; };
+template <> struct LayoutDG<9, 2> { static constexpr int Q = 10, R1 = 89, PP = 10, R2 = 105, PAD = 6; };
+
 template <int P1, int Q, int NE>
 struct CfgDG {
   using L = LayoutDG<P1, NE>;
