@@ -114,6 +114,20 @@ hofem_status hofem_mesh_info_get(const void* mesh, hofem_mesh_info* info_out);
 /* Nodal coordinates: xyz[c*n_local + l], c = 0,1,2 (device, 3*n_local FP64). */
 hofem_status hofem_mesh_coords(const void* mesh, double* xyz, void* stream);
 void hofem_mesh_destroy(void* mesh);
+/* Interface-exchange transport of a multi-rank mesh (no-op on one rank).
+ * mode 0: the communicator's collective (NCCL grouped send/recv, or the
+ * loopback copies).  mode 1: kernel-initiated puts (§2.3
+ * "GPU-initiated communication"; §8(f) f1): one small cooperative kernel per
+ * exchange writes this rank's boundary planes straight into the z neighbours'
+ * receive slots through peer pointers (CUDA IPC handles swapped over NCCL and
+ * opened with cudaIpcOpenMemHandle -- NVLink stores between GPUs; plain
+ * pointers in the loopback transport), raises their "filled" flags with a
+ * system-scope release, waits for its own, adds the received planes
+ * (Dirichlet rows re-imposed) and publishes "consumed" (double-buffered slots:
+ * a rank runs at most one exchange ahead of its neighbours).  Collective: every
+ * rank of the mesh calls it with the same mode.  Not graph-capturable (the
+ * exchange counter lives on the host). */
+hofem_status hofem_mesh_set_exchange(void* mesh, int mode, void* stream);
 
 /* ---------------------------------------------------------- operator (a2-a9) */
 typedef enum { HOFEM_MASS = 1, HOFEM_DIFFUSION = 2 } hofem_kind;

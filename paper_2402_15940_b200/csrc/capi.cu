@@ -58,6 +58,7 @@ hofem_status dalloc(T** p, long long n, const char* what) {
 
 void free_mesh(Mesh* m) {
   if (!m) return;
+  mesh_release_exchange(m);
   cudaFree(m->d_xi); cudaFree(m->d_coords);
   cudaFree(m->d_l2e); cudaFree(m->d_toff); cudaFree(m->d_tidx);
   cudaFree(m->d_partials); cudaFree(m->d_counter); cudaFree(m->d_scalars);

@@ -84,6 +84,17 @@ struct Mesh {
   double* d_scalars = nullptr;              // scratch scalars
   double* d_recv = nullptr;                 // 2 planes for the interface exchange
   double* d_send = nullptr;                 // 2 planes staging (copies of own planes)
+  // kernel-initiated exchange (hofem_mesh_set_exchange, comm.cu): the
+  // neighbours write their planes straight into d_xrecv (2 parities x [lo|hi])
+  // and raise d_xflag[lo|hi]; d_xflag[2] counts the exchanges this rank has
+  // consumed (read by the neighbours before reusing a parity slot)
+  int xmode = 0;                            // 0 collective (NCCL / loopback copies), 1 peer puts
+  double* d_xrecv = nullptr;                // 4 planes
+  unsigned long long* d_xflag = nullptr;    // [lo filled, hi filled, consumed, arrivals]
+  double* peer_recv[2] = {nullptr, nullptr};               // lower / upper neighbour's d_xrecv
+  unsigned long long* peer_flag[2] = {nullptr, nullptr};   // lower / upper neighbour's d_xflag
+  bool peer_ipc[2] = {false, false};        // opened with cudaIpcOpenMemHandle
+  unsigned long long xseq = 0;              // exchanges issued
 };
 
 // Grid-wide barrier state of a cooperative launch: arrival count and
@@ -208,6 +219,10 @@ bool fused_supported(const Op* op);
 // ---- comm (comm.cu): sum duplicated interface planes, fix BC there
 hofem_status exchange_planes(Op* op, const double* x, double* y, cudaStream_t s);
 hofem_status exchange_planes_bc(Op* op, const double* x, double* y, int bcmode, cudaStream_t s);
+// switch a multi-rank mesh to the kernel-initiated exchange (collective: every
+// rank of the mesh calls it); comm.cu
+hofem_status mesh_set_exchange(Mesh* m, int mode, cudaStream_t s);
+void mesh_release_exchange(Mesh* m);
 hofem_status allreduce_sum(Mesh* m, double* d_val, int count, cudaStream_t s);
 
 // ---- vector kernels (cg.cu)

@@ -91,6 +91,7 @@ SIGNATURES = {
     "hofem_mesh_info_get": (_I, [_V, ctypes.POINTER(MeshInfo)]),
     "hofem_mesh_coords": (_I, [_V, _V, _V]),
     "hofem_mesh_destroy": (None, [_V]),
+    "hofem_mesh_set_exchange": (_I, [_V, _I, _V]),
     "hofem_op_create": (_I, [_V, _I, _I, _I, _I, _V, _PV]),
     "hofem_op_apply": (_I, [_V, _V, _V, _V]),
     "hofem_op_apply_unfused": (_I, [_V, _V, _V, _V]),
@@ -273,6 +274,11 @@ class Mesh:
         _check(lib().hofem_fill_random(self.handle, ctypes.c_ulonglong(seed), _ptr(out, self.n_local),
                                        _stream(stream)))
         return out
+
+    def set_exchange(self, mode: int, stream=None):
+        """Interface exchange: 0 collective (NCCL / loopback copies), 1 kernel-
+        initiated peer puts (collective call)."""
+        _check(lib().hofem_mesh_set_exchange(self.handle, int(mode), _stream(stream)))
 
     def dot(self, a: torch.Tensor, b: torch.Tensor, stream=None) -> float:
         v = ctypes.c_double()

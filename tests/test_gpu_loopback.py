@@ -4,7 +4,10 @@ R = 2, 3 ranks as host threads with the in-process loopback transport
 stream, drive comm.cu's plane exchange (with Dirichlet re-imposition on the
 interface planes), the owned-dof dot products / allreduce, the fused kernel's
 owned-dof p.Ap and the multi-rank CG -- compared with the GLOBAL single-mesh
-oracle."""
+oracle.  Both exchange transports: the collective (loopback copies standing
+in for NCCL) and the kernel-initiated peer puts (hofem_mesh_set_exchange).
+The peer-put exchange is also hammered by many back-to-back applies without
+any other collective in between (run-ahead bounded by the consumed flags)."""
 import threading
 
 import numpy as np
@@ -69,8 +72,9 @@ CFG = [(2, "bp3", 3, (3, 2, 4), 1), (3, "bp3", 2, (4, 3, 6), 1), (2, "bp1", 4, (
 KINDS = {"bp1": (1, 1), "bp3": (2, 1), "bp5": (2, 2)}
 
 
+@pytest.mark.parametrize("xmode", [0, 1])
 @pytest.mark.parametrize("R,bench,p,dims,bc", CFG)
-def test_loopback_apply_rhs_dot_match_global(hf, R, bench, p, dims, bc):
+def test_loopback_apply_rhs_dot_match_global(hf, R, bench, p, dims, bc, xmode):
     kind, rule = KINDS[bench]
     nx, ny, nz = dims
     nzl = nz // R
@@ -78,6 +82,7 @@ def test_loopback_apply_rhs_dot_match_global(hf, R, bench, p, dims, bc):
 
     def fn(r, comm, s):
         m = hf.Mesh(nx, ny, nz, p, alpha=0.1, comm=comm, stream=s)
+        m.set_exchange(xmode, stream=s)
         op = hf.Operator(m, kind=kind, rule=rule, bc=bc, stream=s)
         x = m.random(5, stream=s)
         y = op.apply(x, stream=s)
@@ -114,8 +119,9 @@ def test_loopback_apply_rhs_dot_match_global(hf, R, bench, p, dims, bc):
     assert abs(res[0]["xx"] - float(xg @ xg)) <= 1e-12 * float(xg @ xg)
 
 
+@pytest.mark.parametrize("xmode", [0, 1])
 @pytest.mark.parametrize("R,bench,p,dims", [(2, "bp3", 3, (3, 2, 4)), (3, "bp3", 2, (3, 3, 6))])
-def test_loopback_cg_iterates_match_global(hf, R, bench, p, dims):
+def test_loopback_cg_iterates_match_global(hf, R, bench, p, dims, xmode):
     """Multi-rank CG (separate vector kernels, NCCL-path scalars via the loopback
     allreduce) against the global oracle CG iterates."""
     kind, rule = KINDS[bench]
@@ -131,6 +137,7 @@ def test_loopback_cg_iterates_match_global(hf, R, bench, p, dims):
 
     def fn(r, comm, s):
         m = hf.Mesh(nx, ny, nz, p, alpha=0.1, comm=comm, stream=s)
+        m.set_exchange(xmode, stream=s)
         op = hf.Operator(m, kind=kind, rule=rule, bc=1, stream=s)
         b = op.rhs(stream=s)
         out = {}
@@ -150,3 +157,26 @@ def test_loopback_cg_iterates_match_global(hf, R, bench, p, dims):
         st_r, it_r, x_r = res[r]["conv"]
         assert st_r == 0 and abs(it_r - kconv) <= 2
         assert rel(x_r, slab(xo, plane, p, nzl, r)) <= 1e-11
+
+
+def test_loopback_peer_puts_back_to_back(hf):
+    """30 applies per rank with no collective between them: the double-buffered
+    receive slots and the consumed counters keep a fast rank from overwriting a
+    slot its neighbour has not added yet; every result equals the collective
+    transport's bit for bit (both sum a + b on each plane)."""
+    R, p, dims = 3, 3, (3, 2, 6)
+
+    def fn(r, comm, s):
+        m = hf.Mesh(*dims, p, alpha=0.1, comm=comm, stream=s)
+        op = hf.Operator(m, kind=hf.DIFFUSION, rule=hf.GAUSS, bc=1, stream=s)
+        x = m.random(3, stream=s)
+        ref = host(op.apply(x, stream=s))
+        m.set_exchange(1, stream=s)
+        ys = [op.apply(x, stream=s) for _ in range(30)]
+        s.synchronize()
+        return ref, [host(y) for y in ys]
+
+    res = run_ranks(hf, R, fn)
+    for ref, ys in res:
+        for y in ys:
+            assert np.array_equal(y.view(np.uint64), ref.view(np.uint64))
