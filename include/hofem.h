@@ -126,7 +126,11 @@ void hofem_mesh_destroy(void* mesh);
  * (Dirichlet rows re-imposed) and publishes "consumed" (double-buffered slots:
  * a rank runs at most one exchange ahead of its neighbours).  Collective: every
  * rank of the mesh calls it with the same mode.  Not graph-capturable (the
- * exchange counter lives on the host). */
+ * exchange counter lives on the host).  With the loopback transport (all ranks
+ * on ONE device) a rank's thread must not synchronize the whole device
+ * (cudaDeviceSynchronize, cudaFree, torch.cuda.synchronize) between exchanges:
+ * it would wait on a neighbour's put kernel that waits on this rank -- use
+ * stream synchronization; the library itself allocates stream-ordered. */
 hofem_status hofem_mesh_set_exchange(void* mesh, int mode, void* stream);
 
 /* ---------------------------------------------------------- operator (a2-a9) */

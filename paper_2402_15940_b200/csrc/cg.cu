@@ -302,19 +302,21 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
   const long long n = m->n_local, no = m->n_owned;
   if (max_iter < 0) { set_error("hofem_cg: max_iter < 0"); return HOFEM_ERR_ARG; }
   if (check_every < 1) check_every = 1;
+  // stream-ordered allocations: no implicit device synchronization (a rank of
+  // the loopback transport must never wait on another rank's pending kernels)
   if (!op->d_r) {
-    if (cudaMalloc(&op->d_r, sizeof(double) * n) != cudaSuccess ||
-        cudaMalloc(&op->d_p, sizeof(double) * n) != cudaSuccess ||
-        cudaMalloc(&op->d_Ap, sizeof(double) * n) != cudaSuccess) {
+    if (cudaMallocAsync(&op->d_r, sizeof(double) * n, s) != cudaSuccess ||
+        cudaMallocAsync(&op->d_p, sizeof(double) * n, s) != cudaSuccess ||
+        cudaMallocAsync(&op->d_Ap, sizeof(double) * n, s) != cudaSuccess) {
       cudaGetLastError();
       set_error("hofem_cg: out of device memory for work vectors");
       return HOFEM_ERR_OOM;
     }
   }
   if (op->cg_cap < max_iter + 1) {
-    if (op->d_cg) cudaFree(op->d_cg);
+    if (op->d_cg) HOFEM_CUDA(cudaFreeAsync(op->d_cg, s));
     op->d_cg = nullptr;
-    HOFEM_CUDA(cudaMalloc(&op->d_cg, sizeof(double) * (max_iter + 1 + 8)));
+    HOFEM_CUDA(cudaMallocAsync(&op->d_cg, sizeof(double) * (max_iter + 1 + 8), s));
     op->cg_cap = max_iter + 1;
   }
   double* rr = op->d_cg;                  // rr[k], k = 0..max_iter
@@ -381,8 +383,8 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
         per > 0) {
       ugrid = std::min(per * num_sms(), kDotBlocks);
       if (!op->d_bar) {
-        if (cudaMalloc(&op->d_bar, sizeof(GridBar)) != cudaSuccess ||
-            cudaMemset(op->d_bar, 0, sizeof(GridBar)) != cudaSuccess) {
+        if (cudaMallocAsync(&op->d_bar, sizeof(GridBar), s) != cudaSuccess ||
+            cudaMemsetAsync(op->d_bar, 0, sizeof(GridBar), s) != cudaSuccess) {
           cudaGetLastError();
           op->d_bar = nullptr;
           ugrid = 0;

@@ -187,8 +187,8 @@ hofem_status mesh_set_exchange(Mesh* m, int mode, cudaStream_t s) {
       set_error("hofem_mesh_set_exchange: out of device memory");
       return HOFEM_ERR_OOM;
     }
-    HOFEM_CUDA(cudaMemset(m->d_xflag, 0, sizeof(unsigned long long) * 8));
-    HOFEM_CUDA(cudaDeviceSynchronize());
+    HOFEM_CUDA(cudaMemsetAsync(m->d_xflag, 0, sizeof(unsigned long long) * 8, s));
+    HOFEM_CUDA(cudaStreamSynchronize(s));
   }
   if (LoopGroup* g = m->comm->loop) {
     g->xrecv[r] = m->d_xrecv;

@@ -188,13 +188,16 @@ struct Prepared {
   bool need_fix = false, zero_y = false;
 };
 
+// Stream-ordered (re)allocation of operator scratch: no implicit device
+// synchronization, so a rank of the loopback transport never waits on another
+// rank's pending kernels.
 template <class T>
-hofem_status grow(T** p, long long* len, long long need, const char* what) {
+hofem_status grow(T** p, long long* len, long long need, const char* what, cudaStream_t s) {
   if (*len >= need) return HOFEM_OK;
-  if (*p) cudaFree(*p);
+  if (*p) cudaFreeAsync(*p, s);
   *p = nullptr;
   *len = 0;
-  if (cudaMalloc(p, sizeof(T) * need) != cudaSuccess) {
+  if (cudaMallocAsync(p, sizeof(T) * need, s) != cudaSuccess) {
     cudaGetLastError();
     set_error("fused apply: out of device memory for %s", what);
     return HOFEM_ERR_OOM;
@@ -203,10 +206,10 @@ hofem_status grow(T** p, long long* len, long long need, const char* what) {
   return HOFEM_OK;
 }
 
-hofem_status ensure_bar(Op* op) {
+hofem_status ensure_bar(Op* op, cudaStream_t s) {
   if (op->d_bar) return HOFEM_OK;
-  if (cudaMalloc(&op->d_bar, sizeof(GridBar)) != cudaSuccess ||
-      cudaMemset(op->d_bar, 0, sizeof(GridBar)) != cudaSuccess) {
+  if (cudaMallocAsync(&op->d_bar, sizeof(GridBar), s) != cudaSuccess ||
+      cudaMemsetAsync(op->d_bar, 0, sizeof(GridBar), s) != cudaSuccess) {
     cudaGetLastError();
     op->d_bar = nullptr;
     set_error("fused apply: out of device memory for the grid barrier");
@@ -216,7 +219,7 @@ hofem_status ensure_bar(Op* op) {
 }
 
 hofem_status prepare(Op* op, const double* x, double* y, bool fdot, Prepared* out,
-                     bool for_cg = false) {
+                     cudaStream_t s, bool for_cg = false) {
   Mesh* m = op->mesh;
   const int p = m->p;
   Prepared& R = *out;
@@ -224,7 +227,7 @@ hofem_status prepare(Op* op, const double* x, double* y, bool fdot, Prepared* ou
   const Plan& PL = R.PL;
   const FusedLaunch L = PL.L;
   HOFEM_TRY(grow(&op->d_bbuf, &op->bbuf_len, PL.nbricks * L.face_block,
-                 "the brick-interface buffer"));
+                 "the brick-interface buffer", s));
   ColArgs& A = R.A;
   A = ColArgs{};
   A.x = x; A.y = y; A.qd = op->d_qdata; A.bbuf = op->d_bbuf;
@@ -246,7 +249,7 @@ hofem_status prepare(Op* op, const double* x, double* y, bool fdot, Prepared* ou
   }
   R.need_fix = R.nfixp > 0;
   R.nfixb = R.need_fix ? (R.nfixp + 255) / 256 : 0;
-  if (fdot) HOFEM_TRY(grow(&op->d_dotp, &op->dotp_len, PL.grid + R.nfixb, "the dot partials"));
+  if (fdot) HOFEM_TRY(grow(&op->d_dotp, &op->dotp_len, PL.grid + R.nfixb, "the dot partials", s));
   A.dotp = fdot ? op->d_dotp : nullptr;
   A.kown = m->n_owned / (m->Nx * m->Ny);
   FixArgs F;
@@ -309,7 +312,7 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
   Mesh* m = op->mesh;
   const bool fdot = dot_out != nullptr;
   Prepared R;
-  HOFEM_TRY(prepare(op, x, y, fdot, &R));
+  HOFEM_TRY(prepare(op, x, y, fdot, &R, s));
   const Plan& PL = R.PL;
   if (PL.nbricks == 0) return HOFEM_OK;
   ColArgs& A = R.A;
@@ -320,7 +323,7 @@ hofem_status apply_fused(Op* op, const double* x, double* y, cudaStream_t s,
   const bool loopback = m->nranks > 1 && m->comm && m->comm->loop;
   bool infix = R.need_fix && !loopback &&
                (op->opt_infix == 2 || (op->opt_infix == 1 && R.npts <= (8LL << 20)));
-  if (infix) HOFEM_TRY(ensure_bar(op));
+  if (infix) HOFEM_TRY(ensure_bar(op, s));
   A.infix = infix ? 1 : 0;
   A.bar = op->d_bar;
   // with infix the zeroing of y moves into the kernel too (first barrier)
@@ -392,10 +395,10 @@ hofem_status cg_persistent(Op* op, double* x, double* r, double* p, double* Ap, 
     return HOFEM_ERR_ARG;
   }
   Prepared R;
-  HOFEM_TRY(prepare(op, p, Ap, false, &R, true));
+  HOFEM_TRY(prepare(op, p, Ap, false, &R, s, true));
   const Plan& PL = R.PL;
-  HOFEM_TRY(ensure_bar(op));
-  HOFEM_TRY(grow(&op->d_cgparts, &op->cgparts_len, 2LL * PL.grid, "the CG partials"));
+  HOFEM_TRY(ensure_bar(op, s));
+  HOFEM_TRY(grow(&op->d_cgparts, &op->cgparts_len, 2LL * PL.grid, "the CG partials", s));
   ColArgs& A = R.A;
   A.infix = 1;
   A.zero_n = 0;  // the CG kernel zeroes Ap itself

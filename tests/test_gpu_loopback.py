@@ -55,7 +55,8 @@ def run_ranks(hf, R, fn):
 
 
 def host(t):
-    torch.cuda.synchronize()
+    # stream-local copy (the current stream is the rank's): never a device-wide
+    # synchronization, which would wait on another rank's pending put kernel
     return t.detach().cpu().numpy()
 
 
