@@ -128,10 +128,14 @@ int num_sms() {
 // Split each column into chunks so that the units fill the persistent grid in
 // as few, as full, rounds as possible (fewer chunks on ties: each chunk boundary
 // is a plane the fix-up kernel has to sum).
+#ifndef HOFEM_CHUNKS_MIN
+#define HOFEM_CHUNKS_MIN 1  // tuning knob: at least this many z chunks per column
+#endif
 void choose_chunks(long long ncol, int nzl, int G, int* zc_out, int* nchunks_out) {
   double best = -1.0;
   int bz = nzl, bn = 1;
-  for (int want = 1; want <= 16 && want <= nzl; ++want) {
+  for (int want = HOFEM_CHUNKS_MIN < nzl ? HOFEM_CHUNKS_MIN : nzl; want <= 16 && want <= nzl;
+       ++want) {
     const int zc = (nzl + want - 1) / want, nch = (nzl + zc - 1) / zc;
     const long long units = ncol * nch;
     const long long rounds = (units + G - 1) / G;

@@ -20,12 +20,15 @@ name, p1, flags = args[0], int(args[1]), args[2:]
 B.build()
 os.makedirs("scratch/obj", exist_ok=True)
 src = os.path.join(B.CSRC, f"{unit}.cu")
-obj = os.path.abspath(f"scratch/obj/{unit}{p1}_{name}.o")
-cmd = [B.NVCC] + B._common_flags() + [f"-DHOFEM_P1={p1}"] + flags + ["-c", src, "-o", obj]
+per_p1 = unit.endswith("_p")  # per-P1 units get -DHOFEM_P1; host units (e.g. fused) do not
+obj = os.path.abspath(f"scratch/obj/{unit}{p1 if per_p1 else ''}_{name}.o")
+cmd = [B.NVCC] + B._common_flags() + ([f"-DHOFEM_P1={p1}"] if per_p1 else []) + flags + [
+    "-c", src, "-o", obj]
 r = subprocess.run(cmd, capture_output=True, text=True)
 if r.returncode:
     sys.exit(r.stderr)
-objs = [obj if os.path.basename(j[1]) == f"{unit}{p1}.o" else j[1] for j in B._jobs()]
+target = f"{unit}{p1}.o" if per_p1 else f"{unit}.o"
+objs = [obj if os.path.basename(j[1]) == target else j[1] for j in B._jobs()]
 nccl = B._nccl_dir()
 out = os.path.abspath(f"scratch/libhofem_{name}.so")
 cmd = [B.NVCC] + B.ARCH + ["-shared", "-o", out] + objs + [
