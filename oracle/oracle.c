@@ -25,6 +25,15 @@
  *     the EA form by tests/test_oracle_pins.py.
  *   - CG: textbook unpreconditioned Hestenes-Stiefel (§2.1 "Krylov
  *     subspace method").
+ *   - §8(f) f4, DG (L2) mass: element matrices
+ *     M_e = sum_q W detJ psi_a psi_b with the Gauss-Legendre-nodal basis (reading
+ *     R16) by brute-force quadrature; the operator is block diagonal.
+ *   - §8(f) f2, p-multigrid pieces: the assembled
+ *     diagonal sum_e R_e^T diag(A_e), prolongation by evaluating the coarse
+ *     element function at the fine nodes (owner element, product formula),
+ *     restriction as its exact transpose, Chebyshev acceleration of Jacobi step
+ *     by step (Saad, Alg. 12.1) and power iteration (readings R17-R18); the
+ *     V-cycle and PCG are composed in oracle/__init__.py in the algorithm's order.
  *   - Readings for everything the paper leaves open (reference element [0,1]^3,
  *     quadrature rules, ordering, the deformation Phi, BCs, RHS) are SURVEY.md
  *     §8(c) R1-R14, restated in DESIGN.md §3.
