@@ -835,10 +835,12 @@ __device__ __forceinline__ double ld_dp(const double* ptr, unsigned long long po
 // profiles/ab/r2h_ab_layout.txt, r2i_ab_layout2.txt; brick-kernel ms at 30M
 // dofs): qx-fastest T2 wins at P1 = 2 (BP3 -2.7 %), 3 (BP3 -4 %, BP5 -6 %),
 // 4 (BP3 -5 %), 6 (p=5: BP3 -2.7 %, BP5 -5 %) and 8 (p=7: BP3 -12 %, BP5 -6 %);
-// loses at P1 = 5 (BP3 +2.5 %, BP5 +8 %); ~neutral at P1 = 7, 9 (old kept).
+// loses at P1 = 5 (BP3 +2.5 %, BP5 +8 %); at P1 = 7 BP3 even, BP5 -1.3 % (r2m);
+// ~neutral at P1 = 9 (old kept).
 template <int P1>
 constexpr bool simt_t2qx() {
-  return HOFEM_SIMT_T2QX >= 0 ? HOFEM_SIMT_T2QX != 0 : (P1 == 3 || P1 == 6 || P1 == 2 || P1 == 4 || P1 == 8);
+  return HOFEM_SIMT_T2QX >= 0 ? HOFEM_SIMT_T2QX != 0
+                              : (P1 == 2 || P1 == 3 || P1 == 4 || P1 == 6 || P1 == 7 || P1 == 8);
 }
 
 template <int KIND, int P1, int Q, int BX, int BY>
@@ -1050,9 +1052,14 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
   constexpr int HQ = (Q + 1) / 2, NCD = KIND == KIND_MASS ? 1 : 6;
   // measured (gpurun_out/e4, e5, e8): register hoist helps at p = 6, 7 (3-4 %), costs
   // at p = 4, 5 (register cap 128); deeper rings and L1 prefetch do not help
-  constexpr int LA0 = HOFEM_EO_DLA > 0 ? HOFEM_EO_DLA : 1;
+  // measured (gpurun_out/r2m, profiles/ab/r2m_ab_knobs.txt): two pairs in flight
+  // at P1 = 6 (BP3 -1.8 %, BP5 -3.1 %); the hoist also pays for collocated BP5 at
+  // P1 = 6 (-6.4 %) but not for BP3 there (+14 %)
+  constexpr int LA0 = HOFEM_EO_DLA > 0 ? HOFEM_EO_DLA : (P1 == 6 ? 2 : 1);
   constexpr int LA = LA0 < HQ ? LA0 : HQ;
-  constexpr int PRE = HOFEM_EO_PRE >= 0 ? HOFEM_EO_PRE : (P1 == 7 || P1 == 8 ? 1 : 0);
+  constexpr int PRE = HOFEM_EO_PRE >= 0
+                          ? HOFEM_EO_PRE
+                          : (P1 == 7 || P1 == 8 || (P1 == 6 && KIND == KIND_COLLOC) ? 1 : 0);
   constexpr bool EOPRE = EO && !C::DSM && PRE == 1;
   constexpr bool EOPF1 = EO && !C::DSM && PRE == 2;  // L1 prefetch instead
   // COLLOC (BP5): GLL points = nodes, so B = I; every B contraction is the
