@@ -1052,10 +1052,12 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
   constexpr int HQ = (Q + 1) / 2, NCD = KIND == KIND_MASS ? 1 : 6;
   // measured (gpurun_out/e4, e5, e8): register hoist helps at p = 6, 7 (3-4 %), costs
   // at p = 4, 5 (register cap 128); deeper rings and L1 prefetch do not help
-  // measured (gpurun_out/r2m, profiles/ab/r2m_ab_knobs.txt): two pairs in flight
-  // at P1 = 6 (BP3 -1.8 %, BP5 -3.1 %); the hoist also pays for collocated BP5 at
-  // P1 = 6 (-6.4 %) but not for BP3 there (+14 %)
-  constexpr int LA0 = HOFEM_EO_DLA > 0 ? HOFEM_EO_DLA : (P1 == 6 ? 2 : 1);
+  // measured (gpurun_out/r2m, r2n; profiles/ab/r2m_ab_knobs.txt, r2n_ab_p6.txt):
+  // two pairs in flight at P1 = 6 (BP3 -1.8 %, BP5 -3.1 %); the first-pair hoist
+  // pays more for collocated BP5 at P1 = 6 (-6.4 %) but not with two pairs in
+  // flight (+5.6 %), and not for BP3 (+14 %)
+  constexpr int LA0 =
+      HOFEM_EO_DLA > 0 ? HOFEM_EO_DLA : (P1 == 6 && KIND != KIND_COLLOC ? 2 : 1);
   constexpr int LA = LA0 < HQ ? LA0 : HQ;
   constexpr int PRE = HOFEM_EO_PRE >= 0
                           ? HOFEM_EO_PRE
