@@ -1,4 +1,6 @@
-"""Host-side z-slab partition logic (reading R9).
+"""TEST INFRASTRUCTURE: a Python mirror of the host-side z-slab partition logic
+(reading R9) for the gloo multi-rank tests on CPU; the product
+path is csrc/comm.cu (exercised on the GPU by tests/test_gpu_loopback.py).
 
 Mirrors what ``hofem_mesh_create`` (capi.cu) and ``exchange_planes`` (comm.cu)
 do for the multi-GPU path, in plain Python over ``torch.distributed`` so the

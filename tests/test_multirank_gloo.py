@@ -2,7 +2,7 @@
 ownership, the interface-plane exchange and the allreduced dot products
 reproduce the global operator.  Per-slab local operators come from the oracle's
 window mode (elements of the slab only); the exchange is
-paper_2402_15940_b200.partition.exchange_planes, the same logic comm.cu
+tests/partition_mirror.py (exchange_planes), the same logic comm.cu
 implements with NCCL."""
 import os
 import socket
@@ -15,7 +15,7 @@ import torch.multiprocessing as mp
 
 import oracle as O
 import workloads as W
-from paper_2402_15940_b200 import partition
+from tests import partition_mirror as partition
 
 
 def _free_port():
