@@ -13,6 +13,10 @@ $NCU --metrics gpu__time_duration.sum -c 400 --csv --log-file $out/launches.csv 
     python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --no-sweep > $out/launch_run.log 2>&1
 FULL="$NCU --set full --import-source on -c 1"
 $FULL -k regex:fused_elem -o $out/simt_p5_200x200x25 python scripts/prof_apply.py --p 5 --slab 200,200,25 > /dev/null 2>&1
+$FULL -k regex:fused_elem -o $out/simt_p5 python scripts/prof_apply.py --p 5 > /dev/null 2>&1
+$FULL -k regex:fused_elem -o $out/simt_p4 python scripts/prof_apply.py --p 4 > /dev/null 2>&1
+$FULL -k regex:fused_elem -o $out/simt_p6 python scripts/prof_apply.py --p 6 > /dev/null 2>&1
+$FULL -k regex:fused_elem -o $out/bp5_p5 python scripts/prof_apply.py --bench bp5 --p 5 > /dev/null 2>&1
 $FULL -k regex:fused_elem -o $out/simt_p7 python scripts/prof_apply.py --p 7 > /dev/null 2>&1
 $FULL -k regex:fused_elem -o $out/simt_p8 python scripts/prof_apply.py --p 8 > /dev/null 2>&1
 $FULL -k regex:fused_elem -o $out/bp1_p5 python scripts/prof_apply.py --bench bp1 --p 5 > /dev/null 2>&1
