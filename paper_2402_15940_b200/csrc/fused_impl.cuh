@@ -1059,9 +1059,11 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
   constexpr int LA0 =
       HOFEM_EO_DLA > 0 ? HOFEM_EO_DLA : (P1 == 6 && KIND != KIND_COLLOC ? 2 : 1);
   constexpr int LA = LA0 < HQ ? LA0 : HQ;
+  // (P1 = 8: the hoist won with round 1's layout; with the searched layout it
+  // costs BP3 p=7 6.3 % and BP5 1.5 %, r2o -- off)
   constexpr int PRE = HOFEM_EO_PRE >= 0
                           ? HOFEM_EO_PRE
-                          : (P1 == 7 || P1 == 8 || (P1 == 6 && KIND == KIND_COLLOC) ? 1 : 0);
+                          : (P1 == 7 || (P1 == 6 && KIND == KIND_COLLOC) ? 1 : 0);
   constexpr bool EOPRE = EO && !C::DSM && PRE == 1;
   constexpr bool EOPF1 = EO && !C::DSM && PRE == 2;  // L1 prefetch instead
   // COLLOC (BP5): GLL points = nodes, so B = I; every B contraction is the
