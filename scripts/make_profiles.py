@@ -19,9 +19,9 @@ def run(cmd):
     return subprocess.run(cmd, capture_output=True, text=True).stdout
 
 
-def main(tag):
+def main(tag, dst=None):
     src = os.path.join(ROOT, "gpurun_out", tag)
-    dst = os.path.join(ROOT, "profiles")
+    dst = dst or os.path.join(ROOT, "profiles")
     os.makedirs(dst, exist_ok=True)
     if os.path.exists(os.path.join(src, "launches.csv")):
         shutil.copy(os.path.join(src, "launches.csv"), os.path.join(dst, f"{tag}_launches.csv"))
@@ -65,4 +65,12 @@ def main(tag):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    # usage: make_profiles.py <tag> [--out DIR]  (DIR: e.g. gpurun_out/<tag>/profiles on
+    # the GPU box, so only the small summaries travel back)
+    out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
+    if out:
+        os.makedirs(out, exist_ok=True)
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            shutil.copy(tp, os.path.join(out, "traffic.json"))
+    main(sys.argv[1], out)
