@@ -416,7 +416,7 @@ template <int P1>
 struct ShapeMFD;
 template <> struct ShapeMFD<2> { static constexpr int NE = 8, NT = 96; };
 template <> struct ShapeMFD<3> { static constexpr int NE = 4, NT = 64; };
-template <> struct ShapeMFD<4> { static constexpr int NE = 2, NT = 64; };
+template <> struct ShapeMFD<4> { static constexpr int NE = 4, NT = 128; };  // r2q: -3.6 %
 template <> struct ShapeMFD<5> { static constexpr int NE = 2, NT = 96; };
 template <> struct ShapeMFD<6> { static constexpr int NE = 1, NT = 64; };
 template <> struct ShapeMFD<7> { static constexpr int NE = 1, NT = 64; };
