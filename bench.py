@@ -13,9 +13,10 @@ e2e (host buffers through the public API), the CPU oracle baseline and -- on
 rank 0 at N = 1, time-bounded -- ``sweep``: apply GDOF/s and HBM-roofline
 fraction vs p for configs 2-4 (BP3 fused / unfused / fully matrix-free, BP5,
 BP1 eager / CUDA-graph / L2-flushed + 100-iteration CG), the DG mass operator,
-the DOFs needed to reach 80 % of peak, and BPS3 p-multigrid PCG vs CG.
+the DOFs needed to reach 80 % of peak, BPS3 p-multigrid PCG vs CG, and
+BASELINE config 4 (BP5 CG to 1e-10, p = 4..8).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--p 5] [--no-sweep] [--bp5-cg]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--p 5] [--no-sweep] [--no-bp5-cg]
     python bench.py --impl reference ...   # the CPU oracle (rank 0 only)
 
 Prints ONE JSON line on rank 0.
@@ -569,7 +570,7 @@ def run_sweep(args, hf, torch, stream):
     op.close()
     m.close()
     torch.cuda.empty_cache()
-    if getattr(args, "bp5_cg", False):
+    if not getattr(args, "no_bp5_cg", False):
         out["bp5_cg_1e-10"] = []
         for p in range(4, 9):
             n = W.bp3_sweep_n(p)
@@ -610,8 +611,8 @@ def main():
     ap.add_argument("--oracle-plan", action="store_true",
                     help="SURVEY §8(d) oracle timing plan on the host cores (no GPU work)")
     ap.add_argument("--sweep-reps", type=int, default=20)
-    ap.add_argument("--bp5-cg", action="store_true",
-                    help="sweep also runs the BP5 CG solves to 1e-10 (BASELINE config 4, ~15 s)")
+    ap.add_argument("--no-bp5-cg", action="store_true",
+                    help="skip the sweep's BP5 CG solves to 1e-10 (BASELINE config 4, ~15 s)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
