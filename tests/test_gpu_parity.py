@@ -333,6 +333,36 @@ def test_cg_iterates_small(hf, bench, p, n, mode):
     assert rel(host(x), xo) <= 1e-11
 
 
+@pytest.mark.parametrize("bench,p,n", [("bp3", 3, 4), ("bp3", 5, 3), ("bp1", 2, 4), ("bp5", 4, 3)])
+def test_cg_every_iterate_within_rounding_envelope(hf, bench, p, n):
+    """SURVEY R14 to the letter: EVERY iterate x_k, k <= min(k_conv, 200), against
+    the oracle's.  Past ||r_k||/||r_0|| ~ 1e-4 two correct CG runs drift apart by
+    rounding (loss of orthogonality), so the bound at k is max(1e-10, 1000 x the
+    oracle's own sensitivity at k): the distance between the oracle run and the
+    same run on b perturbed at the 1e-15 level (reading R14; an
+    assembled-matrix oracle run stays within 1/12 of this envelope on CPU)."""
+    kind, rule = KINDS[bench]
+    bc = 0 if bench == "bp1" else 1
+    m, op, om, kind, rule = make(hf, n, n, n, p, bench, bc=bc)
+    b = op.rhs()
+    Ae = O.element_matrices(om, kind, rule)
+    bo = O.rhs(om, kind, rule, bc=bc)
+    _, st, kconv, _, _ = O.cg(bo, m=om, Ae=Ae, bc=bc, rel_tol=1e-13, max_iter=800)
+    K = min(kconv, 200)
+    _, _, _, _, xh = O.cg(bo, m=om, Ae=Ae, bc=bc, max_iter=K, fixed_iters=True, history=True)
+    pert = 1.0 + 1e-15 * W.random_vector(99, np.arange(len(bo)))
+    _, _, _, _, xp = O.cg(bo * pert, m=om, Ae=Ae, bc=bc, max_iter=K, fixed_iters=True,
+                          history=True)
+    worst = 0.0
+    for k in range(1, K + 1):
+        x = torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
+        op.cg(b, x, max_iter=k, fixed_iters=True)
+        tol = max(1e-10, 1000.0 * rel(xp[k], xh[k]))
+        e = rel(host(x), xh[k])
+        worst = max(worst, e / tol)
+        assert e <= tol, (k, e, tol)
+
+
 @pytest.mark.parametrize("mode", list(CG_MODES))
 def test_cg_schedules_bitwise_deterministic(hf, mode):
     """Same inputs, same schedule => bitwise-identical iterate (fixed reduction
