@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(NT) dg_mass_simt(const __grid_constant__ Tab<P
     const int buf = k & 1;
     const long long nb = bk + gridDim.x;
     const int tid = vtid();
-    const int zo = (int)(bk >> 40);  // == 0, loop-variant (see cb_row in fused_impl.cuh)
+    const int zo = (int)(bk >> 40);  // == 0, loop-variant (see cdot in fused_impl.cuh)
     double* X = XS0 + buf * C::XB;
     const double* QD = QS0 + buf * C::QSL;
     if (threadIdx.x == 0 && nb < A.nbatch) {

@@ -39,12 +39,6 @@
 #ifndef HOFEM_SIMT_DSMEM
 #define HOFEM_SIMT_DSMEM -1  // SIMT: D staged in smem (1), from L2 in registers (0), per p (-1)
 #endif
-#ifndef HOFEM_SIMT_CB
-#define HOFEM_SIMT_CB -1  // SIMT tables: 1 constant bank (uniform loads), 0 shared memory, -1 per p
-#endif
-#ifndef HOFEM_SIMT_DPF
-#define HOFEM_SIMT_DPF 0  // SIMT stage 3: qz-steps of D loads in flight (0: per p, measured)
-#endif
 #ifndef HOFEM_SIMT_EO
 #define HOFEM_SIMT_EO 1  // SIMT: even-odd (symmetry-halved) 1D contractions
 #endif
@@ -873,33 +867,19 @@ struct CfgS {
   static constexpr int EB = QXF ? EB0 + ((EBD - EB0) % 16 + 16) % 16
                                 : EB0 + ((7 - EB0) % 16 + 16) % 16;  // old: == 7 (mod 16)
   static constexpr int CARRY = LX * LY;
-  static constexpr int PR = P + (P & 1);  // table row stride
   static constexpr int TOFF0 = NE * EB + 2 * LAT + 2 * CARRY;
-  static constexpr int TOFF = TOFF0 + (TOFF0 & 1);  // tables 16-byte aligned
+  static constexpr int TOFF = TOFF0 + (TOFF0 & 1);  // 16-byte aligned
   // D staged in shared memory (one buffer, bulk-copied one brick ahead) or
   // loaded from L2 into registers inside stage 3.
   static constexpr bool DSM =
       HOFEM_SIMT_DSMEM >= 0 ? HOFEM_SIMT_DSMEM != 0 : (P1 == 9);  // measured
-  static constexpr int QOFF = TOFF + 2 * Q * PR;  // even => 16-byte aligned
+  static constexpr int QOFF = TOFF;  // D stage (DSM), 16-byte aligned
   static constexpr int QSLOT = ((NC * Q * Q * Q + 2) + 1) / 2 * 2;
   static constexpr int SMEM_DOUBLES = QOFF + (DSM ? NE * QSLOT : 0);
   static constexpr int SMEM_BYTES = SMEM_DOUBLES * 8;
   static constexpr int NQ1 = Q;
   __device__ static constexpr int lat(int i, int j, int k) { return k + LZ * j + LXS * i; }
 };
-
-// One row of the shared-memory tables (B or G, row stride PR even) into
-// registers with 16-byte broadcast loads.
-template <int P, int PR>
-__device__ __forceinline__ void ld_row(const double* row, double (&r)[P]) {
-#pragma unroll
-  for (int c = 0; c + 1 < P; c += 2) {
-    const double2 v = *reinterpret_cast<const double2*>(row + c);
-    r[c] = v.x;
-    r[c + 1] = v.y;
-  }
-  if (P & 1) r[P - 1] = row[P - 1];
-}
 
 template <class C, int NT, int BX, int BY>
 __device__ __forceinline__ void simt_epilogue(const ColArgs& A, double* smem, double* CY,
@@ -912,15 +892,6 @@ __device__ __forceinline__ void simt_epilogue(const ColArgs& A, double* smem, do
       (long long)p * ex0, (long long)p * ey0, (long long)p * ez, ez == b.z0, ez + 1 == b.z1, L, dsum);
 }
 
-// Table row from the kernel-parameter constant bank.  `zo` is a loop-variant
-// uniform zero: it keeps the compiler from hoisting the 2QP table values out of
-// the persistent loop into (spilled) registers, while the loads stay uniform
-// (LDCU into uniform registers, DFMA reads them as operands).
-template <int P>
-__device__ __forceinline__ void cb_row(const double* row, int zo, double (&r)[P]) {
-#pragma unroll
-  for (int c = 0; c < P; ++c) r[c] = row[c + zo];
-}
 // ---- even-odd contractions (tables BE/BO/GE/GO of Tab, constant bank).  S is
 // the symmetry sign of the 1D matrix: +1 for B, -1 for G.
 template <int P>
@@ -1020,18 +991,6 @@ __device__ __forceinline__ void eo_ldpair(const double* qde, int t, double (&d)[
   }
 }
 
-// measured: constant-bank tables win at p = 4, 6, 7; shared-memory rows elsewhere
-template <int P1>
-constexpr bool simt_cb() {
-  return HOFEM_SIMT_CB >= 0 ? HOFEM_SIMT_CB != 0 : (P1 == 5 || P1 == 7 || P1 == 8);
-}
-#define TROW(M, q, r)                                 \
-  do {                                                \
-    if constexpr (simt_cb<P1>())                      \
-      cb_row<P>(T.M + (q) * P, zo, r);                \
-    else                                              \
-      ld_row<P, PR>(T##M##s + (q) * PR, r);           \
-  } while (0)
 
 // One pass of the brick pipeline over all of this CTA's work units: y = A x
 // (A.x -> A.y) for the CTA's bricks, edge-line partials to A.bbuf, x.y terms of
@@ -1065,7 +1024,6 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
                           ? HOFEM_EO_PRE
                           : (P1 == 7 || (P1 == 6 && KIND == KIND_COLLOC) ? 1 : 0);
   constexpr bool EOPRE = EO && !C::DSM && PRE == 1;
-  constexpr bool EOPF1 = EO && !C::DSM && PRE == 2;  // L1 prefetch instead
   // COLLOC (BP5): GLL points = nodes, so B = I; every B contraction is the
   // identity and is skipped (diffusion structure otherwise).
   constexpr bool COL = KIND == KIND_COLLOC;
@@ -1073,15 +1031,13 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
   // folded end-of-brick barrier: +1-2 % for BP1/BP3, -1.5 % for BP5
   constexpr bool ENDBAR = HOFEM_SIMT_ENDBAR >= 0 ? HOFEM_SIMT_ENDBAR != 0 : COL;
   constexpr int EB = C::EB, S1 = C::S1, T1M = C::T1M, T1SZ = C::T1SZ, SP = C::SP,
-                T2M = C::T2M, PR = C::PR, TY = C::TY, TX = C::TX, TC = C::TC;
+                T2M = C::T2M, TY = C::TY, TX = C::TX, TC = C::TC;
   (void)SP;
   extern __shared__ __align__(16) double smem[];
   double* LB = smem + NE * EB;
   double* CY = LB + 2 * C::LAT;
-  double* TBs = smem + C::TOFF;  // B[q][c], row stride PR (16-byte aligned)
-  double* TGs = TBs + Q * PR;
   double* QS = smem + C::QOFF;  // staged D of the current brick (DSM)
-  (void)TBs; (void)TGs; (void)QS; (void)CY;
+  (void)QS; (void)CY;
   Brick cur = unit_first(A, blockIdx.x);
   if (cur.u >= A.nunits) return;  // no work unit for this CTA
   if (C::DSM) {
@@ -1100,7 +1056,7 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
   for (int kb = 0; cur.u < A.nunits; ++kb) {
     const int tid = vtid();
 #if HOFEM_EO_ZO
-    const int zo = cur.ez >> 30;  // == 0, loop-variant (see cb_row)
+    const int zo = cur.ez >> 30;  // == 0, loop-variant (see eo_fwd / cdot)
 #else
     constexpr int zo = 0;  // EO tables: direct constant-bank operands
 #endif
@@ -1126,7 +1082,7 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
 #pragma unroll
       for (int a = 0; a < P; ++a) xa[a] = xl[C::LXS * a];
       double* t1 = smem + el * EB + r;
-      if constexpr (EO) {
+      {
         double e[H], o[PH];
         eo_split<P>(xa, e, o);
 #pragma unroll
@@ -1150,21 +1106,6 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
           t1[QH * S1] = COL ? xa[QH] : eo_fwd_mid<1, P>(T.BE, T.BO, QH, zo, e, o);
           if (DIFF) t1[T1M + QH * S1] = eo_fwd_mid<-1, P>(T.GE, T.GO, QH, zo, e, o);
         }
-      } else {
-#pragma unroll
-      for (int qx = 0; qx < Q; ++qx) {
-        double br[P], gr[P];
-        if (!COL) TROW(B, qx, br);
-        if (DIFF) TROW(G, qx, gr);
-        double sb = 0.0, sg = 0.0;
-#pragma unroll
-        for (int a = 0; a < P; ++a) {
-          if (!COL) sb = fma(br[a], xa[a], sb);
-          if (DIFF) sg = fma(gr[a], xa[a], sg);
-        }
-        t1[qx * S1] = COL ? xa[qx] : sb;  // B_x x (= x when collocated)
-        if (DIFF) t1[T1M + qx * S1] = sg;
-      }
       }
     }
     cta_sync();
@@ -1175,25 +1116,6 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
                                (long long)p * nxt.by * BY, (long long)p * nxt.ez);
 
     double dpre[LA][2][NCD];
-    if constexpr (EOPF1) {
-      // the first LA point pairs of this thread's stage-3 item into L1
-      if (tid < NE * Q2) {
-        const int el = tid / Q2, pt = tid % Q2;
-        const int ex = ex0 + el % BX, ey = ey0 + el / BX;
-        if (ex < A.nx && ey < A.ny) {
-          const double* qde = A.qd + (ex + (long long)A.nx * (ey + (long long)A.ny * ez)) *
-                                         (long long)(C::NC * Q3) + pt;
-#pragma unroll
-          for (int k = 0; k < LA; ++k)
-#pragma unroll
-            for (int m = 0; m < NCD; ++m) {
-              asm volatile("prefetch.global.L1 [%0];" ::"l"(qde + m * Q3 + k * Q2));
-              if (!((Q & 1) && k == QH))
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(qde + m * Q3 + (Q - 1 - k) * Q2));
-            }
-        }
-      }
-    }
     if constexpr (EOPRE) {
       if (tid < NE * Q2) {
         const int el = tid / Q2, pt = tid % Q2;
@@ -1218,7 +1140,7 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
         vg[b] = DIFF ? t1[T1M + b * P] : 0.0;
       }
       double* t2 = smem + el * EB + T1SZ + qx * TX + c * TC;
-      if constexpr (EO) {
+      {
         double eb[H], ob[PH], eg[H], og[PH];
         eo_split<P>(vb, eb, ob);
         if (DIFF && !COL) eo_split<P>(vg, eg, og);
@@ -1256,33 +1178,6 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
           if (DIFF) bg = eo_fwd_mid<-1, P>(T.GE, T.GO, QH, zo, eb, ob);
           put(QH, bb, gb, bg);
         }
-      } else {
-#pragma unroll
-      for (int qy = 0; qy < Q; ++qy) {
-        double br[P], gr[P];
-        if (!COL) TROW(B, qy, br);
-        if (DIFF) TROW(G, qy, gr);
-        double bb = 0.0, gb = 0.0, bg = 0.0;
-#pragma unroll
-        for (int b = 0; b < P; ++b) {
-          if (!COL) bb = fma(br[b], vb[b], bb);
-          if (DIFF) {
-            if (!COL) gb = fma(br[b], vg[b], gb);
-            bg = fma(gr[b], vb[b], bg);
-          }
-        }
-        if (COL) {
-          bb = vb[qy];
-          gb = vg[qy];
-        }
-        if (DIFF) {
-          t2[qy * TY] = gb;            // G_x B_y  (-> u_x)
-          t2[T2M + qy * TY] = bg;      // B_x G_y  (-> u_y)
-          t2[2 * T2M + qy * TY] = bb;  // B_x B_y  (-> u_z)
-        } else {
-          t2[qy * TY] = bb;
-        }
-      }
       }
     }
     cta_sync();
@@ -1303,7 +1198,7 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
                  : A.qd + (ex + (long long)A.nx * (ey + (long long)A.ny * ez)) *
                               (long long)(C::NC * Q3) + pt;
       double* t2 = smem + el * EB + T1SZ + (pt / Q) * TY + (pt % Q) * TX;
-      if constexpr (EO) {
+      {
         // pairs (qz = t, Q-1-t), then the middle point (odd Q); the next pair's
         // D values are loaded while this pair computes
         double dr[LA][2][NCD];
@@ -1424,93 +1319,6 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
 #pragma unroll
           for (int c = 0; c < P; ++c) t2[c * TC] = s[c];
         }
-      } else {
-      if (DIFF) {
-        // D ring: qz .. qz+DPF-1 in flight (volatile loads keep program order)
-        constexpr int DPF0 =
-            C::DSM ? 1 : (HOFEM_SIMT_DPF > 0 ? HOFEM_SIMT_DPF : (P1 >= 7 ? 2 : 1));
-        constexpr int DPF = DPF0 < Q ? DPF0 : Q;
-        double dq[DPF][6];
-#pragma unroll
-        for (int k = 0; k < DPF; ++k)
-#pragma unroll
-          for (int m = 0; m < 6; ++m) dq[k][m] = ld_d<C::DSM>(qde + m * Q3 + k * Q2);
-        double g0[P], g1[P], g2[P], s0[P], s1[P], s2[P];
-#pragma unroll
-        for (int c = 0; c < P; ++c) {
-          g0[c] = t2[c * TC];
-          g1[c] = t2[T2M + c * TC];
-          g2[c] = t2[2 * T2M + c * TC];
-          s0[c] = s1[c] = s2[c] = 0.0;
-        }
-#pragma unroll
-        for (int qz = 0; qz < Q; ++qz) {
-          double dc[6];
-#pragma unroll
-          for (int m = 0; m < 6; ++m) dc[m] = dq[qz % DPF][m];
-          if (qz + DPF < Q) {
-#pragma unroll
-            for (int m = 0; m < 6; ++m) dq[qz % DPF][m] = ld_d<C::DSM>(qde + m * Q3 + (qz + DPF) * Q2);
-          }
-          double br[P], gr[P];
-          if (!COL) TROW(B, qz, br);
-          TROW(G, qz, gr);
-          double u0 = 0.0, u1 = 0.0, u2 = 0.0;
-#pragma unroll
-          for (int c = 0; c < P; ++c) {
-            if (!COL) {
-              u0 = fma(br[c], g0[c], u0);
-              u1 = fma(br[c], g1[c], u1);
-            }
-            u2 = fma(gr[c], g2[c], u2);
-          }
-          if (COL) {
-            u0 = g0[qz];
-            u1 = g1[qz];
-          }
-          const double w0 = dc[0] * u0 + dc[1] * u1 + dc[2] * u2;
-          const double w1 = dc[1] * u0 + dc[3] * u1 + dc[4] * u2;
-          const double w2 = dc[2] * u0 + dc[4] * u1 + dc[5] * u2;
-#pragma unroll
-          for (int c = 0; c < P; ++c) {
-            if (!COL) {
-              s0[c] = fma(br[c], w0, s0[c]);
-              s1[c] = fma(br[c], w1, s1[c]);
-            }
-            s2[c] = fma(gr[c], w2, s2[c]);
-          }
-          if (COL) {
-            s0[qz] = w0;
-            s1[qz] = w1;
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < P; ++c) {
-          t2[c * TC] = s0[c];
-          t2[T2M + c * TC] = s1[c];
-          t2[2 * T2M + c * TC] = s2[c];
-        }
-      } else {
-        double g[P], s[P];
-#pragma unroll
-        for (int c = 0; c < P; ++c) { g[c] = t2[c * TC]; s[c] = 0.0; }
-        double dn = ld_d<C::DSM>(qde);
-#pragma unroll
-        for (int qz = 0; qz < Q; ++qz) {
-          const double dc = dn;
-          if (qz + 1 < Q) dn = ld_d<C::DSM>(qde + (qz + 1) * Q2);
-          double br[P];
-          TROW(B, qz, br);
-          double u = 0.0;
-#pragma unroll
-          for (int c = 0; c < P; ++c) u = fma(br[c], g[c], u);
-          const double v = dc * u;
-#pragma unroll
-          for (int c = 0; c < P; ++c) s[c] = fma(br[c], v, s[c]);
-        }
-#pragma unroll
-        for (int c = 0; c < P; ++c) t2[c * TC] = s[c];
-      }
       }
     }
     cta_sync();
@@ -1522,7 +1330,7 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
       const int qx = C::QXF ? r % Q : r / P, c = C::QXF ? r / Q : r % P;
       const double* t2 = smem + el * EB + T1SZ + qx * TX + c * TC;
       double* t1 = smem + el * EB + qx * S1 + c;
-      if constexpr (EO) {
+      {
         // rg = B_y^T v0 (x part), rb = G_y^T v1 + B_y^T v2 (y, z parts); mass: rb = B_y^T v0
         double SEg[H], SOg[PH], SEb[H], SOb[PH];
         zero(SEg); zero(SOg); zero(SEb); zero(SOb);
@@ -1575,43 +1383,6 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
           t1[b * P] = rb[b];
           if (DIFF) t1[T1M + b * P] = rg[b];
         }
-      } else {
-      double rb[P], rg[P];
-#pragma unroll
-      for (int b = 0; b < P; ++b) rb[b] = rg[b] = 0.0;
-#pragma unroll
-      for (int qy = 0; qy < Q; ++qy) {
-        double br[P], gr[P];
-        if (!COL) TROW(B, qy, br);
-        if (COL) {
-          TROW(G, qy, gr);
-          const double v0 = t2[qy * TY], v1 = t2[T2M + qy * TY],
-                       v2 = t2[2 * T2M + qy * TY];
-          rg[qy] = v0;
-#pragma unroll
-          for (int b = 0; b < P; ++b) rb[b] = fma(gr[b], v1, rb[b]);
-          rb[qy] += v2;
-        } else if (DIFF) {
-          TROW(G, qy, gr);
-          const double v0 = t2[qy * TY], v1 = t2[T2M + qy * TY],
-                       v2 = t2[2 * T2M + qy * TY];
-#pragma unroll
-          for (int b = 0; b < P; ++b) {
-            rg[b] = fma(br[b], v0, rg[b]);
-            rb[b] = fma(gr[b], v1, rb[b]);
-            rb[b] = fma(br[b], v2, rb[b]);
-          }
-        } else {
-          const double v = t2[qy * TY];
-#pragma unroll
-          for (int b = 0; b < P; ++b) rb[b] = fma(br[b], v, rb[b]);
-        }
-      }
-#pragma unroll
-      for (int b = 0; b < P; ++b) {
-        t1[b * P] = rb[b];                  // -> B_x^T
-        if (DIFF) t1[T1M + b * P] = rg[b];  // -> G_x^T
-      }
       }
     }
     cta_sync();
@@ -1621,7 +1392,7 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
       const int el = it / (P * P), r = it % (P * P);
       const double* t1 = smem + el * EB + r;
       double ye[P];
-      if constexpr (EO) {
+      {
         // ye = B_x^T vb + G_x^T vg (collocated: vb + G_x^T vg; mass: B_x^T vb)
         double SE[H], SO[PH];
         zero(SE); zero(SO);
@@ -1641,30 +1412,6 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
 #pragma unroll
           for (int a = 0; a < P; ++a) ye[a] += t1[a * S1];
         }
-      } else {
-#pragma unroll
-      for (int a = 0; a < P; ++a) ye[a] = 0.0;
-#pragma unroll
-      for (int qx = 0; qx < Q; ++qx) {
-        double br[P], gr[P];
-        if (!COL) TROW(B, qx, br);
-        const double vb = t1[qx * S1];
-        if (COL) {
-          TROW(G, qx, gr);
-          const double vg = t1[T1M + qx * S1];
-#pragma unroll
-          for (int a = 0; a < P; ++a) ye[a] = fma(gr[a], vg, ye[a]);
-          ye[qx] += vb;
-        } else if (DIFF) {
-          TROW(G, qx, gr);
-          const double vg = t1[T1M + qx * S1];
-#pragma unroll
-          for (int a = 0; a < P; ++a) ye[a] = fma(gr[a], vg, fma(br[a], vb, ye[a]));
-        } else {
-#pragma unroll
-          for (int a = 0; a < P; ++a) ye[a] = fma(br[a], vb, ye[a]);
-        }
-      }
       }
       double* yo = smem + el * EB + T1SZ + r;
 #pragma unroll
@@ -1688,25 +1435,19 @@ __device__ __forceinline__ void simt_pass(const Tab<P1, Q>& T, const ColArgs& A,
   }
 }
 
-// Per-launch shared-memory setup: zero everything (padding included), tables
-// into shared memory (non-constant-bank variants), the D-staging mbarrier.
+// Per-launch shared-memory setup: zero everything (padding included) and
+// initialise the D-staging mbarrier.  (The 1D tables are kernel-parameter
+// constant-bank operands, never copied to shared memory.)
 template <int KIND, int P1, int Q, int BX, int BY, int NT, int MAXR, bool EO>
 __device__ __forceinline__ void simt_prologue(const Tab<P1, Q>& T, unsigned long long* qbar) {
   using C = CfgS<KIND, P1, Q, BX, BY>;
-  constexpr int P = P1, PR = C::PR;
+  (void)T;
   extern __shared__ __align__(16) double smem[];
-  double* TBs = smem + C::TOFF;
-  double* TGs = TBs + Q * PR;
   if (C::DSM && threadIdx.x == 0) {
     mbar_init(qbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   FOR_ITEMS(i, C::SMEM_DOUBLES, NT, threadIdx.x) smem[i] = 0.0;
-  cta_sync();
-  FOR_ITEMS(i, Q * P, NT, threadIdx.x) {
-    TBs[(i / P) * PR + i % P] = T.B[i];
-    TGs[(i / P) * PR + i % P] = T.G[i];
-  }
   cta_sync();
 }
 

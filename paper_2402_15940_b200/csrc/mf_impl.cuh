@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(NT) mf_diffusion_simt(const __grid_constant__ 
     const int buf = k & 1;
     const long long nb = bk + gridDim.x;
     const int tid = vtid();
-    const int zo = (int)(bk >> 40);  // == 0, loop-variant (see cb_row)
+    const int zo = (int)(bk >> 40);  // == 0, loop-variant (see cdot in fused_impl.cuh)
     if (nb < A.nbatch)
       mf_issue<P1, Q, NE, NT>(A, GS0 + (buf ^ 1) * C::GS, nb);
     else
