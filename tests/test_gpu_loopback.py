@@ -91,9 +91,15 @@ def test_loopback_apply_rhs_dot_match_global(hf, R, bench, p, dims, bc, xmode):
         yu = op.apply_unfused(x, stream=s)
         b = op.rhs(stream=s)
         xx = m.dot(x, x, stream=s)
+        diag = op.diagonal(stream=s)
+        ymf = op.apply_mf(x, stream=s) if bench == "bp3" else None
+        dg = hf.DGMass(m, stream=s)
+        xdg = dg.random(4, stream=s)
+        ydg = dg.apply(xdg, stream=s)
         s.synchronize()
         return dict(x=host(x), y=host(y), yd=host(yd), yu=host(yu), b=host(b), d=d, xx=xx,
-                    n_owned=m.n_owned)
+                    n_owned=m.n_owned, diag=host(diag),
+                    ymf=None if ymf is None else host(ymf), xdg=host(xdg), ydg=host(ydg))
 
     res = run_ranks(hf, R, fn)
     om = O.Mesh(nx, ny, nz, p, alpha=0.1)
@@ -114,6 +120,21 @@ def test_loopback_apply_rhs_dot_match_global(hf, R, bench, p, dims, bc, xmode):
             top = R_["y"][-plane:]
             bot = res[r + 1]["y"][:plane]
             assert np.array_equal(top.view(np.uint64), bot.view(np.uint64))
+    dg_ref = O.diagonal(om, Ae, bc=bc)
+    nd = (p + 1) ** 3
+    Me = O.dg_mass_matrices(om)
+    xdg = W.random_vector(4, np.arange(om.n_elems * nd))
+    ydg = O.dg_apply(om, Me, xdg)
+    eslab = nx * ny * nzl * nd
+    for r in range(R):
+        R_ = res[r]
+        # matrix-free diagonal with the interface sums and Dirichlet rows = 1
+        assert rel(R_["diag"], slab(dg_ref, plane, p, nzl, r)) <= 1e-13
+        if R_["ymf"] is not None:  # fully matrix-free apply through the exchange
+            assert rel(R_["ymf"], slab(yg, plane, p, nzl, r)) <= 1e-12
+        # DG: rank r holds elements [r nx ny nzl, (r+1) nx ny nzl), global DG index
+        assert np.array_equal(R_["xdg"], xdg[r * eslab:(r + 1) * eslab])
+        assert rel(R_["ydg"], ydg[r * eslab:(r + 1) * eslab]) <= 1e-12
     assert sum(res[r]["n_owned"] for r in range(R)) == om.n_dofs
     scale = float(np.abs(xg) @ np.abs(yg))
     assert abs(res[0]["d"] - float(xg @ yg)) <= 1e-12 * scale
