@@ -130,7 +130,11 @@ void hofem_mesh_destroy(void* mesh);
  * on ONE device) a rank's thread must not synchronize the whole device
  * (cudaDeviceSynchronize, cudaFree, torch.cuda.synchronize) between exchanges:
  * it would wait on a neighbour's put kernel that waits on this rank -- use
- * stream synchronization; the library itself allocates stream-ordered. */
+ * stream synchronization.  Calls on existing handles allocate stream-ordered
+ * (cudaMallocAsync); creating a handle (mesh, operator, DG, p-MG) and
+ * allocating caller buffers (cudaMalloc, a torch caching-allocator miss) may
+ * synchronize the device, so on a loopback mesh create every object and
+ * buffer before switching mode 1 on. */
 hofem_status hofem_mesh_set_exchange(void* mesh, int mode, void* stream);
 
 /* ---------------------------------------------------------- operator (a2-a9) */

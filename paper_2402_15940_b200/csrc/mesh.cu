@@ -123,9 +123,10 @@ hofem_status mesh_build_restriction(Mesh* m, cudaStream_t s) {
     set_error("unfused path: mesh too large for 32-bit restriction tables");
     return HOFEM_ERR_ARG;
   }
-  if (cudaMalloc(&m->d_l2e, sizeof(int) * ent) != cudaSuccess ||
-      cudaMalloc(&m->d_toff, sizeof(long long) * (m->n_local + 1)) != cudaSuccess ||
-      cudaMalloc(&m->d_tidx, sizeof(int) * ent) != cudaSuccess) {
+  // stream-ordered (no device-wide synchronization between exchanges)
+  if (cudaMallocAsync(&m->d_l2e, sizeof(int) * ent, s) != cudaSuccess ||
+      cudaMallocAsync(&m->d_toff, sizeof(long long) * (m->n_local + 1), s) != cudaSuccess ||
+      cudaMallocAsync(&m->d_tidx, sizeof(int) * ent, s) != cudaSuccess) {
     cudaGetLastError();
     set_error("restriction tables: out of device memory");
     return HOFEM_ERR_OOM;

@@ -25,8 +25,9 @@ hofem_status apply_mf(Op* op, const double* x, double* y, cudaStream_t s) {
   HOFEM_TRY(mesh_build_restriction(m, s));
   const long long ent = m->elems * m->P1 * m->P1 * m->P1;
   if (!op->d_eout) {
-    if (cudaMalloc(&op->d_ein, sizeof(double) * (ent + 1)) != cudaSuccess ||
-        cudaMalloc(&op->d_eout, sizeof(double) * (ent + 1)) != cudaSuccess) {
+    // stream-ordered (no device-wide synchronization between exchanges)
+    if (cudaMallocAsync(&op->d_ein, sizeof(double) * (ent + 1), s) != cudaSuccess ||
+        cudaMallocAsync(&op->d_eout, sizeof(double) * (ent + 1), s) != cudaSuccess) {
       cudaGetLastError();
       set_error("fully matrix-free apply: out of device memory for the E-vector");
       return HOFEM_ERR_OOM;

@@ -267,8 +267,12 @@ hofem_status op_diagonal(Op* op, double* d, cudaStream_t s) {
   double* ed = nullptr;
   HOFEM_CUDA(cudaMallocAsync(&ed, sizeof(double) * (ent + 1), s));
   const size_t smem = sizeof(double) * (2 * Q * P1 + nc * Q * Q * Q + P1 * Q * Q + P1 * P1 * Q + nd);
-  HOFEM_CUDA(cudaFuncSetAttribute(diag_elem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+  static size_t smem_set = 0;  // set once per size class, not per call
+  if (smem > 48 * 1024 && smem > smem_set) {
+    HOFEM_CUDA(cudaFuncSetAttribute(diag_elem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+    smem_set = smem;
+  }
   if (m->elems > 0) {
     diag_elem_kernel<<<(unsigned)m->elems, 128, smem, s>>>(P1, Q, op->kind == HOFEM_MASS,
                                                            op->d_qdata, op->d_B, op->d_G, ed);

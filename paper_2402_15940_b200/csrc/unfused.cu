@@ -193,8 +193,9 @@ hofem_status apply_unfused(Op* op, const double* x, double* y, cudaStream_t s) {
   const int P1 = m->P1, Q = op->Q, nd = P1 * P1 * P1;
   const long long ent = m->elems * nd;
   if (!op->d_ein) {
-    if (cudaMalloc(&op->d_ein, sizeof(double) * (ent + 1)) != cudaSuccess ||
-        cudaMalloc(&op->d_eout, sizeof(double) * (ent + 1)) != cudaSuccess) {
+    // stream-ordered (no device-wide synchronization between exchanges)
+    if (cudaMallocAsync(&op->d_ein, sizeof(double) * (ent + 1), s) != cudaSuccess ||
+        cudaMallocAsync(&op->d_eout, sizeof(double) * (ent + 1), s) != cudaSuccess) {
       cudaGetLastError();
       set_error("unfused path: out of device memory for E-vectors");
       return HOFEM_ERR_OOM;

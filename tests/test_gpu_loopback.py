@@ -82,20 +82,30 @@ def test_loopback_apply_rhs_dot_match_global(hf, R, bench, p, dims, bc, xmode):
     plane = (p * nx + 1) * (p * ny + 1)
 
     def fn(r, comm, s):
+        # every object and output buffer exists before the kernel-initiated
+        # exchange is switched on: an allocation or object creation between two
+        # exchanges may synchronize the whole (shared) device while a
+        # neighbour's put kernel spins on this rank (hofem.h, set_exchange)
         m = hf.Mesh(nx, ny, nz, p, alpha=0.1, comm=comm, stream=s)
-        m.set_exchange(xmode, stream=s)
         op = hf.Operator(m, kind=kind, rule=rule, bc=bc, stream=s)
-        x = m.random(5, stream=s)
-        y = op.apply(x, stream=s)
-        yd, d = op.apply_dot(x, stream=s)
-        yu = op.apply_unfused(x, stream=s)
-        b = op.rhs(stream=s)
-        xx = m.dot(x, x, stream=s)
-        diag = op.diagonal(stream=s)
-        ymf = op.apply_mf(x, stream=s) if bench == "bp3" else None
         dg = hf.DGMass(m, stream=s)
+        x = m.random(5, stream=s)
+        y, yd, yu, b, diag, ymf = (torch.empty_like(x) for _ in range(6))
         xdg = dg.random(4, stream=s)
-        ydg = dg.apply(xdg, stream=s)
+        ydg = torch.empty_like(xdg)
+        s.synchronize()
+        m.set_exchange(xmode, stream=s)
+        op.apply(x, y, stream=s)
+        _, d = op.apply_dot(x, yd, stream=s)
+        op.apply_unfused(x, yu, stream=s)
+        op.rhs(b, stream=s)
+        xx = m.dot(x, x, stream=s)
+        op.diagonal(diag, stream=s)
+        if bench == "bp3":
+            op.apply_mf(x, ymf, stream=s)
+        else:
+            ymf = None
+        dg.apply(xdg, ydg, stream=s)
         s.synchronize()
         return dict(x=host(x), y=host(y), yd=host(yd), yu=host(yu), b=host(b), d=d, xx=xx,
                     n_owned=m.n_owned, diag=host(diag),
@@ -159,15 +169,18 @@ def test_loopback_cg_iterates_match_global(hf, R, bench, p, dims, xmode):
 
     def fn(r, comm, s):
         m = hf.Mesh(nx, ny, nz, p, alpha=0.1, comm=comm, stream=s)
-        m.set_exchange(xmode, stream=s)
         op = hf.Operator(m, kind=kind, rule=rule, bc=1, stream=s)
-        b = op.rhs(stream=s)
+        xs = {k: torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
+              for k in ks + ["conv"]}
+        b = torch.empty_like(xs["conv"])
+        s.synchronize()
+        m.set_exchange(xmode, stream=s)  # after every allocation (see the test above)
+        op.rhs(b, stream=s)
         out = {}
         for k in ks:
-            x = torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
-            op.cg(b, x, max_iter=k, fixed_iters=True, stream=s)
-            out[k] = host(x)
-        x = torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
+            op.cg(b, xs[k], max_iter=k, fixed_iters=True, stream=s)
+            out[k] = host(xs[k])
+        x = xs["conv"]
         st, stats, _ = op.cg(b, x, rel_tol=1e-13, max_iter=1000, check_every=1, stream=s)
         out["conv"] = (st, stats.iterations, host(x))
         return out
@@ -193,8 +206,11 @@ def test_loopback_peer_puts_back_to_back(hf):
         op = hf.Operator(m, kind=hf.DIFFUSION, rule=hf.GAUSS, bc=1, stream=s)
         x = m.random(3, stream=s)
         ref = host(op.apply(x, stream=s))
+        ys = [torch.empty_like(x) for _ in range(30)]
+        s.synchronize()
         m.set_exchange(1, stream=s)
-        ys = [op.apply(x, stream=s) for _ in range(30)]
+        for y in ys:
+            op.apply(x, y, stream=s)
         s.synchronize()
         return ref, [host(y) for y in ys]
 
