@@ -1666,7 +1666,13 @@ template <> struct ShapeSD<2> { static constexpr int BX = 4, BY = 4, NT = 160, M
 template <> struct ShapeSD<3> { static constexpr int BX = 4, BY = 2, NT = 128, MAXR = 128, CPS = 4; };
 template <> struct ShapeSD<4> { static constexpr int BX = 3, BY = 2, NT = 160, MAXR = 102, CPS = 4; };
 template <> struct ShapeSD<5> { static constexpr int BX = 3, BY = 1, NT = 128, MAXR = 102, CPS = 5; };
-template <> struct ShapeSD<6> { static constexpr int BX = 1, BY = 2, NT = 128, MAXR = 128, CPS = 4; };
+// P1 = 6: 1x3 bricks with 160 threads (S1 / S2 / S3 fill 108 / 126 / 147 of them,
+// epilogue 96 rows; 3 CTAs/SM at 128 registers) beat round 2's 1x2 / 128 threads
+// (72 / 84 / 98 items: the fourth warp idled in most stages): BP3 p=5 brick kernel
+// 4.94 -> 4.70 ms on the config-5 slab, 1.015 -> 0.979 ms at 60^3, 1.120 -> 1.110 ms
+// at 62^3 (profiles/ab/r2v_ab_shapes2.txt); BP1 p=5 (~1M dofs) 45.5 -> 43.5 us
+// (r2v_ab_p6x3.txt, which also re-checked DLA, T2QX, PRE, ENDBAR on this shape)
+template <> struct ShapeSD<6> { static constexpr int BX = 1, BY = 3, NT = 160, MAXR = 128, CPS = 3; };
 template <> struct ShapeSD<7> { static constexpr int BX = 1, BY = 1, NT = 64, MAXR = 168, CPS = 6; };
 template <> struct ShapeSD<8> { static constexpr int BX = 1, BY = 1, NT = 96, MAXR = 168, CPS = 4; };
 template <> struct ShapeSD<9> { static constexpr int BX = 1, BY = 1, NT = 128, MAXR = 232, CPS = 2; };
