@@ -1719,8 +1719,13 @@ template <int P1>
 struct ShapeSMD : ShapeS<P1> {};
 // measured (BP1 at ~1M dofs, whole apply incl. memset and fix-up; gpurun_out/e12,
 // f5): single-element bricks pay off at p = 8 only (more edge lines elsewhere)
-template <> struct ShapeSMD<5> { static constexpr int BX = 2, BY = 2, NT = 160, MAXR = 128, CPS = 3; };
-template <> struct ShapeSMD<9> { static constexpr int BX = 1, BY = 1, NT = 128, MAXR = 96, CPS = 5; };
+// register caps (r2v, profiles/ab/r2v_ab_massregs.txt, BP1 ~1M dofs): the mass kernels fit
+// in 64-80 registers without spills; a lower cap (more CTAs per SM) pays at P1 = 2 (64: -7 %),
+// 5 (80: -9 %), 6 (80: -6.5 %), 9 (64: -2 %) and loses elsewhere (the inherited caps stay)
+template <> struct ShapeSMD<2> { static constexpr int BX = 4, BY = 4, NT = 160, MAXR = 64, CPS = 6; };
+template <> struct ShapeSMD<5> { static constexpr int BX = 2, BY = 2, NT = 160, MAXR = 80, CPS = 5; };
+template <> struct ShapeSMD<6> { static constexpr int BX = 1, BY = 3, NT = 160, MAXR = 80, CPS = 5; };
+template <> struct ShapeSMD<9> { static constexpr int BX = 1, BY = 1, NT = 128, MAXR = 64, CPS = 8; };
 #ifdef HOFEM_SM_P1
 struct ShapeSMOverride {
   static constexpr int BX = HOFEM_SM_BX, BY = HOFEM_SM_BY, NT = HOFEM_SM_NT,
