@@ -47,6 +47,7 @@ def main():
     ap.add_argument("--ns", default="", help="elements per axis (default: the config-2/3 size)")
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--modes", default="persistent,fused,separate")
+    ap.add_argument("--slab", default="", help="nx,ny,nz (one mesh; overrides --ns)")
     a = ap.parse_args()
     kind = hf.MASS if a.bench == "bp1" else hf.DIFFUSION
     rule = hf.GLL if a.bench == "bp5" else hf.GAUSS
@@ -54,8 +55,10 @@ def main():
     for p in [int(v) for v in a.ps.split(",")]:
         ns = [int(v) for v in a.ns.split(",")] if a.ns else \
             [int(round((99.0 if a.bench == "bp1" else 311.0) / p))]
-        for n in ns:
-            m = hf.Mesh(n, n, n, p, alpha=0.1)
+        dims = [tuple(int(v) for v in a.slab.split(","))] if a.slab else [(n, n, n) for n in ns]
+        for dd in dims:
+            n = dd[0]
+            m = hf.Mesh(*dd, p, alpha=0.1)
             op = hf.Operator(m, kind=kind, rule=rule, bc=bc)
             b = op.rhs()
             for mode in a.modes.split(","):
