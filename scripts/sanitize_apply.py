@@ -15,7 +15,7 @@ import torch  # noqa: E402
 import paper_2402_15940_b200 as hf  # noqa: E402
 
 for bench, p, n in (("bp3", 5, 3), ("bp3", 4, 3), ("bp3", 6, 2), ("bp5", 6, 2), ("bp1", 8, 2),
-                    ("bp3", 2, 3)):
+                    ("bp3", 2, 3), ("bp1", 5, 3), ("bp1", 1, 3), ("bp1", 4, 3)):
     kind = hf.MASS if bench == "bp1" else hf.DIFFUSION
     rule = hf.GLL if bench == "bp5" else hf.GAUSS
     m = hf.Mesh(n, n, n + 1, p)
