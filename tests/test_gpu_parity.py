@@ -390,88 +390,101 @@ def test_cg_converges_manufactured(hf):
 
 
 # ----------------------------------------------------------------------------- at scale
-def _contributors(I, J, K, p, n):
+def _contributors(I, J, K, p, dims):
     """Elements (and local node indices) whose closure holds lattice point
-    (I, J, K) of an n^3-element mesh: 1 (interior), 2 (face), 4 (edge), 8."""
-    def axis(L):
+    (I, J, K) of an nx*ny*nz-element mesh: 1 (interior), 2 (face), 4 (edge), 8."""
+    nx, ny, nz = dims
+    def axis(L, n):
         if L % p == 0:
             return [(e, L - p * e) for e in (L // p - 1, L // p) if 0 <= e < n]
         return [(L // p, L % p)]
     out = []
-    for ez, c in axis(K):
-        for ey, b in axis(J):
-            for ex, a in axis(I):
-                out.append((ex + n * (ey + n * ez), a + (p + 1) * (b + (p + 1) * c)))
+    for ez, c in axis(K, nz):
+        for ey, b in axis(J, ny):
+            for ex, a in axis(I, nx):
+                out.append((ex + nx * (ey + ny * ez), a + (p + 1) * (b + (p + 1) * c)))
     return out
 
 
-def _sample_points(rng, p, n, bc):
+def _sample_points(rng, p, dims, bc):
     """Seeded lattice points of every contribution class: element interiors,
     x / y / z single-face points (2 elements: the points the fused kernel
     completes by two-term reductions onto the zeroed y), edge-line points (4:
     the fix-up's partial sums), vertices (8), and with bc the Dirichlet faces."""
-    N = p * n + 1
+    Ns = [p * n + 1 for n in dims]
     lo = 1 if bc else 0
-    def coord(on_plane):
+    def coord(on_plane, N):
         while True:
             v = int(rng.integers(lo, N - lo))
             if (v % p == 0) == on_plane and (not bc or 0 < v < N - 1):
                 return v
+    def point(planes):
+        return tuple(coord(planes[a], Ns[a]) for a in range(3))
     pts = []
     if p > 1:
-        pts += [(coord(False), coord(False), coord(False)) for _ in range(96)]
+        pts += [point((False, False, False)) for _ in range(96)]
         for axis in range(3):
             for _ in range(48):
-                c = [coord(False), coord(False), coord(False)]
-                c[axis] = coord(True)
-                pts.append(tuple(c))
+                pts.append(point(tuple(a == axis for a in range(3))))
         for axis in range(3):
             for _ in range(24):
-                c = [coord(True), coord(True), coord(True)]
-                c[axis] = coord(False)
-                pts.append(tuple(c))
-    pts += [(coord(True), coord(True), coord(True)) for _ in range(32)]
+                pts.append(point(tuple(a != axis for a in range(3))))
+    pts += [point((True, True, True)) for _ in range(32)]
     if bc:
-        pts += [(0, int(rng.integers(0, N)), int(rng.integers(0, N))) for _ in range(8)]
-        pts += [(int(rng.integers(0, N)), int(rng.integers(0, N)), N - 1) for _ in range(8)]
+        pts += [(0, int(rng.integers(0, Ns[1])), int(rng.integers(0, Ns[2]))) for _ in range(8)]
+        pts += [(int(rng.integers(0, Ns[0])), int(rng.integers(0, Ns[1])), Ns[2] - 1)
+                for _ in range(8)]
     return pts
 
 
-@pytest.mark.parametrize("bench,p,bc", [("bp3", 5, 1), ("bp3", 5, 0), ("bp1", 8, 0),
-                                        ("bp5", 6, 1), ("bp3", 4, 1), ("bp3", 6, 0)])
-def test_sampled_points_full_size(hf, bench, p, bc):
+C5 = W.config5()
+C5_DIMS = (C5["nx"], C5["ny"], C5["nz"])
+
+
+@pytest.mark.parametrize("bench,p,bc,dims", [
+    ("bp3", 5, 1, None), ("bp3", 5, 0, None), ("bp1", 8, 0, None), ("bp5", 6, 1, None),
+    ("bp3", 4, 1, None), ("bp3", 6, 0, None),
+    ("bp3", 5, 1, C5_DIMS),  # the bench's own workload: config 5, 200x200x25, 126M dofs
+])
+def test_sampled_points_full_size(hf, bench, p, bc, dims):
     """Sampled parity at the bench's full size and launch configuration (SURVEY.md
     §8(c) "parity at scale"; default options, so the memset + separate fix-up
     path the bench times): y at seeded lattice points of every contribution
     class against the oracle's dense-B element actions of the 1-8 elements that
-    hold each point, summed; Dirichlet rows y = x (reading R6)."""
+    hold each point, summed; Dirichlet rows y = x (reading R6).  Meshes: the
+    config-2/3 sweep sizes and BASELINE config 5's slab (the headline bench)."""
     kind, rule = KINDS[bench]
-    n = W.bp3_sweep_n(p) if bench != "bp1" else W.bp1_sweep_n(p)
-    m = hf.Mesh(n, n, n, p, alpha=W.ALPHA)
+    if dims is None:
+        n = W.bp3_sweep_n(p) if bench != "bp1" else W.bp1_sweep_n(p)
+        dims = (n, n, n)
+    nx, ny, nz = dims
+    m = hf.Mesh(nx, ny, nz, p, alpha=W.ALPHA)
     op = hf.Operator(m, kind=kind, rule=rule, bc=bc)
-    om = O.Mesh(n, n, n, p, alpha=W.ALPHA)
+    om = O.Mesh(nx, ny, nz, p, alpha=W.ALPHA)
     x = m.random(11)
     y = host(op.apply(x))
     xh = host(x)
-    N = p * n + 1
+    del x
+    op.close()
+    Nx, Ny, Nz = (p * nx + 1, p * ny + 1, p * nz + 1)
+    rng = np.random.default_rng(7 + p + 10 * bc)
+    pts = _sample_points(rng, p, dims, bc)
+    contrib = {pt: _contributors(*pt, p, dims) for pt in pts}
+    elems = np.array(sorted({e for c in contrib.values() for e, _ in c}))
     xz = xh
     if bc:  # z = x with the Dirichlet entries zeroed (reading R6)
-        xz = xh.reshape(N, N, N).copy()
+        xz = xh.reshape(Nz, Ny, Nx).copy()
         xz[0, :, :] = xz[-1, :, :] = 0.0
         xz[:, 0, :] = xz[:, -1, :] = 0.0
         xz[:, :, 0] = xz[:, :, -1] = 0.0
         xz = xz.reshape(-1)
-    rng = np.random.default_rng(7 + p + 10 * bc)
-    pts = _sample_points(rng, p, n, bc)
-    contrib = {pt: _contributors(*pt, p, n) for pt in pts}
-    elems = np.array(sorted({e for c in contrib.values() for e, _ in c}))
     ye = O.element_apply_sample(om, kind, rule, xz, elems)
     row = {e: i for i, e in enumerate(elems)}
     scale = np.abs(ye).max()
     num = den = 0.0
     for (I, J, K), c in contrib.items():
-        g = I + N * (J + N * K)
-        if bc and (min(I, J, K) == 0 or max(I, J, K) == N - 1):
+        g = I + Nx * (J + Ny * K)
+        if bc and (min(I, J, K) == 0 or I == Nx - 1 or J == Ny - 1 or K == Nz - 1):
             assert y[g] == xh[g]
             continue
         r = sum(ye[row[e], loc] for e, loc in c)
@@ -481,14 +494,18 @@ def test_sampled_points_full_size(hf, bench, p, bc):
     assert np.sqrt(num / den) <= APPLY_TOL
 
 
-def test_cg_full_size_properties(hf):
-    """The bench's CG (BP3 p=5, 62^3 elements, Dirichlet, manufactured RHS) at
-    full size, where the oracle cannot run the solve: x_1 = alpha_0 b with
+@pytest.mark.parametrize("dims", [None, C5_DIMS])
+def test_cg_full_size_properties(hf, dims):
+    """The bench's CG (BP3 p=5, Dirichlet, manufactured RHS; config 3's 62^3
+    elements and config 5's 200x200x25 slab, the headline workload) at full
+    size, where the oracle cannot run the solve: x_1 = alpha_0 b with
     alpha_0 = b.b / b.Ab; after k iterations ||b - A x_k||^2 equals the
     recurrence's r_k.r_k; the per-iteration schedule (default at this size)
     and the persistent kernel give the same iterates up to reduction order."""
-    n = W.bp3_sweep_n(5)
-    m = hf.Mesh(n, n, n, 5, alpha=W.ALPHA)
+    if dims is None:
+        n = W.bp3_sweep_n(5)
+        dims = (n, n, n)
+    m = hf.Mesh(*dims, 5, alpha=W.ALPHA)
     op = hf.Operator(m, kind=hf.DIFFUSION, rule=hf.GAUSS, bc=hf.BC_DIRICHLET)
     b = op.rhs()
     bb = m.dot(b, b)
