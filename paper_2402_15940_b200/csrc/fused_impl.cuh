@@ -59,7 +59,7 @@
 #define HOFEM_EO_DPOL -1  // SIMT-EO: L2 policy of the stage-3 D loads (see ld_dp; -1 per p)
 #endif
 #ifndef HOFEM_L2PF_POL
-#define HOFEM_L2PF_POL 0  // 1: the qdata L2 prefetch marks its lines evict_last
+#define HOFEM_L2PF_POL -1  // 1: the qdata L2 prefetch marks its lines evict_last (-1: per P1)
 #endif
 #ifndef HOFEM_SIMT_T2QX
 #define HOFEM_SIMT_T2QX -1  // SIMT: 1 = T2 [m][qy][c][qx] with qx-fastest stage-2 items
@@ -744,7 +744,9 @@ __device__ __forceinline__ void prefetch_qdata_l2(const ColArgs& A, const Brick&
     if (ex < A.nx && ey < A.ny) {
       const long long e = ex + (long long)A.nx * (ey + (long long)A.ny * b.ez);
       const long long lo = (e * per) & ~15LL, hi = ((e + 1) * per + 15) & ~15LL;
-      if (HOFEM_L2PF_POL) {
+      // evict_last: measured -1.1 % on the config-5 slab, neutral at 62^3, for the
+      // P1 = 6 1x3 brick (profiles/ab/r2v_ab_p6knobs3.txt); off elsewhere (round 2)
+      if (HOFEM_L2PF_POL >= 0 ? HOFEM_L2PF_POL != 0 : C::P == 6 && C::KINDV == KIND_DIFF) {
         unsigned long long pol;
         asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
         asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(base + lo),
@@ -839,7 +841,7 @@ constexpr bool simt_t2qx() {
 
 template <int KIND, int P1, int Q, int BX, int BY>
 struct CfgS {
-  static constexpr int p = P1 - 1, P = P1, NE = BX * BY;
+  static constexpr int p = P1 - 1, P = P1, NE = BX * BY, KINDV = KIND;
   static constexpr int LX = p * BX + 1, LY = p * BY + 1, LZ = P1;
   static constexpr int LXS = ((LY * LZ) % 2 == 0) ? LY * LZ + 1 : LY * LZ;
   static constexpr int LAT = LXS * LX;
