@@ -525,7 +525,7 @@ def run_sweep(args, hf, torch, stream):
     # f1 metric: DOFs needed to reach 80 % of peak, BP3 p=5 CG
     # iterations, fused schedule (in-kernel fix-up + fused update / persistent
     # kernel, i.e. the defaults) vs the separate-kernel schedule
-    sizes = [4, 6, 8, 12, 16, 24, 32, 44, 62]
+    sizes = [4, 6, 8, 12, 16, 20, 24, 28, 32, 38, 44, 52, 62]
     curves = {"fused": [], "separate": []}
     for n in sizes:
         m = hf.Mesh(n, n, n, 5, alpha=0.1)
@@ -543,12 +543,22 @@ def run_sweep(args, hf, torch, stream):
         op.close()
         m.close()
         torch.cuda.empty_cache()
-    d80 = {}
+    d80, d80i = {}, {}
     for name, cv in curves.items():
         top = max(c["gdof_it_s"] for c in cv)
-        d80[name] = next(c["dofs"] for c in cv if c["gdof_it_s"] >= 0.8 * top)
+        k = next(i for i, c in enumerate(cv) if c["gdof_it_s"] >= 0.8 * top)
+        d80[name] = cv[k]["dofs"]
+        d80i[name] = cv[k]["dofs"]
+        if k > 0:  # crossing, interpolated linearly in log(dofs)
+            a, b = cv[k - 1], cv[k]
+            f = (0.8 * top - a["gdof_it_s"]) / (b["gdof_it_s"] - a["gdof_it_s"])
+            d80i[name] = int(round(np.exp(np.log(a["dofs"]) +
+                                          f * (np.log(b["dofs"]) - np.log(a["dofs"])))))
     out["dofs_to_80pct_of_peak"] = {"bench": "bp3 p=5 CG (Dirichlet), 50 fixed iterations",
-                                    "curves": curves, "dofs_80pct": d80}
+                                    "curves": curves, "dofs_80pct": d80,
+                                    "dofs_80pct_interpolated": d80i,
+                                    "peak": {k: max(c["gdof_it_s"] for c in v)
+                                             for k, v in curves.items()}}
     # f2: BPS3 -- p-multigrid preconditioned CG vs CG to 1e-10 (BP3 p=5, 24^3 elements)
     m = hf.Mesh(24, 24, 24, 5, alpha=0.1)
     op = hf.Operator(m, kind=hf.DIFFUSION, rule=hf.GAUSS, bc=hf.BC_DIRICHLET)
