@@ -1530,7 +1530,7 @@ __device__ __forceinline__ double grid_sum(const double* parts, double* red) {
 // the inlined brick pass (spills); a call per phase per iteration is free.
 // Grid-stride over 16-byte pairs (vectors are 16-byte aligned, hofem.h); the
 // traversal order is fixed, so the returned partial is deterministic.
-constexpr int CGU = 4;
+constexpr int CGU = 2;
 
 // r -= alpha Ap; returns this thread's share of r.r
 static __device__ __noinline__ double cg_r_update(long long n, double alpha, const double* Ap,
@@ -1616,45 +1616,61 @@ __global__ void __maxnreg__(MAXR)
   __shared__ __align__(8) unsigned long long qbar;
   simt_prologue<KIND, P1, Q, BX, BY, NT, MAXR, EO>(T, &qbar);
   unsigned qphase = 0;
-  const long long st = (long long)gridDim.x * NT;
-  const long long t0 = (long long)blockIdx.x * NT + threadIdx.x;
-  if (G.zero_ap)
-    for (long long i = t0; i < G.n; i += st) G.Ap[i] = 0.0;
-  grid_barrier(A.bar);
-  const double rr0 = __ldcg(G.rr);
-  double rr = rr0;
-  int k = 0;
-  bool brk = false;
-  const bool stop0 = !G.fixed && rr0 == 0.0;
-  while (!stop0 && k < G.max_iter) {
+  // CG state (identical in every thread of every CTA) lives in shared memory
+  // across the brick pass: registers held over simt_pass made it spill
+  __shared__ double s_rr0, s_rr;
+  __shared__ int s_k, s_brk;
+  {
+    const long long st = (long long)gridDim.x * NT;
+    const long long t0 = (long long)blockIdx.x * NT + threadIdx.x;
+    if (G.zero_ap)
+      for (long long i = t0; i < G.n; i += st) G.Ap[i] = 0.0;
+  }
+  if (threadIdx.x == 0) {
+    s_rr0 = s_rr = __ldcg(G.rr);
+    s_k = 0;
+    s_brk = 0;
+  }
+  grid_barrier(A.bar);  // (also orders the shared stores for the CTA)
+  for (;;) {
+    if ((!G.fixed && s_rr0 == 0.0) || s_k >= G.max_iter) break;
     double dsum = 0.0;
     simt_pass<KIND, P1, Q, BX, BY, NT, MAXR, EO>(T, A, &qbar, qphase, dsum);
     grid_barrier(A.bar);
+    const long long st = (long long)gridDim.x * NT;
+    const long long t0 = (long long)blockIdx.x * NT + threadIdx.x;
     const long long nfx = fixup_count(A.fx);
     for (long long g = t0; g < nfx; g += st) dsum += fixup_flat(A.fx, g);
     block_sum_store(dsum, G.parts + blockIdx.x, smem);
     grid_barrier(A.bar);
     const double pAp = grid_sum<NT>(G.parts, smem);
     if (!(pAp > 0.0)) {  // same value in every CTA: all stop here
-      brk = true;
+      if (threadIdx.x == 0) s_brk = 1;
       break;
     }
+    const double rr = s_rr;
     const double alpha = rr / pAp;
-    const double s = cg_r_update(G.n, alpha, G.Ap, G.r);
-    block_sum_store(s, G.parts2 + blockIdx.x, smem);
+    const double sr = cg_r_update(G.n, alpha, G.Ap, G.r);
+    block_sum_store(sr, G.parts2 + blockIdx.x, smem);
     grid_barrier(A.bar);
-    const double rn = grid_sum<NT>(G.parts2, smem);
+    const double rn = grid_sum<NT>(G.parts2, smem);  // every thread has read s_rr
     const double beta = rr > 0.0 ? rn / rr : 0.0;
     cg_xp_update(G.n, alpha, beta, G.x, G.p, G.r, G.Ap, G.zero_ap);
-    ++k;
-    rr = rn;
-    if (blockIdx.x == 0 && threadIdx.x == 0) G.rr[k] = rn;
-    if (!G.fixed && (rn == 0.0 || sqrt(rn) <= G.rel_tol * sqrt(rr0))) break;
+    const int k = s_k + 1;
+    const bool stop = !G.fixed && (rn == 0.0 || sqrt(rn) <= G.rel_tol * sqrt(s_rr0));
+    cta_sync();  // every thread has read s_k / s_rr0 of this iteration
+    if (threadIdx.x == 0) {
+      s_rr = rn;
+      s_k = k;
+      if (blockIdx.x == 0) G.rr[k] = rn;
+    }
+    if (stop) break;
     grid_barrier(A.bar);
   }
+  cta_sync();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    G.result[0] = k;
-    G.result[1] = brk ? 1 : 0;
+    G.result[0] = s_k;
+    G.result[1] = s_brk;
   }
 }
 
