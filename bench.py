@@ -38,7 +38,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "BP3 diffusion GDOF/s per GPU vs p; CG [DOFs x iters]/s at 1/2/4/8 B200"
+METRIC = "BP3 diffusion GDOF/s per GPU vs p; CG [DOFs\u00d7iters]/s at 1/2/4/8 B200"  # BASELINE.json
 UNIT = "GDOF*it/s"
 
 
