@@ -134,7 +134,11 @@ void hofem_mesh_destroy(void* mesh);
  * (cudaMallocAsync); creating a handle (mesh, operator, DG, p-MG) and
  * allocating caller buffers (cudaMalloc, a torch caching-allocator miss) may
  * synchronize the device, so on a loopback mesh create every object and
- * buffer before switching mode 1 on. */
+ * buffer before switching mode 1 on -- and load the kernel modules eagerly
+ * (CUDA_MODULE_LOADING=EAGER): a kernel's first, lazy load may synchronize the
+ * context as well.  With mode 1, hofem_cg's persistent schedule
+ * (HOFEM_OPT_CG_PERSISTENT) also runs on several ranks: the planes and both
+ * dot products are then exchanged inside the one kernel per rank. */
 hofem_status hofem_mesh_set_exchange(void* mesh, int mode, void* stream);
 
 /* ---------------------------------------------------------- operator (a2-a9) */
@@ -348,8 +352,12 @@ hofem_status hofem_op_fused_info(const void* op, hofem_fused_info* out);
  *                 cooperative kernel; auto = single rank, <= 8 Mi dofs.
  *  CG_PERSISTENT  hofem_cg runs the whole solve in ONE cooperative kernel (brick
  *                 pass, fix-up, p.Ap, updates, r.r, stop test, all behind grid
- *                 barriers; §2.3); single rank only; auto =
- *                 <= 256 Ki dofs (measured crossover).  Convergence is then tested every iteration.
+ *                 barriers; §2.3); a single rank, or several
+ *                 ranks with the kernel-initiated exchange (mesh mode 1: the
+ *                 interface planes are put into the neighbours' slots and p.Ap /
+ *                 r.r allreduced by a chain over the ranks inside the kernel,
+ *                 PAPER.md:197); auto = <= 256 Ki local dofs (measured crossover).
+ *                 Convergence is then tested every iteration.
  *  L2_PREFETCH    bulk-prefetch the next brick's qdata into L2. */
 typedef enum {
   HOFEM_OPT_INFIX = 1,

@@ -340,18 +340,22 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
   // 8^3 elements 31.4 vs 32.8 us/it); from ~0.5M dofs on, the per-iteration
   // kernels (fused cooperative update) win.  Convergence is tested every
   // iteration on the device (check_every does not apply).
-  const bool persist = m->nranks == 1 && fused_supported(op) &&
+  // (several ranks: with the kernel-initiated exchange, mesh mode 1 -- the
+  // planes and both dot products are then exchanged inside the kernel)
+  const bool persist = (m->nranks == 1 || m->xmode == 1) && fused_supported(op) &&
                        (op->opt_cg_persist == 2 || (op->opt_cg_persist == 1 && n <= (256LL << 10)));
   if (persist && !(rr0 == 0.0 && !fixed_iters)) {
     int* dres = reinterpret_cast<int*>(flag + 1);
-    HOFEM_CUDA(cudaMemsetAsync(dres, 0, 2 * sizeof(int), s));
+    HOFEM_CUDA(cudaMemsetAsync(dres, 0, 4 * sizeof(int), s));
     hofem_status st = cg_persistent(op, x, op->d_r, op->d_p, op->d_Ap, rr, max_iter, fixed_iters,
                                     rel_tol, dres, s);
     if (st == HOFEM_OK) {
-      int res[2] = {0, 0};
+      int res[4] = {0, 0, 0, 0};
       HOFEM_CUDA(cudaMemcpyAsync(res, dres, sizeof(res), cudaMemcpyDeviceToHost, s));
       HOFEM_CUDA(cudaStreamSynchronize(s));
       const int k = res[0];
+      m->xseq += (unsigned long long)res[2];  // the kernel's exchanges / chain reductions
+      m->rseq += (unsigned long long)res[3];
       double rr_last = rr0;
       if (k > 0) HOFEM_CUDA(cudaMemcpy(&rr_last, rr + k, sizeof(double), cudaMemcpyDeviceToHost));
       hofem_status status = HOFEM_OK;

@@ -102,7 +102,7 @@ struct PutArgs {
   const unsigned long long* cons_hi;
   const double* recv_lo;   // my receive slots (this parity)
   const double* recv_hi;
-  unsigned long long* my;  // my flags [lo filled, hi filled, consumed, arrivals]
+  unsigned long long* my;  // my flags [lo filled, hi filled, consumed, -, up, down, barrier x2]
   unsigned long long seq;  // this exchange's number (1, 2, ...)
   int bcmode;
 };
@@ -111,15 +111,20 @@ struct PutArgs {
 // initiated communication"): (1) once the neighbour has
 // consumed the previous use of this parity's slot, write my boundary planes
 // straight into its receive slots through peer pointers (NVLink stores);
-// (2) the last block to finish raises the neighbours' "filled" flags with a
-// system-scope release; (3) every block waits for my own slots to be filled and
-// for all my blocks to have read my planes, then adds the received planes
-// (Dirichlet rows re-imposed); (4) the last block publishes "consumed".
+// (2) after a grid barrier (every block wrote and read my planes) block 0
+// raises the neighbours' "filled" flags with a system-scope release; (3) every
+// block waits for my own slots to be filled, then adds the received planes
+// (Dirichlet rows re-imposed); (4) after a second barrier block 0 publishes
+// "consumed".  Flags: [0] lo filled, [1] hi filled, [2] consumed, [4..5] the
+// persistent CG's chain allreduce, [6..7] this kernel's grid barrier.
 // Small cooperative grid: co-resident, and it leaves room for the other ranks'
 // kernels when several ranks share one device (loopback).
 __global__ void __launch_bounds__(256) plane_put_kernel(PutArgs P) {
   const long long st = (long long)gridDim.x * blockDim.x;
   const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  // the kernel's own self-resetting grid barrier in flags [6..7] (independent of
+  // the exchange numbering, which the persistent CG kernel shares)
+  GridBar* bar = reinterpret_cast<GridBar*>(P.my + 6);
   if (threadIdx.x == 0) {
     if (P.put_lo && P.seq > 2) spin_until(P.cons_lo, P.seq - 2);
     if (P.put_hi && P.seq > 2) spin_until(P.cons_hi, P.seq - 2);
@@ -130,20 +135,15 @@ __global__ void __launch_bounds__(256) plane_put_kernel(PutArgs P) {
     if (P.put_hi) P.put_hi[i] = P.yhi[i];
   }
   __syncthreads();
-  __shared__ bool last;
+  if (threadIdx.x == 0) __threadfence_system();
+  grid_barrier(bar);  // every block's planes are written (and read)
   if (threadIdx.x == 0) {
-    __threadfence_system();
-    // arrivals: 2 per block per exchange, so exchange seq's first round ends at
-    // 2 G (seq - 1) + G and its second round at 2 G seq
-    const unsigned long long G = gridDim.x, first = 2ull * G * (P.seq - 1) + G;
-    const unsigned long long a = atomicAdd(P.my + 3, 1ull) + 1;
-    last = (a == first);
-    if (last) {
+    if (blockIdx.x == 0) {
+      __threadfence_system();
       if (P.put_lo) st_rel_sys(P.flag_lo, P.seq);
       if (P.put_hi) st_rel_sys(P.flag_hi, P.seq);
     }
-    // my planes read by every block, neighbours' planes arrived
-    spin_until(P.my + 3, first);
+    // neighbours' planes arrived
     if (P.put_lo) spin_until(P.my + 0, P.seq);
     if (P.put_hi) spin_until(P.my + 1, P.seq);
   }
@@ -165,11 +165,9 @@ __global__ void __launch_bounds__(256) plane_put_kernel(PutArgs P) {
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    const unsigned long long a = atomicAdd(P.my + 3, 1ull) + 1;
-    if (a == 2ull * gridDim.x * P.seq) st_rel_sys(P.my + 2, P.seq);  // consumed
-  }
+  if (threadIdx.x == 0) __threadfence_system();
+  grid_barrier(bar);  // every block added its received planes
+  if (blockIdx.x == 0 && threadIdx.x == 0) st_rel_sys(P.my + 2, P.seq);  // consumed
 }
 
 }  // namespace
@@ -181,7 +179,8 @@ hofem_status mesh_set_exchange(Mesh* m, int mode, cudaStream_t s) {
   if (mode == 0) { m->xmode = 0; return HOFEM_OK; }
   const int r = m->rank, R = m->nranks;
   if (!m->d_xrecv) {
-    if (cudaMalloc(&m->d_xrecv, sizeof(double) * 4 * m->plane) != cudaSuccess ||
+    // 2 parities x [lo | hi] planes, then the chain-allreduce slots (up, down)
+    if (cudaMalloc(&m->d_xrecv, sizeof(double) * (4 * m->plane + 8)) != cudaSuccess ||
         cudaMalloc(&m->d_xflag, sizeof(unsigned long long) * 8) != cudaSuccess) {
       cudaGetLastError();
       set_error("hofem_mesh_set_exchange: out of device memory");

@@ -394,15 +394,19 @@ hofem_status cg_persistent(Op* op, double* x, double* r, double* p, double* Ap, 
                            int max_iter, int fixed, double rel_tol, int* d_result,
                            cudaStream_t s) {
   Mesh* m = op->mesh;
-  if (m->nranks != 1 || !fused_supported(op)) {
-    set_error("persistent CG: single rank, fused operator only");
+  const bool multi = m->nranks > 1;
+  if (!fused_supported(op) || (multi && m->xmode != 1)) {
+    set_error("persistent CG: fused operator; several ranks need the kernel-initiated "
+              "exchange (hofem_mesh_set_exchange mode 1)");
     return HOFEM_ERR_ARG;
   }
   Prepared R;
   HOFEM_TRY(prepare(op, p, Ap, false, &R, s, true));
-  const Plan& PL = R.PL;
+  Plan& PL = R.PL;
+  // loopback: all ranks' grids share one device and must be co-resident
+  if (multi && m->comm && m->comm->loop) PL.grid = std::max(1, PL.grid / m->nranks);
   HOFEM_TRY(ensure_bar(op, s));
-  HOFEM_TRY(grow(&op->d_cgparts, &op->cgparts_len, 2LL * PL.grid, "the CG partials", s));
+  HOFEM_TRY(grow(&op->d_cgparts, &op->cgparts_len, 2LL * PL.grid + 2, "the CG partials", s));
   ColArgs& A = R.A;
   A.infix = 1;
   A.zero_n = 0;  // the CG kernel zeroes Ap itself
@@ -413,6 +417,7 @@ hofem_status cg_persistent(Op* op, double* x, double* r, double* p, double* Ap, 
   A.fx.dotp = nullptr;
   CGArgs G;
   G.n = m->n_local;
+  G.n_owned = m->n_owned;
   G.x = x; G.r = r; G.p = p; G.Ap = Ap; G.rr = rr;
   G.parts = op->d_cgparts;
   G.parts2 = op->d_cgparts + PL.grid;
@@ -421,6 +426,27 @@ hofem_status cg_persistent(Op* op, double* x, double* r, double* p, double* Ap, 
   G.fixed = fixed;
   G.rel_tol = rel_tol;
   G.zero_ap = R.zero_y ? 1 : 0;
+  G.multi = multi ? 1 : 0;
+  G.X = XArgs{};
+  if (multi) {
+    XArgs& X = G.X;
+    X.R = m->nranks;
+    X.rank = m->rank;
+    X.plane = m->plane;
+    X.Nx = m->Nx; X.Ny = m->Ny; X.NzG = m->NzG;
+    X.Klo = (long long)m->p * m->z0;
+    X.Khi = X.Klo + m->Nzl - 1;
+    X.peer_lo = m->peer_recv[0];
+    X.peer_hi = m->peer_recv[1];
+    X.pflag_lo = m->peer_flag[0];
+    X.pflag_hi = m->peer_flag[1];
+    X.recv = m->d_xrecv;
+    X.my = m->d_xflag;
+    X.seq0 = m->xseq;
+    X.rseq0 = m->rseq;
+    X.scratch = op->d_cgparts + 2 * PL.grid;
+    X.bcmode = op->bc ? 1 : 0;
+  }
   cudaError_t err = cudaSuccess;
   bool ok = false;
   switch (m->P1) {

@@ -1498,8 +1498,32 @@ __global__ void __maxnreg__(MAXR)
 // they agree bitwise and take the same stop decision (tolerance, breakdown) --
 // no host round trip, no launch gaps.  Deterministic run to run.
 // ---------------------------------------------------------------------------
+// Multi-rank persistent CG (kernel-initiated communication, PAPER.md:197,
+// §2.3): the interface planes of Ap go straight into the z neighbours' receive
+// slots through peer pointers (the hofem_mesh_set_exchange(mode 1) buffers and
+// flag protocol), and p.Ap / r.r are allreduced inside the kernel by a chain
+// over the z neighbours -- up: s_r = s_{r-1} + v_r (fixed rank order), down:
+// the top rank's total back to every rank -- so every rank gets bitwise the same
+// scalar without leaving the kernel.
+struct XArgs {
+  int R, rank;
+  long long plane, Nx, Ny, NzG, Klo, Khi;
+  double* peer_lo;                   // lower neighbour's receive buffer (null at rank 0)
+  double* peer_hi;                   // upper neighbour's receive buffer (null at the top)
+  unsigned long long* pflag_lo;      // lower / upper neighbour's flags
+  unsigned long long* pflag_hi;
+  double* recv;                      // my receive buffer: 2 parities x [lo | hi] planes, then
+                                     // [4P] = up slot, [4P+1] = down slot
+  unsigned long long* my;            // my flags: [0] lo filled, [1] hi filled, [2] consumed,
+                                     // [4] up value ready, [5] down value ready
+  unsigned long long seq0, rseq0;    // exchanges / chain reductions done before this launch
+  double* scratch;                   // my device scalar for the reduced value
+  int bcmode;                        // Dirichlet rows of the summed planes: 1 y = x
+};
+
 struct CGArgs {
-  long long n;           // local vector length (single rank: all owned)
+  long long n;           // local vector length
+  long long n_owned;     // local dofs this rank owns (dot products, R8-R9)
   double* x;
   double* r;
   double* p;             // == ColArgs::x
@@ -1507,10 +1531,13 @@ struct CGArgs {
   double* rr;            // rr[0] (input, r0.r0) .. rr[k] (output)
   double* parts;         // [gridDim.x] p.Ap partials
   double* parts2;        // [gridDim.x] r.r partials
-  int* result;           // [0] iterations done, [1] 1 = breakdown (p.Ap <= 0)
+  int* result;           // [0] iterations done, [1] 1 = breakdown (p.Ap <= 0),
+                         // [2] exchanges, [3] chain reductions performed (multi-rank)
   int max_iter, fixed;
   double rel_tol;
   int zero_ap;           // Ap must be zero before each pass (face reductions)
+  int multi;             // 1: multi-rank (X below)
+  XArgs X;
 };
 
 // Fixed-order sum of gridDim.x partials; every thread of every CTA gets the same
@@ -1533,8 +1560,8 @@ __device__ __forceinline__ double grid_sum(const double* parts, double* red) {
 constexpr int CGU = 2;
 
 // r -= alpha Ap; returns this thread's share of r.r
-static __device__ __noinline__ double cg_r_update(long long n, double alpha, const double* Ap,
-                                           double* r) {
+static __device__ __noinline__ double cg_r_update(long long n, long long no, double alpha,
+                                                  const double* Ap, double* r) {
   const long long st = (long long)gridDim.x * blockDim.x;
   const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long np = n >> 1;
@@ -1555,15 +1582,15 @@ static __device__ __noinline__ double cg_r_update(long long n, double alpha, con
         v[u].x = fma(-alpha, a[u].x, v[u].x);
         v[u].y = fma(-alpha, a[u].y, v[u].y);
         r2[i] = v[u];
-        s = fma(v[u].x, v[u].x, s);
-        s = fma(v[u].y, v[u].y, s);
+        if (2 * i < no) s = fma(v[u].x, v[u].x, s);  // owned dofs only (R8-R9)
+        if (2 * i + 1 < no) s = fma(v[u].y, v[u].y, s);
       }
     }
   }
   if ((n & 1) && t0 == 0) {
     const double v = fma(-alpha, __ldcg(Ap + n - 1), r[n - 1]);
     r[n - 1] = v;
-    s = fma(v, v, s);
+    if (n - 1 < no) s = fma(v, v, s);
   }
   return s;
 }
@@ -1608,6 +1635,113 @@ static __device__ __noinline__ void cg_xp_update(long long n, double alpha, doub
   }
 }
 
+__device__ __forceinline__ unsigned long long px_ld_acq(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void px_st_rel(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void px_spin(const unsigned long long* p, unsigned long long v) {
+  const unsigned long long t0 = global_ns();
+  unsigned spins = 0;
+  while (px_ld_acq(p) < v) {
+    if ((++spins & 1023u) == 0u && global_ns() - t0 > 20000000000ull) __trap();  // 20 s
+    __nanosleep(64);
+  }
+}
+
+// In-kernel interface exchange of y's boundary planes (all CTAs; mirrors
+// plane_put_kernel in comm.cu, same slots, flags and sequence numbers): wait
+// until the neighbours consumed this parity's previous use, put my planes into
+// their slots, raise their "filled" flags, wait for mine, add the received
+// planes (Dirichlet rows re-imposed, y = x), publish "consumed".
+static __device__ __noinline__ void px_exchange(const XArgs& X, double* y, const double* x,
+                                         unsigned long long seq, GridBar* bar) {
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  const long long P = X.plane;
+  const long long par = (long long)(seq & 1ull) * 2 * P;
+  if (lead) {
+    if (X.peer_lo && seq > 2) px_spin(X.pflag_lo + 2, seq - 2);
+    if (X.peer_hi && seq > 2) px_spin(X.pflag_hi + 2, seq - 2);
+  }
+  grid_barrier(bar);
+  double* ylo = y;
+  double* yhi = y + (X.Khi - X.Klo) * P;
+  const long long st = (long long)gridDim.x * blockDim.x;
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (long long i = t0; i < P; i += st) {
+    if (X.peer_lo) X.peer_lo[par + P + i] = ylo[i];  // the lower rank's "hi" slot
+    if (X.peer_hi) X.peer_hi[par + i] = yhi[i];      // the upper rank's "lo" slot
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
+  grid_barrier(bar);
+  if (lead) {
+    __threadfence_system();
+    if (X.peer_lo) px_st_rel(X.pflag_lo + 1, seq);
+    if (X.peer_hi) px_st_rel(X.pflag_hi + 0, seq);
+    if (X.peer_lo) px_spin(X.my + 0, seq);
+    if (X.peer_hi) px_spin(X.my + 1, seq);
+  }
+  grid_barrier(bar);
+  const double* xlo = x;
+  const double* xhi = x + (X.Khi - X.Klo) * P;
+  for (long long i = t0; i < P; i += st) {
+    const long long I = i % X.Nx, J = i / X.Nx;
+    const bool side = I == 0 || I == X.Nx - 1 || J == 0 || J == X.Ny - 1;
+    if (X.peer_lo) {
+      double v = ylo[i] + __ldcv(X.recv + par + i);
+      if (X.bcmode == 1 && (side || X.Klo == 0 || X.Klo == X.NzG - 1)) v = xlo[i];
+      ylo[i] = v;
+    }
+    if (X.peer_hi) {
+      double v = yhi[i] + __ldcv(X.recv + par + P + i);
+      if (X.bcmode == 1 && (side || X.Khi == 0 || X.Khi == X.NzG - 1)) v = xhi[i];
+      yhi[i] = v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
+  grid_barrier(bar);
+  if (lead) px_st_rel(X.my + 2, seq);  // consumed
+}
+
+// In-kernel allreduce of v (the same value in every thread of this rank) over
+// the ranks: chain up (s_r = s_{r-1} + v_r), the top rank's total back down;
+// the leader runs the chain, every thread returns the total after a grid barrier.
+static __device__ __noinline__ double px_allreduce(const XArgs& X, double v, unsigned long long c,
+                                            GridBar* bar) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long P = X.plane;
+    double s = v;
+    if (X.peer_lo) {
+      px_spin(X.my + 4, c);
+      s = __ldcv(X.recv + 4 * P) + v;  // lower ranks first: fixed order
+    }
+    double t;
+    if (X.peer_hi) {
+      X.peer_hi[4 * P] = s;            // the upper rank's up slot
+      __threadfence_system();
+      px_st_rel(X.pflag_hi + 4, c);
+      px_spin(X.my + 5, c);
+      t = __ldcv(X.recv + 4 * P + 1);
+    } else {
+      t = s;                           // the top rank holds the total
+    }
+    if (X.peer_lo) {
+      X.peer_lo[4 * P + 1] = t;        // the lower rank's down slot
+      __threadfence_system();
+      px_st_rel(X.pflag_lo + 5, c);
+    }
+    *X.scratch = t;
+    __threadfence();
+  }
+  grid_barrier(bar);
+  return __ldcg(X.scratch);
+}
+
 template <int KIND, int P1, int Q, int BX, int BY, int NT, int MAXR, bool EO>
 __global__ void __maxnreg__(MAXR)
     cg_persistent_simt(const __grid_constant__ Tab<P1, Q> T, const __grid_constant__ ColArgs A,
@@ -1619,7 +1753,7 @@ __global__ void __maxnreg__(MAXR)
   // CG state (identical in every thread of every CTA) lives in shared memory
   // across the brick pass: registers held over simt_pass made it spill
   __shared__ double s_rr0, s_rr;
-  __shared__ int s_k, s_brk;
+  __shared__ int s_k, s_brk, s_nx, s_nr;  // iterations, breakdown, exchanges, reductions
   {
     const long long st = (long long)gridDim.x * NT;
     const long long t0 = (long long)blockIdx.x * NT + threadIdx.x;
@@ -1630,6 +1764,8 @@ __global__ void __maxnreg__(MAXR)
     s_rr0 = s_rr = __ldcg(G.rr);
     s_k = 0;
     s_brk = 0;
+    s_nx = 0;
+    s_nr = 0;
   }
   grid_barrier(A.bar);  // (also orders the shared stores for the CTA)
   for (;;) {
@@ -1641,19 +1777,34 @@ __global__ void __maxnreg__(MAXR)
     const long long t0 = (long long)blockIdx.x * NT + threadIdx.x;
     const long long nfx = fixup_count(A.fx);
     for (long long g = t0; g < nfx; g += st) dsum += fixup_flat(A.fx, g);
+    if (G.multi) {  // Ap's interface planes: neighbours' contributions added in-kernel
+      px_exchange(G.X, G.Ap, G.p, G.X.seq0 + (unsigned long long)s_nx + 1, A.bar);
+      __syncthreads();
+      if (threadIdx.x == 0) ++s_nx;
+    }
     block_sum_store(dsum, G.parts + blockIdx.x, smem);
     grid_barrier(A.bar);
-    const double pAp = grid_sum<NT>(G.parts, smem);
-    if (!(pAp > 0.0)) {  // same value in every CTA: all stop here
+    double pAp = grid_sum<NT>(G.parts, smem);
+    if (G.multi) {
+      pAp = px_allreduce(G.X, pAp, G.X.rseq0 + (unsigned long long)s_nr + 1, A.bar);
+      __syncthreads();
+      if (threadIdx.x == 0) ++s_nr;
+    }
+    if (!(pAp > 0.0)) {  // same value in every CTA (and rank): all stop here
       if (threadIdx.x == 0) s_brk = 1;
       break;
     }
     const double rr = s_rr;
     const double alpha = rr / pAp;
-    const double sr = cg_r_update(G.n, alpha, G.Ap, G.r);
+    const double sr = cg_r_update(G.n, G.n_owned, alpha, G.Ap, G.r);
     block_sum_store(sr, G.parts2 + blockIdx.x, smem);
     grid_barrier(A.bar);
-    const double rn = grid_sum<NT>(G.parts2, smem);  // every thread has read s_rr
+    double rn = grid_sum<NT>(G.parts2, smem);  // every thread has read s_rr
+    if (G.multi) {
+      rn = px_allreduce(G.X, rn, G.X.rseq0 + (unsigned long long)s_nr + 1, A.bar);
+      __syncthreads();
+      if (threadIdx.x == 0) ++s_nr;
+    }
     const double beta = rr > 0.0 ? rn / rr : 0.0;
     cg_xp_update(G.n, alpha, beta, G.x, G.p, G.r, G.Ap, G.zero_ap);
     const int k = s_k + 1;
@@ -1671,6 +1822,8 @@ __global__ void __maxnreg__(MAXR)
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     G.result[0] = s_k;
     G.result[1] = s_brk;
+    G.result[2] = s_nx;
+    G.result[3] = s_nr;
   }
 }
 

@@ -90,11 +90,12 @@ struct Mesh {
   // consumed (read by the neighbours before reusing a parity slot)
   int xmode = 0;                            // 0 collective (NCCL / loopback copies), 1 peer puts
   double* d_xrecv = nullptr;                // 4 planes
-  unsigned long long* d_xflag = nullptr;    // [lo filled, hi filled, consumed, arrivals]
+  unsigned long long* d_xflag = nullptr;    // [lo filled, hi filled, consumed, -, chain up, chain down, put-kernel barrier x2]
   double* peer_recv[2] = {nullptr, nullptr};               // lower / upper neighbour's d_xrecv
   unsigned long long* peer_flag[2] = {nullptr, nullptr};   // lower / upper neighbour's d_xflag
   bool peer_ipc[2] = {false, false};        // opened with cudaIpcOpenMemHandle
   unsigned long long xseq = 0;              // exchanges issued
+  unsigned long long rseq = 0;              // in-kernel chain allreduces (persistent CG)
 };
 
 // Grid-wide barrier state of a cooperative launch: arrival count and

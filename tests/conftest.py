@@ -4,6 +4,12 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# Load every kernel module when the CUDA context is created: with lazy loading a
+# kernel's first use may synchronize the context, which deadlocks the loopback
+# transport's kernel-initiated exchange (a neighbour's put / persistent CG kernel
+# spins on this rank while the load waits for it; hofem.h, set_exchange).
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 

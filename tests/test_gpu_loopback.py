@@ -218,3 +218,63 @@ def test_loopback_peer_puts_back_to_back(hf):
     for ref, ys in res:
         for y in ys:
             assert np.array_equal(y.view(np.uint64), ref.view(np.uint64))
+
+
+@pytest.mark.parametrize("R,p,dims", [(2, 3, (3, 2, 4)), (3, 2, (3, 3, 6)), (2, 5, (2, 3, 4))])
+def test_loopback_persistent_cg_in_kernel_exchange(hf, R, p, dims):
+    """The whole multi-rank CG in ONE persistent kernel per rank (§8(f) f1;
+    PAPER.md:177-182, 197): the interface planes of Ap are put into the z
+    neighbours' slots and p.Ap / r.r are allreduced (chain over the ranks) inside
+    the kernel.  Iterates and the converged solution against the global oracle;
+    afterwards a host-driven apply and a second solve still agree (the kernel
+    continues the mesh's exchange and reduction sequence numbers)."""
+    nx, ny, nz = dims
+    nzl = nz // R
+    plane = (p * nx + 1) * (p * ny + 1)
+    om = O.Mesh(nx, ny, nz, p, alpha=0.1)
+    Ae = O.element_matrices(om, hf.DIFFUSION, hf.GAUSS)
+    bg = O.rhs(om, hf.DIFFUSION, hf.GAUSS, bc=1)
+    ks = [1, 3, 9]
+    _, _, _, _, xh = O.cg(bg, m=om, Ae=Ae, bc=1, max_iter=max(ks), fixed_iters=True, history=True)
+    xo, st, kconv, _, _ = O.cg(bg, m=om, Ae=Ae, bc=1, rel_tol=1e-13, max_iter=1000)
+    xg = W.random_vector(5, np.arange(om.n_dofs))
+    yg = O.apply_ea(om, Ae, xg, bc=1)
+
+    def fn(r, comm, s):
+        m = hf.Mesh(nx, ny, nz, p, alpha=0.1, comm=comm, stream=s)
+        op = hf.Operator(m, kind=hf.DIFFUSION, rule=hf.GAUSS, bc=1, stream=s)
+        op.set_option(hf.OPT_CG_PERSISTENT, hf.ALWAYS)
+        xs = {k: torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
+              for k in ks + ["conv", "again"]}
+        b = torch.empty_like(xs["conv"])
+        xa = m.random(5, stream=s)
+        ya = torch.empty_like(xa)
+        s.synchronize()
+        m.set_exchange(1, stream=s)
+        op.rhs(b, stream=s)
+        out = {}
+        for k in ks:
+            st, stats, _ = op.cg(b, xs[k], max_iter=k, fixed_iters=True, stream=s)
+            out[k] = (st, stats.iterations, host(xs[k]))
+        st, stats, _ = op.cg(b, xs["conv"], rel_tol=1e-13, max_iter=1000, stream=s)
+        out["conv"] = (st, stats.iterations, host(xs["conv"]))
+        op.apply(xa, ya, stream=s)  # host-driven peer-put exchange after the kernels
+        out["y"] = host(ya)
+        st, stats, _ = op.cg(b, xs["again"], max_iter=ks[-1], fixed_iters=True, stream=s)
+        out["again"] = host(xs["again"])
+        return out
+
+    res = run_ranks(hf, R, fn)
+    for r in range(R):
+        for k in ks:
+            st_k, it_k, x_k = res[r][k]
+            assert st_k == 0 and it_k == k
+            assert rel(x_k, slab(xh[k], plane, p, nzl, r)) <= 1e-10, (r, k)
+        st_r, it_r, x_r = res[r]["conv"]
+        assert st_r == 0 and abs(it_r - kconv) <= 2
+        assert rel(x_r, slab(xo, plane, p, nzl, r)) <= 1e-11
+        assert rel(res[r]["y"], slab(yg, plane, p, nzl, r)) <= 1e-12
+        assert np.array_equal(res[r]["again"].view(np.uint64), res[r][ks[-1]][2].view(np.uint64))
+        if r + 1 < R:  # duplicated interface plane: the same iterate on both ranks
+            assert np.array_equal(res[r]["conv"][2][-plane:].view(np.uint64),
+                                  res[r + 1]["conv"][2][:plane].view(np.uint64))
