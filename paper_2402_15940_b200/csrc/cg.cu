@@ -357,13 +357,21 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
       m->xseq += (unsigned long long)res[2];  // the kernel's exchanges / chain reductions
       m->rseq += (unsigned long long)res[3];
       double rr_last = rr0;
-      if (k > 0) HOFEM_CUDA(cudaMemcpy(&rr_last, rr + k, sizeof(double), cudaMemcpyDeviceToHost));
+      // stream-ordered copies only: a legacy-stream cudaMemcpy could wait on
+      // another loopback rank's spinning kernel
+      if (k > 0) {
+        HOFEM_CUDA(cudaMemcpyAsync(&rr_last, rr + k, sizeof(double), cudaMemcpyDeviceToHost, s));
+        HOFEM_CUDA(cudaStreamSynchronize(s));
+      }
       hofem_status status = HOFEM_OK;
       if (res[1]) status = HOFEM_ERR_BREAKDOWN;
       else if (!fixed_iters && !(rr_last == 0.0 || sqrt(rr_last) <= rel_tol * sqrt(rr0)))
         status = HOFEM_NOT_CONVERGED;
-      if (rr_history)
-        HOFEM_CUDA(cudaMemcpy(rr_history, rr, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost));
+      if (rr_history) {
+        HOFEM_CUDA(cudaMemcpyAsync(rr_history, rr, sizeof(double) * (k + 1),
+                                   cudaMemcpyDeviceToHost, s));
+        HOFEM_CUDA(cudaStreamSynchronize(s));
+      }
       if (stats) {
         stats->iterations = k;
         stats->converged = status == HOFEM_OK ? 1 : 0;

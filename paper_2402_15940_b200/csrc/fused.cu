@@ -403,8 +403,10 @@ hofem_status cg_persistent(Op* op, double* x, double* r, double* p, double* Ap, 
   Prepared R;
   HOFEM_TRY(prepare(op, p, Ap, false, &R, s, true));
   Plan& PL = R.PL;
-  // loopback: all ranks' grids share one device and must be co-resident
-  if (multi && m->comm && m->comm->loop) PL.grid = std::max(1, PL.grid / m->nranks);
+  // loopback: all ranks' grids share one device and must be co-resident; 1/(R+1)
+  // of the device each leaves room for the other ranks' put kernels and the
+  // waves of their (non-cooperative) brick kernels
+  if (multi && m->comm && m->comm->loop) PL.grid = std::max(1, PL.grid / (m->nranks + 1));
   HOFEM_TRY(ensure_bar(op, s));
   HOFEM_TRY(grow(&op->d_cgparts, &op->cgparts_len, 2LL * PL.grid + 2, "the CG partials", s));
   ColArgs& A = R.A;

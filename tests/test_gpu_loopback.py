@@ -220,29 +220,34 @@ def test_loopback_peer_puts_back_to_back(hf):
             assert np.array_equal(y.view(np.uint64), ref.view(np.uint64))
 
 
-@pytest.mark.parametrize("R,p,dims", [(2, 3, (3, 2, 4)), (3, 2, (3, 3, 6)), (2, 5, (2, 3, 4))])
-def test_loopback_persistent_cg_in_kernel_exchange(hf, R, p, dims):
+@pytest.mark.parametrize("R,bench,p,dims", [(2, "bp3", 3, (3, 2, 4)), (3, "bp3", 2, (3, 3, 6)),
+                                            (2, "bp3", 5, (2, 3, 4)), (2, "bp5", 4, (3, 2, 4)),
+                                            (3, "bp1", 3, (2, 3, 3))])
+def test_loopback_persistent_cg_in_kernel_exchange(hf, R, bench, p, dims):
     """The whole multi-rank CG in ONE persistent kernel per rank (§8(f) f1;
     PAPER.md:177-182, 197): the interface planes of Ap are put into the z
     neighbours' slots and p.Ap / r.r are allreduced (chain over the ranks) inside
     the kernel.  Iterates and the converged solution against the global oracle;
     afterwards a host-driven apply and a second solve still agree (the kernel
     continues the mesh's exchange and reduction sequence numbers)."""
+    kind, rule = KINDS[bench]
+    bc = 0 if bench == "bp1" else 1
     nx, ny, nz = dims
     nzl = nz // R
     plane = (p * nx + 1) * (p * ny + 1)
     om = O.Mesh(nx, ny, nz, p, alpha=0.1)
-    Ae = O.element_matrices(om, hf.DIFFUSION, hf.GAUSS)
-    bg = O.rhs(om, hf.DIFFUSION, hf.GAUSS, bc=1)
+    Ae = O.element_matrices(om, kind, rule)
+    bg = O.rhs(om, kind, rule, bc=bc)
     ks = [1, 3, 9]
-    _, _, _, _, xh = O.cg(bg, m=om, Ae=Ae, bc=1, max_iter=max(ks), fixed_iters=True, history=True)
-    xo, st, kconv, _, _ = O.cg(bg, m=om, Ae=Ae, bc=1, rel_tol=1e-13, max_iter=1000)
+    _, _, _, _, xh = O.cg(bg, m=om, Ae=Ae, bc=bc, max_iter=max(ks), fixed_iters=True,
+                          history=True)
+    xo, st, kconv, _, _ = O.cg(bg, m=om, Ae=Ae, bc=bc, rel_tol=1e-13, max_iter=1000)
     xg = W.random_vector(5, np.arange(om.n_dofs))
-    yg = O.apply_ea(om, Ae, xg, bc=1)
+    yg = O.apply_ea(om, Ae, xg, bc=bc)
 
     def fn(r, comm, s):
         m = hf.Mesh(nx, ny, nz, p, alpha=0.1, comm=comm, stream=s)
-        op = hf.Operator(m, kind=hf.DIFFUSION, rule=hf.GAUSS, bc=1, stream=s)
+        op = hf.Operator(m, kind=kind, rule=rule, bc=bc, stream=s)
         op.set_option(hf.OPT_CG_PERSISTENT, hf.ALWAYS)
         xs = {k: torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
               for k in ks + ["conv", "again"]}
