@@ -151,11 +151,13 @@ def test_loopback_apply_rhs_dot_match_global(hf, R, bench, p, dims, bc, xmode):
     assert abs(res[0]["xx"] - float(xg @ xg)) <= 1e-12 * float(xg @ xg)
 
 
-@pytest.mark.parametrize("xmode", [0, 1])
+@pytest.mark.parametrize("xmode,persist", [(0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("R,bench,p,dims", [(2, "bp3", 3, (3, 2, 4)), (3, "bp3", 2, (3, 3, 6))])
-def test_loopback_cg_iterates_match_global(hf, R, bench, p, dims, xmode):
-    """Multi-rank CG (separate vector kernels, NCCL-path scalars via the loopback
-    allreduce) against the global oracle CG iterates."""
+def test_loopback_cg_iterates_match_global(hf, R, bench, p, dims, xmode, persist):
+    """Multi-rank CG against the global oracle CG iterates: per-iteration kernels
+    with the scalars through the loopback allreduce (either exchange transport),
+    and -- with the kernel-initiated exchange and the auto setting -- the
+    persistent kernel with the in-kernel exchange and chain allreduce."""
     kind, rule = KINDS[bench]
     nx, ny, nz = dims
     nzl = nz // R
@@ -170,6 +172,7 @@ def test_loopback_cg_iterates_match_global(hf, R, bench, p, dims, xmode):
     def fn(r, comm, s):
         m = hf.Mesh(nx, ny, nz, p, alpha=0.1, comm=comm, stream=s)
         op = hf.Operator(m, kind=kind, rule=rule, bc=1, stream=s)
+        op.set_option(hf.OPT_CG_PERSISTENT, persist)  # 0 never, 1 auto
         xs = {k: torch.zeros(m.n_local, dtype=torch.float64, device="cuda")
               for k in ks + ["conv"]}
         b = torch.empty_like(xs["conv"])
