@@ -248,15 +248,22 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 __device__ __forceinline__ void grid_barrier(GridBar* bar) {
+  // thread 0 carries the CTA: bar.sync orders the CTA's memory operations, the
+  // acq_rel arrival releases them to / acquires the other CTAs' at gpu scope,
+  // and the generation flip is a release store read with acquire loads -- no
+  // separate fences (measured: 3.07 -> 2.14 us per barrier at 444 CTAs,
+  // scratch microbenchmark, DESIGN.md §4 CG)
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned int g;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(&bar->gen) : "memory");
-    __threadfence();
-    const unsigned int arrived = atomicAdd(&bar->count, 1u);
+    unsigned int arrived;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(arrived)
+                 : "l"(&bar->count)
+                 : "memory");
     if (arrived == gridDim.x - 1) {
-      bar->count = 0u;
-      __threadfence();
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(&bar->count) : "memory");
       asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&bar->gen), "r"(g + 1u) : "memory");
     } else {
       const unsigned long long t0 = global_ns();
@@ -269,7 +276,6 @@ __device__ __forceinline__ void grid_barrier(GridBar* bar) {
         __nanosleep(32);
       }
     }
-    __threadfence();
   }
   __syncthreads();
 }
