@@ -21,6 +21,9 @@ MODES = {
     "persistent": {hf.OPT_CG_PERSISTENT: 2},
     "fused": {hf.OPT_CG_PERSISTENT: 0, hf.OPT_CG_FUSED_UPDATE: 2, hf.OPT_INFIX: 2},
     "separate": {hf.OPT_CG_PERSISTENT: 0, hf.OPT_CG_FUSED_UPDATE: 0, hf.OPT_INFIX: 0},
+    "infix_only": {hf.OPT_CG_PERSISTENT: 0, hf.OPT_CG_FUSED_UPDATE: 0, hf.OPT_INFIX: 2},
+    "upd_only": {hf.OPT_CG_PERSISTENT: 0, hf.OPT_CG_FUSED_UPDATE: 2, hf.OPT_INFIX: 0},
+    "auto": {hf.OPT_CG_PERSISTENT: 1, hf.OPT_CG_FUSED_UPDATE: 1, hf.OPT_INFIX: 1},
 }
 
 
