@@ -1,31 +1,33 @@
 // fused_impl.cuh -- the fused sm_100a operator kernels (SURVEY.md §8(a) rows
 // a4-a9; north star "one fused sm_100a kernel per operator").
 //
-// Persistent "column" kernel: one CTA per SM.  A work unit is a column of
-// bricks -- BX*BY elements in x,y by one element layer in z -- over a chunk of zc
-// element layers; the CTA streams the column bottom to top.  Per brick it does:
+// Persistent "column" kernel: a grid of SMs x (resident CTAs per SM) CTAs (the
+// residency from the occupancy API).  A work unit is a column of bricks --
+// BX*BY elements in x,y by one element layer in z -- over a chunk of zc element
+// layers; the CTA streams the column bottom to top.  Per brick it does:
 //   a4  gather R: the brick's (p*BX+1)(p*BY+1)(p+1) lattice of x, read with
 //       asynchronous 8-byte copies into a double-buffered shared-memory lattice
 //       (the NEXT brick's lattice is in flight while this one computes);
 //       Dirichlet dofs and out-of-mesh points are zero-filled (reading R6);
 //   a5  B: the 1D B1d/G1d contractions dimension by dimension (x, then y in
 //       shared memory; z in registers, one thread per (qx,qy) quadrature column);
-//   a6  D: the pointwise qdata.  Each stage-3 thread holds its column's qdata for
-//       the NEXT brick in registers, loaded (L2 evict-first, coalesced) right
-//       after it consumed the current one -- the dominant HBM stream is always
-//       one brick ahead of the math, without spending shared memory on it;
+//   a6  D: the pointwise qdata, streamed from L2 into registers inside stage 3
+//       (the next point pairs' loads in flight while a pair computes); the
+//       brick's qdata was bulk-prefetched into L2 one brick ahead, so the
+//       dominant HBM stream runs ahead of the math without shared memory (D is
+//       staged in shared memory by bulk copies only at P1 = 9);
 //   a7  B^T: the transposed contractions (z in registers, then y, x in smem);
 //   a8  R^T: a deterministic in-brick sum -- every brick lattice point sums its
 //       1..4 element contributions in ascending element order; the top lattice
 //       plane is carried in shared memory and added (in fixed order) to the
 //       bottom plane of the next brick of the column, so z-faces inside a unit
-//       never leave the SM.  Points on an interior x/y brick face (or a unit
-//       boundary plane) go to a per-brick partial buffer that fixup_kernel
-//       (fused.cu) sums in ascending brick order; all others are written to y.
-//   a9  y[ess] = x[ess].
-// The 1D tables live in the kernel-parameter constant bank (every index is a
-// compile-time constant after unrolling, so DFMA takes them as uniform-register
-// operands: no shared-memory traffic for B/G).
+//       never leave the SM.  Points on exactly one shared brick face are added to
+//       the zeroed y by two order-independent reductions; points on two or three
+//       (the brick grid's edge lines) go to a per-brick partial buffer that the
+//       fix-up sums in ascending brick order; all others are stored to y.
+//   a9  y[ess] = x[ess] (the fix-up's boundary pass).
+// The 1D tables (even-odd halves) live in the kernel-parameter constant bank and
+// are read as uniform constant loads (no shared-memory traffic for B/G).
 //
 // Shared-memory layouts keep consecutive lanes on consecutive or odd-strided
 // doubles (conflict-free 64-bit accesses): see DESIGN.md §4.
