@@ -225,7 +225,7 @@ def test_loopback_peer_puts_back_to_back(hf):
 
 @pytest.mark.parametrize("R,bench,p,dims", [(2, "bp3", 3, (3, 2, 4)), (3, "bp3", 2, (3, 3, 6)),
                                             (2, "bp3", 5, (2, 3, 4)), (2, "bp5", 4, (3, 2, 4)),
-                                            (3, "bp1", 3, (2, 3, 3))])
+                                            (3, "bp1", 3, (2, 3, 3)), (4, "bp3", 3, (2, 2, 8))])
 def test_loopback_persistent_cg_in_kernel_exchange(hf, R, bench, p, dims):
     """The whole multi-rank CG in ONE persistent kernel per rank (§8(f) f1;
     PAPER.md:177-182, 197): the interface planes of Ap are put into the z
