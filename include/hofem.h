@@ -136,7 +136,9 @@ void hofem_mesh_destroy(void* mesh);
  * synchronize the device, so on a loopback mesh create every object and
  * buffer before switching mode 1 on -- and load the kernel modules eagerly
  * (CUDA_MODULE_LOADING=EAGER): a kernel's first, lazy load may synchronize the
- * context as well.  With mode 1, hofem_cg's persistent schedule
+ * context as well; so may a device-to-host copy into PAGEABLE memory, so read
+ * results back after the ranks' last exchange (the library's own reads --
+ * dots, CG scalars -- go through pinned staging).  With mode 1, hofem_cg's persistent schedule
  * (HOFEM_OPT_CG_PERSISTENT) also runs on several ranks: the planes and both
  * dot products are then exchanged inside the one kernel per rank. */
 hofem_status hofem_mesh_set_exchange(void* mesh, int mode, void* stream);

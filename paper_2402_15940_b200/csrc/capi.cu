@@ -63,6 +63,7 @@ void free_mesh(Mesh* m) {
   cudaFree(m->d_l2e); cudaFree(m->d_toff); cudaFree(m->d_tidx);
   cudaFree(m->d_partials); cudaFree(m->d_counter); cudaFree(m->d_scalars);
   cudaFree(m->d_recv); cudaFree(m->d_send);
+  if (m->h_pin) cudaFreeHost(m->h_pin);
   delete m;
 }
 
@@ -135,6 +136,8 @@ hofem_status mesh_new(const hofem_mesh_desc* d, Comm* c, cudaStream_t stream, Me
   CK(dalloc(&m->d_counter, 4, "mesh"));
   CK(dalloc(&m->d_scalars, 16, "mesh"));
   if (R > 1) CK(dalloc(&m->d_recv, 2 * m->plane, "mesh planes"));
+  CK(cuda_status(cudaHostAlloc(reinterpret_cast<void**>(&m->h_pin), sizeof(double) * kPinDoubles,
+                               cudaHostAllocDefault), "mesh pinned staging"));
   CK(cuda_status(cudaMemcpyAsync(m->d_xi, xi, sizeof(double) * m->P1, cudaMemcpyHostToDevice,
                                  stream), "mesh upload"));
   CK(cuda_status(cudaMemsetAsync(m->d_counter, 0, 4 * sizeof(unsigned), stream), "memset"));
@@ -304,10 +307,7 @@ hofem_status hofem_op_apply_dot(void* op_, const double* x, double* y, double* d
     HOFEM_TRY(dot_local(m, x, y, m->d_scalars, S(stream)));
   }
   HOFEM_TRY(allreduce_sum(m, m->d_scalars, 1, S(stream)));
-  HOFEM_CUDA(cudaMemcpyAsync(dot_host, m->d_scalars, sizeof(double), cudaMemcpyDeviceToHost,
-                             S(stream)));
-  HOFEM_CUDA(cudaStreamSynchronize(S(stream)));
-  return HOFEM_OK;
+  return d2h(m, dot_host, m->d_scalars, sizeof(double), S(stream));
 }
 
 hofem_status hofem_op_apply_unfused(void* op_, const double* x, double* y, void* stream) {
@@ -498,10 +498,7 @@ hofem_status hofem_dot(const void* mesh, const double* a, const double* b, doubl
   if (!m || !a || !b || !out_host) { set_error("hofem_dot: NULL"); return HOFEM_ERR_ARG; }
   HOFEM_ALIGNED("hofem_dot", a, b);
   HOFEM_TRY(dot_device(m, a, b, m->d_scalars, S(stream)));
-  HOFEM_CUDA(cudaMemcpyAsync(out_host, m->d_scalars, sizeof(double), cudaMemcpyDeviceToHost,
-                             S(stream)));
-  HOFEM_CUDA(cudaStreamSynchronize(S(stream)));
-  return HOFEM_OK;
+  return d2h(m, out_host, m->d_scalars, sizeof(double), S(stream));
 }
 
 }  // extern "C"

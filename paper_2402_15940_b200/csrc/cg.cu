@@ -12,6 +12,7 @@
 // partials are ncclAllReduce'd on the same stream before use.
 #include <math.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 
@@ -277,6 +278,19 @@ __global__ void __launch_bounds__(kDotThreads) upd_fused_kernel(
 
 }  // namespace
 
+hofem_status d2h(Mesh* m, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  char* d = static_cast<char*>(dst);
+  const char* sp = static_cast<const char*>(src);
+  const size_t chunk = sizeof(double) * kPinDoubles;
+  for (size_t off = 0; off < bytes; off += chunk) {
+    const size_t nb = bytes - off < chunk ? bytes - off : chunk;
+    HOFEM_CUDA(cudaMemcpyAsync(m->h_pin, sp + off, nb, cudaMemcpyDeviceToHost, s));
+    HOFEM_CUDA(cudaStreamSynchronize(s));
+    memcpy(d + off, m->h_pin, nb);
+  }
+  return HOFEM_OK;
+}
+
 hofem_status dot_local(Mesh* m, const double* a, const double* b, double* d_out,
                        cudaStream_t s) {
   dot_kernel<<<kDotBlocks, kDotThreads, 0, s>>>(m->n_owned, a, b, m->d_partials, m->d_counter,
@@ -330,8 +344,7 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
   HOFEM_LAUNCHED();
   HOFEM_TRY(allreduce_sum(m, rr, 1, s));
   double rr0 = 0.0;
-  HOFEM_CUDA(cudaMemcpyAsync(&rr0, rr, sizeof(double), cudaMemcpyDeviceToHost, s));
-  HOFEM_CUDA(cudaStreamSynchronize(s));
+  HOFEM_TRY(d2h(m, &rr0, rr, sizeof(double), s));
 
   const unsigned vgrid = kDotBlocks;
   // Whole solve in one persistent cooperative kernel (§8(f) f1): single rank,
@@ -351,27 +364,19 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
                                     rel_tol, dres, s);
     if (st == HOFEM_OK) {
       int res[4] = {0, 0, 0, 0};
-      HOFEM_CUDA(cudaMemcpyAsync(res, dres, sizeof(res), cudaMemcpyDeviceToHost, s));
-      HOFEM_CUDA(cudaStreamSynchronize(s));
+      HOFEM_TRY(d2h(m, res, dres, sizeof(res), s));
       const int k = res[0];
       m->xseq += (unsigned long long)res[2];  // the kernel's exchanges / chain reductions
       m->rseq += (unsigned long long)res[3];
       double rr_last = rr0;
       // stream-ordered copies only: a legacy-stream cudaMemcpy could wait on
       // another loopback rank's spinning kernel
-      if (k > 0) {
-        HOFEM_CUDA(cudaMemcpyAsync(&rr_last, rr + k, sizeof(double), cudaMemcpyDeviceToHost, s));
-        HOFEM_CUDA(cudaStreamSynchronize(s));
-      }
+      if (k > 0) HOFEM_TRY(d2h(m, &rr_last, rr + k, sizeof(double), s));
       hofem_status status = HOFEM_OK;
       if (res[1]) status = HOFEM_ERR_BREAKDOWN;
       else if (!fixed_iters && !(rr_last == 0.0 || sqrt(rr_last) <= rel_tol * sqrt(rr0)))
         status = HOFEM_NOT_CONVERGED;
-      if (rr_history) {
-        HOFEM_CUDA(cudaMemcpyAsync(rr_history, rr, sizeof(double) * (k + 1),
-                                   cudaMemcpyDeviceToHost, s));
-        HOFEM_CUDA(cudaStreamSynchronize(s));
-      }
+      if (rr_history) HOFEM_TRY(d2h(m, rr_history, rr, sizeof(double) * (k + 1), s));
       if (stats) {
         stats->iterations = k;
         stats->converged = status == HOFEM_OK ? 1 : 0;
@@ -466,9 +471,8 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
     ++k;
     if ((!fixed_iters && k % check_every == 0) || k == max_iter) {
       double h[2];
-      HOFEM_CUDA(cudaMemcpyAsync(&h[0], rr + k, sizeof(double), cudaMemcpyDeviceToHost, s));
-      HOFEM_CUDA(cudaMemcpyAsync(&h[1], flag, sizeof(double), cudaMemcpyDeviceToHost, s));
-      HOFEM_CUDA(cudaStreamSynchronize(s));
+      HOFEM_TRY(d2h(m, &h[0], rr + k, sizeof(double), s));
+      HOFEM_TRY(d2h(m, &h[1], flag, sizeof(double), s));
       rr_last = h[0];
       if (h[1] != 0.0) { status = HOFEM_ERR_BREAKDOWN; break; }
       if (!fixed_iters && (rr_last == 0.0 || sqrt(rr_last) <= rel_tol * sqrt(rr0))) {
@@ -477,9 +481,7 @@ hofem_status cg_solve(Op* op, const double* b, double* x, double rel_tol, int ma
       }
     }
   }
-  if (rr_history) {
-    HOFEM_CUDA(cudaMemcpyAsync(rr_history, rr, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, s));
-  }
+  if (rr_history) HOFEM_TRY(d2h(m, rr_history, rr, sizeof(double) * (k + 1), s));
   HOFEM_CUDA(cudaStreamSynchronize(s));
   if (stats) {
     stats->iterations = k;

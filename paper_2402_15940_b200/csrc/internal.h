@@ -96,6 +96,10 @@ struct Mesh {
   bool peer_ipc[2] = {false, false};        // opened with cudaIpcOpenMemHandle
   unsigned long long xseq = 0;              // exchanges issued
   unsigned long long rseq = 0;              // in-kernel chain allreduces (persistent CG)
+  // pinned host staging for the library's device->host reads (dot results, CG
+  // scalars): a copy into pageable memory may wait on the whole device, which
+  // deadlocks against a loopback neighbour's spinning kernel
+  double* h_pin = nullptr;                  // kPinDoubles doubles (cudaHostAlloc)
 };
 
 // Grid-wide barrier state of a cooperative launch: arrival count and
@@ -193,6 +197,11 @@ hofem_status fill_random_range(unsigned long long seed, long long g0, long long 
 // ---- qdata / rhs (qdata.cu)
 hofem_status build_qdata(Op* op, cudaStream_t s, int* bad_host);
 hofem_status build_rhs(Op* op, double* b, cudaStream_t s);
+
+// Device -> host read of `bytes` through the mesh's pinned staging buffer
+// (chunked), ordered on stream s: synchronizes s only.
+constexpr int kPinDoubles = 512;
+hofem_status d2h(Mesh* m, void* dst, const void* src, size_t bytes, cudaStream_t s);
 
 // ---- operator apply paths
 hofem_status apply_unfused(Op* op, const double* x, double* y, cudaStream_t s);

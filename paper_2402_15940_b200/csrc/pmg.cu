@@ -311,9 +311,7 @@ double cheb_lo() { return 0.3; }
 
 hofem_status dot_host(Mesh* m, const double* a, const double* b, double* out, cudaStream_t s) {
   HOFEM_TRY(dot_device(m, a, b, m->d_scalars, s));
-  HOFEM_CUDA(cudaMemcpyAsync(out, m->d_scalars, sizeof(double), cudaMemcpyDeviceToHost, s));
-  HOFEM_CUDA(cudaStreamSynchronize(s));
-  return HOFEM_OK;
+  return d2h(m, out, m->d_scalars, sizeof(double), s);
 }
 
 XferGeo xgeo(const PMGLevel& f, const PMGLevel& c) {

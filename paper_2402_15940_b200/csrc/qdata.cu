@@ -184,8 +184,7 @@ hofem_status build_qdata(Op* op, cudaStream_t s, int* bad_host) {
                                                              op->d_G, dw, op->d_qdata, dbad);
     HOFEM_LAUNCHED();
   }
-  HOFEM_CUDA(cudaMemcpyAsync(bad_host, dbad, sizeof(int), cudaMemcpyDeviceToHost, s));
-  HOFEM_CUDA(cudaStreamSynchronize(s));
+  HOFEM_TRY(d2h(m, bad_host, dbad, sizeof(int), s));
   HOFEM_CUDA(cudaFreeAsync(dw, s));
   HOFEM_CUDA(cudaFreeAsync(dbad, s));
   return HOFEM_OK;

@@ -51,13 +51,26 @@ def run_ranks(hf, R, fn):
     for e in err:
         if e is not None:
             raise e
-    return out
+    # every rank synchronized its stream and left: host copies are safe now
+    return [to_host(o) for o in out]
 
 
 def host(t):
-    # stream-local copy (the current stream is the rank's): never a device-wide
-    # synchronization, which would wait on another rank's pending put kernel
-    return t.detach().cpu().numpy()
+    # Inside a rank's function results stay on the device: a copy into pageable
+    # host memory may wait on the whole device, i.e. on a neighbour's put kernel
+    # that spins until this rank's next exchange (deadlock).  run_ranks copies
+    # them to the host after every rank finished.
+    return t
+
+
+def to_host(o):
+    if isinstance(o, torch.Tensor):
+        return o.detach().cpu().numpy()
+    if isinstance(o, dict):
+        return {k: to_host(v) for k, v in o.items()}
+    if isinstance(o, (list, tuple)):
+        return type(o)(to_host(v) for v in o)
+    return o
 
 
 def rel(a, b):
