@@ -355,7 +355,8 @@ hofem_status hofem_op_fused_info(const void* op, hofem_fused_info* out);
  *  CG_PERSISTENT  hofem_cg runs the whole solve in ONE cooperative kernel (brick
  *                 pass, fix-up, p.Ap, updates, r.r, stop test, all behind grid
  *                 barriers; §2.3); a single rank, or several
- *                 ranks with the kernel-initiated exchange (mesh mode 1: the
+ *                 ranks with the kernel-initiated exchange (otherwise the
+ *                 per-iteration kernels run even with "always"; mesh mode 1: the
  *                 interface planes are put into the neighbours' slots and p.Ap /
  *                 r.r allreduced by a chain over the ranks inside the kernel,
  *                 PAPER.md:197); auto = <= 256 Ki local dofs (measured crossover).

@@ -299,3 +299,26 @@ def test_loopback_persistent_cg_in_kernel_exchange(hf, R, bench, p, dims):
         if r + 1 < R:  # duplicated interface plane: the same iterate on both ranks
             assert np.array_equal(res[r]["conv"][2][-plane:].view(np.uint64),
                                   res[r + 1]["conv"][2][:plane].view(np.uint64))
+
+
+def test_loopback_persistent_cg_needs_kernel_exchange(hf):
+    """Several ranks with the collective exchange (mode 0): the persistent CG
+    schedule needs mode 1's peer pointers, so forcing it runs the per-iteration
+    kernels instead -- bitwise the same iterate as asking for them."""
+    R, p, dims = 2, 2, (2, 2, 4)
+
+    def fn(r, comm, s):
+        m = hf.Mesh(*dims, p, alpha=0.1, comm=comm, stream=s)
+        op = hf.Operator(m, kind=hf.DIFFUSION, rule=hf.GAUSS, bc=1, stream=s)
+        b = op.rhs(stream=s)
+        xs = []
+        for mode in (hf.ALWAYS, hf.NEVER):
+            op.set_option(hf.OPT_CG_PERSISTENT, mode)
+            x = torch.zeros_like(b)
+            op.cg(b, x, max_iter=5, fixed_iters=True, stream=s)
+            xs.append(x)
+        s.synchronize()
+        return xs
+
+    for xa, xn in run_ranks(hf, R, fn):
+        assert np.array_equal(xa.view(np.uint64), xn.view(np.uint64))
